@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""PackSELL SpMV benchmark on B200 (BASELINE config 2 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step is one PackSELL SpMV over the configured matrix.  The matrix is generated
+and packed directly in HBM (rows row-partitioned in sigma-aligned slabs across
+ranks, x replicated, no collective on the data path).  Rank 0 prints one JSON
+line.  `value` = aggregate algorithmic GB/s (SURVEY.md §8d bytes: packed words +
+int64 slice offsets + perm + x once + y) over the max-over-ranks CUDA-event time
+of the K timed SpMVs with everything resident in HBM; `e2e` is the same metric
+through the public API `packsell_spmv(M, x_cpu_pinned, out=y_cpu_pinned)`, i.e.
+with the x H2D and y D2H copies inside the timed region.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port of packsell.packsell_spmv, oracle/) on the box's host cores,
+one worker process per core, each on its own sigma-aligned slab sample of the
+same matrix, and prints the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PackSELL SpMV GB/s (% HBM peak), GFLOP/s at 1-8 B200; mixed-prec PCG solve s"
+
+CONFIGS = {
+    "c2": dict(kind="stencil27", nx=256, preset="fp16", xdt="float16", scale=None, c=32, sigma=256,
+               mode="implicit",
+               workload="config 2: 27-point stencil 256^3 (HPCG_8_8_8), PackSELL fp16 (W=32, D=15), "
+                        "C=32, sigma=256, implicit perm; x, y f16; FP32 FMA accumulation"),
+    "c3": dict(kind="stencil27", nx=256, preset="e8m10", xdt="float32", scale="rowsum", c=32, sigma=256,
+               mode="implicit",
+               workload="config 3: 27-point stencil 256^3 row-sum scaled, PackSELL e8m10 (20-bit float, "
+                        "D=12), C=32, sigma=256, implicit; x, y f32"),
+    "c1": dict(kind="poisson2d", nx=512, preset="fp16", xdt="float16", scale=None, c=32, sigma=256,
+               mode="implicit",
+               workload="config 1: 5-point Laplacian 512^2, PackSELL fp16, C=32, sigma=256, implicit; x, y f16"),
+}
+
+
+def stencil_k_left(kind: str, nx: int) -> int:
+    """Lower bandwidth of the generated stencils (checked against the device in tests)."""
+    if kind == "stencil27":
+        return nx * nx + nx + 1
+    if kind == "poisson3d":
+        return nx * nx
+    return nx
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the SpMV kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu_id}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in getattr(self, "lines", []):
+            f = [t.strip() for t in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                                 f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU side
+def _cpu_worker(conn, cfg, r0, r1, k_left, seed):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import oracle as O
+    from paper_2604_13433_b200.stencil import stencil_rows
+    A = stencil_rows(cfg["kind"], cfg["nx"], r0, r1)
+    vals = A.values
+    if cfg["scale"] == "rowsum":
+        rows = np.repeat(np.arange(A.n_rows), A.row_lengths())
+        s = np.zeros(A.n_rows)
+        np.add.at(s, rows, np.abs(vals))
+        vals = vals / s[rows]
+    M = O.build(A.row_ptr, A.col_idx, vals, A.n_cols, cfg["c"], cfg["sigma"], O.preset(cfg["preset"]),
+                cfg["mode"], k_left=k_left, row0=r0)
+    xsz = np.dtype(cfg["xdt"]).itemsize
+    touched = int(A.col_idx.max()) - int(A.col_idx.min()) + 1 if A.nnz else 0
+    nbytes = O.spmv_bytes(M, xsz, xsz) - xsz * A.n_cols + xsz * touched
+    x = np.random.default_rng(seed).uniform(-1, 1, A.n_cols).astype(cfg["xdt"])
+    conn.send(("ready", nbytes, A.nnz))
+    while True:
+        msg = conn.recv()
+        if msg == "stop":
+            break
+        t0 = time.perf_counter()
+        O.spmv(M, x)
+        conn.send(time.perf_counter() - t0)
+
+
+def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: int):
+    """Oracle port of packsell_spmv on `workers` host cores, disjoint slab samples."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    n = cfg["nx"] ** (2 if cfg["kind"] == "poisson2d" else 3)
+    kl = stencil_k_left(cfg["kind"], cfg["nx"])
+    rows_per_worker = max(cfg["sigma"], rows_per_worker // cfg["sigma"] * cfg["sigma"])
+    workers = max(1, min(workers, n // rows_per_worker))
+    procs, conns = [], []
+    stride = (n // workers) // cfg["sigma"] * cfg["sigma"]
+    for w in range(workers):
+        a, b = mp.Pipe()
+        r0 = w * stride
+        p = ctx.Process(target=_cpu_worker, args=(b, cfg, r0, min(n, r0 + rows_per_worker), kl, 7 + w))
+        p.start()
+        procs.append(p)
+        conns.append(a)
+    tot_bytes, tot_nnz = 0, 0
+    for c in conns:
+        _, nb, nz = c.recv()
+        tot_bytes += nb
+        tot_nnz += nz
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        for c in conns:
+            c.send("go")
+        for c in conns:
+            c.recv()
+        if it >= warmup:
+            times.append(time.perf_counter() - t0)
+    for c in conns:
+        c.send("stop")
+    for p in procs:
+        p.join()
+    t = float(np.mean(times))
+    return dict(gbs=tot_bytes / t / 1e9, gflops=2 * tot_nnz / t / 1e9, sec_per_step=t, workers=workers,
+                rows=rows_per_worker, bytes=tot_bytes, nnz=tot_nnz)
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    r = cpu_reference(cfg, cores, args.ref_rows, args.steps, args.warmup)
+    sample = (f"{r['workers']} worker processes x {r['rows']} rows ({r['nnz']} nnz total) of the same matrix, "
+              f"sigma-aligned slabs, global k_left; oracle port of packsell_spmv (numpy, 1 thread each)")
+    line = {
+        "metric": METRIC, "value": r["gbs"], "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["sec_per_step"] * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16" if cfg["xdt"] == "float16" else "f32",
+        "data": "synthetic", "config": {"workload": cfg["workload"], "cpu_sample": sample},
+        "gflops": r["gflops"],
+        "cpu_baseline": {"value": r["gbs"], "unit": "GB/s", "cores": r["workers"], "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": r["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU side
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    import paper_2604_13433_b200 as P
+    from paper_2604_13433_b200.packed import lower_bandwidth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def allreduce(v, op):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op)
+        return t.item()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    nx = cfg["nx"]
+    n = nx ** (2 if cfg["kind"] == "poisson2d" else 3)
+    sig = cfg["sigma"]
+    nblk = -(-n // sig)
+    r0 = min(n, (nblk * rank // world) * sig)
+    r1 = min(n, (nblk * (rank + 1) // world) * sig)
+    fmt = P.parse_format(cfg["preset"])
+
+    t_b0 = time.perf_counter()
+    S = P.stencil_device(cfg["kind"], nx, scale=cfg["scale"], row_begin=r0, row_end=r1)
+    kl = int(allreduce(lower_bandwidth(S), dist.ReduceOp.MAX if world > 1 else None))
+    torch.cuda.synchronize()
+    t_b1 = time.perf_counter()
+    M = P.build_packsell(S, cfg["c"], sig, fmt, cfg["mode"], _k_left_override=kl)
+    torch.cuda.synchronize()
+    t_b2 = time.perf_counter()
+    cmin = int(S.col_idx.min().item()) if S.nnz else 0
+    cmax = int(S.col_idx.max().item()) if S.nnz else -1
+    nnz_local = S.nnz
+    del S
+    torch.cuda.empty_cache()
+
+    xt = getattr(torch, cfg["xdt"])
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    x = (torch.rand(n, generator=g, device=dev, dtype=torch.float32) * 2 - 1).to(xt)
+    y = torch.empty(M.n_rows, dtype=xt, device=dev)
+    xsz = x.element_size()
+    touched = n if world == 1 else (cmax - cmin + 1)
+    bytes_local = M.spmv_bytes(xsz, xsz, with_perm=True, x_elems=touched)
+    bytes_noperm = M.spmv_bytes(xsz, xsz, with_perm=False, x_elems=touched)
+    st = torch.cuda.current_stream()
+
+    for _ in range(max(3, args.warmup)):
+        P.packsell_spmv(M, x, out=y)
+    torch.cuda.synchronize()
+    # soak so the clock sampler sees the kernel under load around the timed region
+    gpu_uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    gpu_id = gpu_uuid if gpu_uuid.startswith("GPU-") else f"GPU-{gpu_uuid}"
+    sampler = ClockSampler(gpu_id)
+    with sampler:
+        t_end = time.perf_counter() + 1.0
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                P.packsell_spmv(M, x, out=y)
+            torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            P.packsell_spmv(M, x, out=y)
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        t_end = time.perf_counter() + 0.5
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                P.packsell_spmv(M, x, out=y)
+            torch.cuda.synchronize()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = allreduce(ms_local, dist.ReduceOp.MAX if world > 1 else None)
+    bytes_all = allreduce(float(bytes_local), dist.ReduceOp.SUM if world > 1 else None)
+    nnz_all = allreduce(float(nnz_local), dist.ReduceOp.SUM if world > 1 else None)
+    value = bytes_all / (ms * 1e-3) / 1e9
+    gflops = 2 * nnz_all / (ms * 1e-3) / 1e9
+
+    # e2e through the public API with host buffers (pinned), copies in the timed region
+    xh = x.cpu().pin_memory()
+    yh = torch.empty(M.n_rows, dtype=xt, pin_memory=True)
+    for _ in range(2):
+        P.packsell_spmv(M, xh, out=yh)
+    barrier()
+    torch.cuda.synchronize()
+    k_e2e = max(3, min(args.steps, 50))
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    f0.record(st)
+    for _ in range(k_e2e):
+        P.packsell_spmv(M, xh, out=yh)
+    f1.record(st)
+    torch.cuda.synchronize()
+    wall_e2e = (time.perf_counter() - w0) / k_e2e * 1e3
+    ms_e2e_local = max(f0.elapsed_time(f1) / k_e2e, wall_e2e)
+    ms_e2e = allreduce(ms_e2e_local, dist.ReduceOp.MAX if world > 1 else None)
+    e2e_value = bytes_all / (ms_e2e * 1e-3) / 1e9
+
+    peak, peak_kind = measured_peak()
+    achieved = bytes_local / (ms_local * 1e-3) / 1e9
+    clocks = sampler.summary()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference(cfg, 1, args.cpu_rows, 3, 1)
+        cpu = {"value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": f"{r['rows']} rows (rows 0..{r['rows'] - 1}, {r['nnz']} nnz) of the same matrix, "
+                         f"global k_left; oracle port of packsell_spmv, numpy single thread; "
+                         f"{r['gflops']:.4f} GFLOP/s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "n": n, "nnz": int(nnz_all),
+                       "n_stored_rank0": M.n_stored, "counts_rank0": list(M.counts), "k_left": kl,
+                       "partition": "sigma-aligned row slabs, x replicated (no collective in the step)",
+                       "l2": "inputs larger than L2: packed words stream at 1.94 GB per SpMV (126 MB L2); "
+                             "x (33.5 MB f16) is L2-resident by design and counted once"},
+            "pct_hbm_peak": value / (peak * world),
+            "gflops": gflops,
+            "bytes_per_step": int(bytes_all),
+            "bytes_per_step_without_perm": int(allreduce(float(bytes_noperm), dist.ReduceOp.SUM if world > 1 else None)),
+            "build_s": t_b2 - t_b1, "gen_s": t_b1 - t_b0,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                         "kernel": "spmv_c32_kernel (one launch per step)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
+                    "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+                    "d2h_bytes_per_step": int(yh.numel() * yh.element_size()),
+                    "api": "paper_2604_13433_b200.packsell_spmv(M, x_pinned_cpu, out=y_pinned_cpu)"},
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--ref-rows", type=int, default=131072, help="rows per CPU worker (reference arm)")
+    ap.add_argument("--cpu-rows", type=int, default=262144, help="rows of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,258 @@
+/*
+ * psell.h — C ABI of the B200-native PackSELL path (libpsell.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference package `packsell` 0.1.0
+ * (pure Python/numpy, /root/reference/pkg/src/packsell).  The reference has
+ * no FFI of its own; each entry point below replaces the numpy body of the
+ * reference function named beside it, and the Python mirror
+ * (paper_2604_13433_b200/*.py) binds them with ctypes exactly where the
+ * reference calls numpy.  See INTEGRATION.md for the bindings.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA
+ *    storage) unless the name ends in `_host`.  `stream` is a cudaStream_t
+ *    passed as void* (NULL = legacy default stream).
+ *  - Calls are stream ordered.  The library keeps no global mutable state
+ *    and allocates nothing persistent; scratch comes from a caller-owned
+ *    workspace sized by the matching *_workspace_bytes() call.
+ *  - Every call returns a psell_status; on failure *err is filled with the
+ *    reference's error payload (kind, first offending index, value) so the
+ *    host can raise the same exception class and message as the reference.
+ *  - Calls that must report data-dependent errors or sizes synchronise the
+ *    stream (build plan/fill, to_csr plan, encode); SpMV and the solver
+ *    kernels never synchronise and are CUDA-graph capturable.
+ */
+#ifndef PSELL_H
+#define PSELL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSELL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PSELL_API __attribute__((visibility("default")))
+#else
+#define PSELL_API
+#endif
+
+typedef enum psell_status {
+  PSELL_OK = 0,
+  PSELL_EVALUE = 1, /* -> ValueError (layout / parameter), packed.py:159-170, sell.py:33-42 */
+  PSELL_ECODEC = 2, /* -> CodecError(ValueError), codec.py:33-34,124-170 */
+  PSELL_ECUDA = 3,  /* CUDA runtime failure (message in err->msg) */
+  PSELL_EARG = 4    /* bad argument to the ABI itself (null pointer, small workspace) */
+} psell_status;
+
+typedef enum psell_err_kind {
+  PSELL_KIND_NONE = 0,
+  PSELL_KIND_FIRST_GAP = 1, /* row index, aux = its first column (packed.py:159-164) */
+  PSELL_KIND_GAP_RANGE = 2, /* any gap > 2^(W-1)-1 (packed.py:166-170) */
+  PSELL_KIND_NONFINITE = 3, /* value index, value (codec.py:124-127) */
+  PSELL_KIND_OVERFLOW = 4,  /* value index, value (codec.py:133-137,154-156,166-169) */
+  PSELL_KIND_PARAM = 5,
+  PSELL_KIND_CUDA = 6
+} psell_err_kind;
+
+typedef enum psell_codec { PSELL_FP16 = 0, PSELL_E8MY = 1, PSELL_FP32EMBED = 2 } psell_codec;
+typedef enum psell_mode { PSELL_MODE_NONE = 0, PSELL_MODE_EXPLICIT = 1, PSELL_MODE_IMPLICIT = 2 } psell_mode;
+typedef enum psell_dtype { PSELL_DT_F16 = 0, PSELL_DT_F32 = 1, PSELL_DT_F64 = 2 } psell_dtype;
+
+/* psell_spmv flags */
+#define PSELL_SPMV_REF_ORDER 1 /* numpy rounding order: value cast to x dtype, product and sum rounded separately */
+
+typedef struct psell_error {
+  int32_t code;  /* psell_status */
+  int32_t kind;  /* psell_err_kind */
+  int64_t index; /* first offending row / value position (reference semantics) */
+  int64_t aux;   /* e.g. the offending first column */
+  double value;  /* offending value for codec errors */
+  char msg[256];
+} psell_error;
+
+/*
+ * One descriptor serves build and SpMV.  Mirrors PackFormat (codec.py:37-44)
+ * plus the layout arguments of build_packsell (packed.py:176-178) and the
+ * scalar fields of PackSellMatrix (packed.py:83-100).
+ *
+ * Multi-GPU slabs: a rank owns global rows [row0, row0 + n_rows); row0 must be
+ * sigma-aligned (C-aligned in mode none).  Base offsets use the global row
+ * index and the global k_left, so the concatenation of slab packs over ranks
+ * is byte-identical to the single-GPU pack.
+ */
+typedef struct psell_desc {
+  int32_t w, d, codec;    /* word bits (32|64), delta bits, psell_codec */
+  int32_t c, sigma, mode; /* slice height C, sorting window sigma, psell_mode */
+  int64_t n_rows;         /* rows of this slab */
+  int64_t n_cols;         /* global number of columns */
+  int64_t row0;           /* global index of local row 0 */
+  int64_t k_left;         /* build: < 0 => compute (matrix.py:319-349); spmv: the matrix's k_left */
+  int64_t nnz;            /* build: CSR nnz of the slab */
+} psell_desc;
+
+PSELL_API const char* psell_version(void);
+PSELL_API int32_t psell_abi_version(void);
+
+/* ---- K1: CSR -> PackSELL builder (replaces build_packsell, packed.py:176-239) ---- */
+
+PSELL_API size_t psell_build_workspace_bytes(const psell_desc* desc);
+
+/* Local lower bandwidth max(0, max_i(row0+i - first_col_i)) (matrix.py:334-339);
+ * ranks all-reduce MAX of this to get the global k_left.  Synchronises. */
+PSELL_API int psell_lower_bandwidth(const psell_desc* desc, const int64_t* row_ptr, const int32_t* col_idx,
+                          void* workspace, size_t ws_bytes, int64_t* k_left_host, void* stream,
+                          psell_error* err);
+
+/* Plan: k_left (unless desc->k_left >= 0), per-row stored counts with dummy
+ * words (packed.py:145-173), stable descending sigma-block sort (sell.py:22-30),
+ * slice widths and the int64 slice offsets (packed.py:208-215), perm
+ * (packed.py:233-235).  offset has n_slices+1 entries (n_slices = ceil(n_rows/C)),
+ * perm has n_rows entries of 1 byte (sigma<=256) or 2 bytes, NULL unless mode
+ * implicit.  out_host receives {k_left, n_stored, n_dummy}.  Synchronises. */
+PSELL_API int psell_build_plan(const psell_desc* desc, const int64_t* row_ptr, const int32_t* col_idx,
+                     void* workspace, size_t ws_bytes, int64_t* offset, void* perm,
+                     int64_t* out_host, void* stream, psell_error* err);
+
+/* Fill: writes every word of pack (offset[n_slices] words of W bits: real,
+ * dummy and all-zero padding) (packed.py:218-231) and validates the codec
+ * (non-finite first, then overflow; minimum position).  desc->k_left must be
+ * the value the plan returned.  Synchronises. */
+PSELL_API int psell_build_fill(const psell_desc* desc, const int64_t* row_ptr, const int32_t* col_idx,
+                     const double* values, const void* workspace, size_t ws_bytes,
+                     const int64_t* offset, void* pack, void* stream, psell_error* err);
+
+/* Stable descending order of counts inside sigma blocks (sell.py:22-30):
+ * order[i] = global (0-based) row stored at position i.  counts are uint32. */
+PSELL_API size_t psell_sort_workspace_bytes(int64_t n, int32_t sigma);
+PSELL_API int psell_sort_order(const uint32_t* counts, int64_t n, int32_t sigma, int32_t* order,
+                               void* workspace, size_t ws_bytes, void* stream, psell_error* err);
+
+/* ---- K2: PackSELL SpMV (replaces packsell_spmv, packed.py:242-271) ----
+ * y[out(s)] = sum_q value(q) * x[cursor(q)] for every storage row s < n_rows,
+ * cursor starting at min(d_s, n_cols-1).  y has x's dtype.  Default: FP32 FMA
+ * accumulation (FP64 for f64 x); PSELL_SPMV_REF_ORDER reproduces numpy's
+ * rounding bit for bit.  x is the GLOBAL vector (n_cols entries). */
+PSELL_API int psell_spmv(const psell_desc* desc, const void* pack, const int64_t* offset, const void* perm,
+               const void* x, int32_t x_dtype, void* y, int32_t flags, void* stream,
+               psell_error* err);
+
+/* Number of double partials psell_spmv_dot writes (one per CTA). */
+PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc);
+
+/* SpMV fused with the PCG curvature dot: also writes partials[b] =
+ * sum over the CTA's rows of (double)p_own[i] * (double)y[i] (solvers.py:294-295),
+ * p_own = the slab's own rows of the direction vector.  f32 x/y only.  If
+ * skip_flag != NULL and *skip_flag != 0 the kernel does nothing (breakdown). */
+PSELL_API int psell_spmv_dot(const psell_desc* desc, const void* pack, const int64_t* offset,
+                   const void* perm, const float* x, float* y, const float* p_own,
+                   double* partials, const int32_t* skip_flag, void* stream, psell_error* err);
+
+/* ---- K5: PackSELL -> CSR decode (replaces packsell_to_csr, packed.py:274-303) ---- */
+PSELL_API size_t psell_to_csr_workspace_bytes(const psell_desc* desc);
+/* Writes row_ptr (n_rows+1, logical row order) and returns nnz in *nnz_host. Synchronises. */
+PSELL_API int psell_to_csr_plan(const psell_desc* desc, const void* pack, const int64_t* offset,
+                      const void* perm, void* workspace, size_t ws_bytes, int64_t* row_ptr,
+                      int64_t* nnz_host, void* stream, psell_error* err);
+PSELL_API int psell_to_csr_fill(const psell_desc* desc, const void* pack, const int64_t* offset,
+                      const void* perm, const int64_t* row_ptr, int32_t* col_idx, double* values,
+                      void* stream, psell_error* err);
+
+/* ---- value codecs on device (replace codec.py:173-250) ---- */
+/* patterns: uint32 (W=32) or uint64 (W=64).  Synchronises (error check). */
+PSELL_API int psell_encode(const psell_desc* fmt, const double* values, int64_t n, void* patterns,
+                 void* workspace16, void* stream, psell_error* err);
+/* values out: float16 (fp16 codec) or float32 */
+PSELL_API int psell_decode(const psell_desc* fmt, const void* patterns, int64_t n, void* values,
+                 void* stream, psell_error* err);
+PSELL_API int psell_pack_words(const psell_desc* fmt, const void* patterns, const int64_t* deltas,
+                     const uint8_t* flags, int64_t n, void* words, void* stream, psell_error* err);
+/* deltas out as uint64; values out float16 (fp16) or float32 */
+PSELL_API int psell_unpack_words(const psell_desc* fmt, const void* words, int64_t n, void* values,
+                       uint64_t* deltas, uint8_t* flags, void* stream, psell_error* err);
+
+/* ---- K4: CSR SpMV in the reference's row-sequential order (matrix.py:272-291) ----
+ * values are f64; converted to x's dtype per element, every product and sum
+ * rounded in that dtype.  Rows [0, n_rows) of the slab, x global. */
+PSELL_API int psell_csr_spmv(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                   const double* values, const void* x, int32_t x_dtype, void* y, void* stream,
+                   psell_error* err);
+
+/* ---- K3: solver vector kernels (solvers.py:87-93,171-308) ----
+ * Reductions are deterministic: fixed-grid partials summed in a fixed tree.
+ * Device scalar blocks (double* scal, int32_t* iflags) are described in
+ * paper_2604_13433_b200/solvers.py. */
+#define PSELL_RED_BLOCKS 592 /* 4 x 148 SMs */
+
+/* out[k] = sum_b partials[k * n_partials + b] for k < n_out (fixed order) */
+PSELL_API int psell_sum_partials(const double* partials, int64_t n_partials, int32_t n_out, double* out,
+                       const int32_t* skip_flag, void* stream);
+
+/* Generic f64 dots: out = {a.b}; a, b of dtype (f32|f64); PSELL_RED_BLOCKS partials. */
+PSELL_API int psell_dot(const void* a, const void* b, int32_t dtype, int64_t n, double* partials,
+              double* out, void* stream);
+
+/* Inner reduced-precision PCG (solvers.py:278-308), f32 vectors.
+ * scal[0]=rz scal[1]=pq scal[2]=alpha scal[3]=beta scal[4]=rz_new  scal[8..] local sums
+ * iflags[0]=breakdown iflags[1]=done */
+PSELL_API int psell_ipcg_begin(int64_t n, const double* r64, float* x, float* r, float* z, float* p,
+                     const float* inv_diag, double* partials, double* local_out, void* stream);
+PSELL_API int psell_ipcg_set_rz(const double* parts, int32_t n_parts, double* scal, int32_t* iflags,
+                      void* stream);
+PSELL_API int psell_ipcg_alpha(const double* parts, int32_t n_parts, double* scal, int32_t* iflags,
+                     void* stream);
+PSELL_API int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
+                      const float* inv_diag, const double* scal, const int32_t* iflags,
+                      double* partials, double* local_out, void* stream);
+PSELL_API int psell_ipcg_beta(const double* parts, int32_t n_parts, double* scal, int32_t* iflags,
+                    void* stream);
+PSELL_API int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal,
+                         const int32_t* iflags, void* stream);
+PSELL_API int psell_ipcg_end(int64_t n, const float* x, double* z64, void* stream);
+
+/* Outer FCG / PCG f64 helpers (solvers.py:171-275).
+ * fcg_zr:  out2 = {z.(r - r_prev), z.r}  (r_prev may be NULL: first iteration)
+ * pq_pr:   out2 = {p.q, p.r}
+ * axpy2:   x += a*p; r -= a*q with a = coef[0] (numpy rounding), out1 = {r.r}
+ * xpby:    p = z + b*p with b = coef[0]; if coef == NULL: p = z
+ * resid:   out1 = {(b - ax).(b - ax)} */
+PSELL_API int psell_fcg_zr(int64_t n, const double* z, const double* r, const double* r_prev,
+                 double* partials, double* out2, void* stream);
+PSELL_API int psell_pq_pr(int64_t n, const double* p, const double* q, const double* r, double* partials,
+                double* out2, void* stream);
+PSELL_API int psell_axpy2(int64_t n, double* x, double* r, const double* p, const double* q,
+                const double* coef, const int32_t* skip_flag, double* partials, double* out1,
+                void* stream);
+PSELL_API int psell_xpby(int64_t n, double* p, const double* z, const double* coef, void* stream);
+PSELL_API int psell_resid(int64_t n, const double* b, const double* ax, double* partials, double* out1,
+                void* stream);
+/* z = r * inv (f64 Jacobi) and rz partial: out1 = {r.z} */
+PSELL_API int psell_precond_dot(int64_t n, double* z, const double* r, const double* inv, double* partials,
+                      double* out1, void* stream);
+/* scalar programs on device: alpha = num/den with breakdown test, beta = num/den */
+PSELL_API int psell_scalar_div(const double* num_parts, const double* den_parts, int32_t n_parts,
+                     int32_t stride, double* dst, int32_t* flag, int32_t check_curvature,
+                     void* stream);
+
+/* ---- synthetic stencil generators (device) for the BASELINE configs ----
+ * Grid d0 x d1 x d2 (d0 slowest), rows [row_begin, row_end) of the matrix.
+ * box = 1: 27-point (HPCG, diag = 26), box = 0: star (2*ndim+1 point, diag 2*ndim).
+ * scale: 0 none, 1 sym_diag_scale (matrix.py:305-316), 2 row_sum_scale (294-302).
+ * Bitwise equal to reference stencil.py:10-52 + the scaling on the host. */
+PSELL_API size_t psell_gen_workspace_bytes(int64_t n_rows);
+PSELL_API int psell_gen_stencil_plan(int64_t d0, int64_t d1, int64_t d2, int32_t box, double diag,
+                                     int64_t row_begin, int64_t row_end, void* workspace,
+                                     size_t ws_bytes, int64_t* row_ptr, int64_t* nnz_host,
+                                     void* stream, psell_error* err);
+PSELL_API int psell_gen_stencil_fill(int64_t d0, int64_t d1, int64_t d2, int32_t box, double diag,
+                                     int32_t scale, int64_t row_begin, int64_t row_end,
+                                     const int64_t* row_ptr, int32_t* col_idx, double* values,
+                                     void* stream, psell_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSELL_H */

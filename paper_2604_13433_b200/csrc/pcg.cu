@@ -1,0 +1,403 @@
+// K3 — solver vector kernels with deterministic FP64 reductions.
+//
+// Replaces the numpy vector algebra of pcg / fcg / _inner_pcg (reference
+// solvers.py:171-308) and _dot/_norm (87-93).  All reductions go through
+// fixed-grid partials (one per CTA, grid-stride over a fixed grid of
+// PSELL_RED_BLOCKS CTAs) summed by one CTA in a fixed tree, so results are
+// bit-reproducible run to run (SPEC determinism, test_acceptance c09).  Across
+// ranks each rank's local sum is gathered and summed in rank order by the
+// scalar kernels (n_parts > 1).  Scalars (alpha, beta, rz, the breakdown flag,
+// the done counter) never leave the device: the inner loop is launch-only and
+// CUDA-graph capturable.  Vector updates reproduce numpy's rounding: the
+// Python-float coefficient is rounded to the vector dtype, then a separately
+// rounded product and sum (no FMA contraction).
+#include "psell_internal.cuh"
+
+namespace psell {
+
+constexpr int kRB = PSELL_RED_BLOCKS;
+
+__global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __restrict__ parts,
+                                                            long long np, int n_out,
+                                                            double* __restrict__ out,
+                                                            const int32_t* skip) {
+  if (skip && *skip) return;
+  __shared__ double sh[32];
+  for (int k = 0; k < n_out; ++k) {
+    double v = 0.0;
+    for (long long i = threadIdx.x; i < np; i += 1024) v += parts[k * np + i];
+    const double t = block_sum<1024>(v, sh);
+    if (threadIdx.x == 0) out[k] = t;
+  }
+}
+
+static int finalize(const double* parts, long long np, int n_out, double* out, const int32_t* skip,
+                    cudaStream_t st) {
+  sum_partials_kernel<<<1, 1024, 0, st>>>(parts, np, n_out, out, skip);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) dot_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                     long long n, double* __restrict__ parts) {
+  __shared__ double sh[kBlock / 32];
+  double v = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock)
+    v += (double)a[i] * (double)b[i];
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+// ---------------------------------------------------------------- inner PCG (f32)
+// solvers.py:286-291: b = r.astype(f32); x = 0; r = b; z = P(r); p = z; rz = r.z
+__global__ void __launch_bounds__(kBlock) ipcg_begin_kernel(long long n, const double* __restrict__ r64,
+                                                            float* __restrict__ x, float* r, float* z,
+                                                            float* __restrict__ p,
+                                                            const float* __restrict__ inv,
+                                                            double* __restrict__ parts) {
+  __shared__ double sh[kBlock / 32];
+  double v = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    const float rf = __double2float_rn(r64[i]);
+    x[i] = 0.f;
+    r[i] = rf;
+    float zf = rf;
+    if (inv) {
+      zf = __fmul_rn(rf, inv[i]);
+      z[i] = zf;
+    }
+    p[i] = zf;
+    v += (double)rf * (double)zf;
+  }
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+// scal: [0]=rz [1]=pq [2]=alpha [3]=beta [4]=rz_new ; iflags: [0]=breakdown [1]=done
+__global__ void ipcg_set_rz_kernel(const double* parts, int np, double* scal, int32_t* iflags) {
+  double s = 0.0;
+  for (int i = 0; i < np; ++i) s += parts[i];
+  scal[0] = s;
+  iflags[0] = 0;
+  iflags[1] = 0;
+}
+
+// solvers.py:295-299
+__global__ void ipcg_alpha_kernel(const double* parts, int np, double* scal, int32_t* iflags) {
+  if (iflags[0]) return;
+  double pq = 0.0;
+  for (int i = 0; i < np; ++i) pq += parts[i];
+  scal[1] = pq;
+  if (pq <= 0.0 || !isfinite(pq) || scal[0] == 0.0) {
+    iflags[0] = 1;
+    return;
+  }
+  scal[2] = scal[0] / pq;
+}
+
+// solvers.py:300-304: x += a p; r -= a q; z = P(r); rz_new partials
+__global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float* __restrict__ x, float* r,
+                                                             float* z, const float* __restrict__ p,
+                                                             const float* __restrict__ q,
+                                                             const float* __restrict__ inv,
+                                                             const double* __restrict__ scal,
+                                                             const int32_t* __restrict__ iflags,
+                                                             double* __restrict__ parts) {
+  if (iflags[0]) return;
+  __shared__ double sh[kBlock / 32];
+  const float a = __double2float_rn(scal[2]);
+  double v = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    x[i] = __fadd_rn(x[i], __fmul_rn(a, p[i]));
+    const float rn = __fsub_rn(r[i], __fmul_rn(a, q[i]));
+    r[i] = rn;
+    float zf = rn;
+    if (inv) {
+      zf = __fmul_rn(rn, inv[i]);
+      z[i] = zf;
+    }
+    v += (double)rn * (double)zf;
+  }
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+// solvers.py:304-306
+__global__ void ipcg_beta_kernel(const double* parts, int np, double* scal, int32_t* iflags) {
+  if (iflags[0]) return;
+  double s = 0.0;
+  for (int i = 0; i < np; ++i) s += parts[i];
+  scal[4] = s;
+  scal[3] = s / scal[0];
+  scal[0] = s;
+  iflags[1] += 1;
+}
+
+// solvers.py:307: p = z + beta p
+__global__ void __launch_bounds__(kBlock) ipcg_direction_kernel(long long n, float* __restrict__ p,
+                                                                const float* __restrict__ z,
+                                                                const double* __restrict__ scal,
+                                                                const int32_t* __restrict__ iflags) {
+  if (iflags[0]) return;
+  const float b = __double2float_rn(scal[3]);
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock)
+    p[i] = __fadd_rn(z[i], __fmul_rn(b, p[i]));
+}
+
+__global__ void __launch_bounds__(kBlock) ipcg_end_kernel(long long n, const float* __restrict__ x,
+                                                          double* __restrict__ z64) {
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock)
+    z64[i] = (double)x[i];
+}
+
+// ---------------------------------------------------------------- outer f64
+// solvers.py:254,256: {z.(r - r_prev), z.r}
+__global__ void __launch_bounds__(kBlock) fcg_zr_kernel(long long n, const double* __restrict__ z,
+                                                        const double* __restrict__ r,
+                                                        const double* __restrict__ rp,
+                                                        double* __restrict__ parts) {
+  __shared__ double sh[kBlock / 32];
+  double v0 = 0.0, v1 = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    const double zi = z[i], ri = r[i];
+    if (rp) v0 += __dmul_rn(zi, __dsub_rn(ri, rp[i]));
+    v1 += __dmul_rn(zi, ri);
+  }
+  v0 = block_sum<kBlock>(v0, sh);
+  v1 = block_sum<kBlock>(v1, sh);
+  if (threadIdx.x == 0) {
+    parts[blockIdx.x] = v0;
+    parts[kRB + blockIdx.x] = v1;
+  }
+}
+
+// solvers.py:259,263: {p.q, p.r}
+__global__ void __launch_bounds__(kBlock) pq_pr_kernel(long long n, const double* __restrict__ p,
+                                                       const double* __restrict__ q,
+                                                       const double* __restrict__ r,
+                                                       double* __restrict__ parts) {
+  __shared__ double sh[kBlock / 32];
+  double v0 = 0.0, v1 = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    const double pi = p[i];
+    v0 += __dmul_rn(pi, q[i]);
+    if (r) v1 += __dmul_rn(pi, r[i]);
+  }
+  v0 = block_sum<kBlock>(v0, sh);
+  v1 = block_sum<kBlock>(v1, sh);
+  if (threadIdx.x == 0) {
+    parts[blockIdx.x] = v0;
+    parts[kRB + blockIdx.x] = v1;
+  }
+}
+
+// solvers.py:201-204 / 264-267: x += a p; r -= a q; {r.r}
+__global__ void __launch_bounds__(kBlock) axpy2_kernel(long long n, double* __restrict__ x,
+                                                       double* __restrict__ r,
+                                                       const double* __restrict__ p,
+                                                       const double* __restrict__ q,
+                                                       const double* __restrict__ coef,
+                                                       const int32_t* skip,
+                                                       double* __restrict__ parts) {
+  if (skip && *skip) return;
+  __shared__ double sh[kBlock / 32];
+  const double a = coef[0];
+  double v = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
+    const double rn = __dsub_rn(r[i], __dmul_rn(a, q[i]));
+    r[i] = rn;
+    v += __dmul_rn(rn, rn);
+  }
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+// p = z + b p  (solvers.py:209,255); coef == NULL -> p = z (252)
+__global__ void __launch_bounds__(kBlock) xpby_kernel(long long n, double* __restrict__ p,
+                                                      const double* __restrict__ z,
+                                                      const double* __restrict__ coef) {
+  const bool first = coef == nullptr;
+  const double b = first ? 0.0 : coef[0];
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock)
+    p[i] = first ? z[i] : __dadd_rn(z[i], __dmul_rn(b, p[i]));
+}
+
+// solvers.py:162-163: {(b - Ax).(b - Ax)}
+__global__ void __launch_bounds__(kBlock) resid_kernel(long long n, const double* __restrict__ b,
+                                                       const double* __restrict__ ax,
+                                                       double* __restrict__ parts) {
+  __shared__ double sh[kBlock / 32];
+  double v = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    const double d = __dsub_rn(b[i], ax[i]);
+    v += __dmul_rn(d, d);
+  }
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+// Jacobi z = r * inv (solvers.py:148-149), {r.z}
+__global__ void __launch_bounds__(kBlock) precond_dot_kernel(long long n, double* __restrict__ z,
+                                                             const double* __restrict__ r,
+                                                             const double* __restrict__ inv,
+                                                             double* __restrict__ parts) {
+  __shared__ double sh[kBlock / 32];
+  double v = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+    const double ri = r[i];
+    const double zi = inv ? __dmul_rn(ri, inv[i]) : ri;
+    if (inv) z[i] = zi;
+    v += __dmul_rn(ri, zi);
+  }
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+__global__ void scalar_div_kernel(const double* num, const double* den, int np, int stride,
+                                  double* dst, int32_t* flag, int check) {
+  if (flag && *flag) return;
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < np; ++i) {
+    a += num[(long long)i * stride];
+    b += den[(long long)i * stride];
+  }
+  dst[1] = b;
+  if (check && (b <= 0.0 || !isfinite(b))) {
+    if (flag) *flag = 1;
+    return;
+  }
+  dst[0] = a / b;
+}
+
+static unsigned vgrid(long long n) {
+  long long g = ceil_div(n, kBlock);
+  if (g > kRB) g = kRB;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace psell
+
+using namespace psell;
+
+#define LAUNCH_OK() (cudaGetLastError() == cudaSuccess ? PSELL_OK : PSELL_ECUDA)
+
+extern "C" {
+
+int psell_sum_partials(const double* partials, int64_t n_partials, int32_t n_out, double* out,
+                       const int32_t* skip_flag, void* stream) {
+  sum_partials_kernel<<<1, 1024, 0, as_stream(stream)>>>(partials, n_partials, n_out, out, skip_flag);
+  return LAUNCH_OK();
+}
+
+int psell_dot(const void* a, const void* b, int32_t dtype, int64_t n, double* partials, double* out,
+              void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (dtype == PSELL_DT_F64)
+    dot_kernel<double><<<kRB, kBlock, 0, st>>>(static_cast<const double*>(a), static_cast<const double*>(b), n, partials);
+  else if (dtype == PSELL_DT_F32)
+    dot_kernel<float><<<kRB, kBlock, 0, st>>>(static_cast<const float*>(a), static_cast<const float*>(b), n, partials);
+  else
+    return PSELL_EARG;
+  finalize(partials, kRB, 1, out, nullptr, st);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_begin(int64_t n, const double* r64, float* x, float* r, float* z, float* p,
+                     const float* inv_diag, double* partials, double* local_out, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  ipcg_begin_kernel<<<kRB, kBlock, 0, st>>>(n, r64, x, r, z, p, inv_diag, partials);
+  finalize(partials, kRB, 1, local_out, nullptr, st);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_set_rz(const double* parts, int32_t n_parts, double* scal, int32_t* iflags, void* stream) {
+  ipcg_set_rz_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, scal, iflags);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_alpha(const double* parts, int32_t n_parts, double* scal, int32_t* iflags, void* stream) {
+  ipcg_alpha_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, scal, iflags);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
+                      const float* inv_diag, const double* scal, const int32_t* iflags,
+                      double* partials, double* local_out, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  ipcg_update_kernel<<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials);
+  finalize(partials, kRB, 1, local_out, iflags, st);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_beta(const double* parts, int32_t n_parts, double* scal, int32_t* iflags, void* stream) {
+  ipcg_beta_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, scal, iflags);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal,
+                         const int32_t* iflags, void* stream) {
+  ipcg_direction_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, scal, iflags);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_end(int64_t n, const float* x, double* z64, void* stream) {
+  ipcg_end_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, x, z64);
+  return LAUNCH_OK();
+}
+
+int psell_fcg_zr(int64_t n, const double* z, const double* r, const double* r_prev,
+                 double* partials, double* out2, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  fcg_zr_kernel<<<kRB, kBlock, 0, st>>>(n, z, r, r_prev, partials);
+  finalize(partials, kRB, 2, out2, nullptr, st);
+  return LAUNCH_OK();
+}
+
+int psell_pq_pr(int64_t n, const double* p, const double* q, const double* r, double* partials,
+                double* out2, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  pq_pr_kernel<<<kRB, kBlock, 0, st>>>(n, p, q, r, partials);
+  finalize(partials, kRB, 2, out2, nullptr, st);
+  return LAUNCH_OK();
+}
+
+int psell_axpy2(int64_t n, double* x, double* r, const double* p, const double* q,
+                const double* coef, const int32_t* skip_flag, double* partials, double* out1,
+                void* stream) {
+  cudaStream_t st = as_stream(stream);
+  axpy2_kernel<<<kRB, kBlock, 0, st>>>(n, x, r, p, q, coef, skip_flag, partials);
+  finalize(partials, kRB, 1, out1, skip_flag, st);
+  return LAUNCH_OK();
+}
+
+int psell_xpby(int64_t n, double* p, const double* z, const double* coef, void* stream) {
+  xpby_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, coef);
+  return LAUNCH_OK();
+}
+
+int psell_resid(int64_t n, const double* b, const double* ax, double* partials, double* out1,
+                void* stream) {
+  cudaStream_t st = as_stream(stream);
+  resid_kernel<<<kRB, kBlock, 0, st>>>(n, b, ax, partials);
+  finalize(partials, kRB, 1, out1, nullptr, st);
+  return LAUNCH_OK();
+}
+
+int psell_precond_dot(int64_t n, double* z, const double* r, const double* inv, double* partials,
+                      double* out1, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  precond_dot_kernel<<<kRB, kBlock, 0, st>>>(n, z, r, inv, partials);
+  finalize(partials, kRB, 1, out1, nullptr, st);
+  return LAUNCH_OK();
+}
+
+int psell_scalar_div(const double* num_parts, const double* den_parts, int32_t n_parts,
+                     int32_t stride, double* dst, int32_t* flag, int32_t check_curvature,
+                     void* stream) {
+  scalar_div_kernel<<<1, 1, 0, as_stream(stream)>>>(num_parts, den_parts, n_parts, stride, dst,
+                                                    flag, check_curvature);
+  return LAUNCH_OK();
+}
+
+}  // extern "C"

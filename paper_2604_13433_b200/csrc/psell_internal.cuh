@@ -1,0 +1,221 @@
+// Internal helpers shared by the libpsell translation units (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/psell.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libpsell is built for sm_100a only"
+#endif
+
+namespace psell {
+
+constexpr int kBlock = 256;
+
+// ---------------------------------------------------------------- errors
+inline int set_err(psell_error* e, int code, int kind, int64_t index, int64_t aux, double value,
+                   const char* msg) {
+  if (e) {
+    e->code = code;
+    e->kind = kind;
+    e->index = index;
+    e->aux = aux;
+    e->value = value;
+    snprintf(e->msg, sizeof(e->msg), "%s", msg ? msg : "");
+  }
+  return code;
+}
+
+inline int ok(psell_error* e) { return set_err(e, PSELL_OK, PSELL_KIND_NONE, -1, 0, 0.0, ""); }
+
+inline int cuda_err(psell_error* e, cudaError_t st, const char* where) {
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(st));
+  return set_err(e, PSELL_ECUDA, PSELL_KIND_CUDA, -1, 0, 0.0, buf);
+}
+
+#define PSELL_CHECK_LAUNCH(err, where)                         \
+  do {                                                         \
+    cudaError_t _st = cudaGetLastError();                      \
+    if (_st != cudaSuccess) return ::psell::cuda_err(err, _st, where); \
+  } while (0)
+
+#define PSELL_CUDA(call, err)                                  \
+  do {                                                         \
+    cudaError_t _st = (call);                                  \
+    if (_st != cudaSuccess) return ::psell::cuda_err(err, _st, #call); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- format
+struct Fmt {
+  int w, d, codec;
+  __host__ __device__ int v() const { return w - d - 1; }
+};
+
+inline Fmt fmt_of(const psell_desc* d) { return Fmt{d->w, d->d, d->codec}; }
+
+// codec.py:45-62 (host-side re-validation at the ABI boundary)
+inline bool fmt_valid(const Fmt& f) {
+  if (f.w != 32 && f.w != 64) return false;
+  if (f.d < 1 || f.d > f.w - 2) return false;
+  int v = f.w - f.d - 1;
+  if (f.codec == PSELL_FP16) return v == 16;
+  if (f.codec == PSELL_E8MY) return f.w == 32 && v - 9 >= 1;
+  if (f.codec == PSELL_FP32EMBED) return f.w == 64 && v >= 32;
+  return false;
+}
+
+// ---------------------------------------------------------------- encode
+// Error codes of the per-value encoders.
+enum { ENC_OK = 0, ENC_NONFINITE = 1, ENC_OVERFLOW = 2 };
+
+// f64 -> IEEE half, direct round-to-nearest-even (codec.py:130-138).
+// __double2half lowers to cvt.rn.f16.f64 on sm_100a (no f32 double rounding).
+__device__ __forceinline__ uint32_t enc_fp16(double v, int& st) {
+  if (!isfinite(v)) { st = ENC_NONFINITE; return 0u; }
+  unsigned short b = __half_as_ushort(__double2half(v));
+  if ((b & 0x7FFFu) == 0x7C00u) st = ENC_OVERFLOW;
+  return (uint32_t)b;
+}
+
+// e8my: f64 -> f32 RNE, subnormal flush to signed zero, then round half away
+// from zero at mantissa bit D on the integer form, inf => overflow
+// (codec.py:141-160; integer form verified in SURVEY.md App. A.2).
+__device__ __forceinline__ uint32_t enc_e8my(double v, int d, int& st) {
+  if (!isfinite(v)) { st = ENC_NONFINITE; return 0u; }
+  uint32_t b = __float_as_uint(__double2float_rn(v));
+  uint32_t sign = b & 0x80000000u;
+  uint32_t mag = b & 0x7FFFFFFFu;
+  uint32_t r = 0u;
+  if (mag >= 0x00800000u) {
+    r = (mag + (1u << d)) & ~((2u << d) - 1u);
+    if (r >= 0x7F800000u) st = ENC_OVERFLOW;
+  }
+  return (sign | r) >> (d + 1);
+}
+
+// fp32embed: f32 bits << (V - 32) (codec.py:163-170).
+__device__ __forceinline__ uint64_t enc_fp32(double v, int vbits, int& st) {
+  if (!isfinite(v)) { st = ENC_NONFINITE; return 0ull; }
+  float f = __double2float_rn(v);
+  if (isinf(f)) st = ENC_OVERFLOW;
+  return ((uint64_t)__float_as_uint(f)) << (vbits - 32);
+}
+
+__device__ __forceinline__ uint64_t encode_value(const Fmt& f, double v, int& st) {
+  if (f.codec == PSELL_FP16) return enc_fp16(v, st);
+  if (f.codec == PSELL_E8MY) return enc_e8my(v, f.d, st);
+  return enc_fp32(v, f.v(), st);
+}
+
+// ---------------------------------------------------------------- decode
+// Branch-free unpack (codec.py:227-250).  Flag in bit 0, delta above it.
+template <typename W>
+__device__ __forceinline__ W unpack_delta(W w, int d) {
+  const W flag = w & W(1);
+  const W mask = flag ? ((W(1) << d) - W(1)) : ~W(0);
+  return (w >> 1) & mask;
+}
+
+// value bits of an e8my word as f32 (0 for flag == 0)
+__device__ __forceinline__ float e8my_value(uint32_t w, int d) {
+  uint32_t keep = (w & 1u) ? ~((2u << d) - 1u) : 0u;
+  return __uint_as_float(w & keep);
+}
+
+__device__ __forceinline__ __half fp16_value(uint32_t w) {
+  return __ushort_as_half((unsigned short)((w & 1u) ? (w >> 16) : 0u));
+}
+
+__device__ __forceinline__ float fp32e_value(uint64_t w) {
+  return __uint_as_float((w & 1ull) ? (uint32_t)(w >> 32) : 0u);
+}
+
+// ---------------------------------------------------------------- loads
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// streaming (read-once) 32/64-bit loads: no L1 allocation, L2 evict-first
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
+               : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// gathered (reused) loads of x: read-only path, L2 evict-last
+__device__ __forceinline__ unsigned short ld_keep_u16(const unsigned short* p, uint64_t pol) {
+  unsigned short v;
+  asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_keep(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ __half ld_keep(const __half* p, uint64_t pol) {
+  return __ushort_as_half(ld_keep_u16(reinterpret_cast<const unsigned short*>(p), pol));
+}
+
+// ---------------------------------------------------------------- reductions
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic CTA sum (fixed tree); result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh /* NT/32 */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = (lane < NT / 32) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;
+}
+
+}  // namespace psell
+
+namespace psell {
+// out[0] = 0, out[i+1] = in[0] + ... + in[i]   (build.cu); tmp >= ceil(n/4096)+1 longs
+int scan_i64(const long long* in, long long n, long long* tmp, long long* out, cudaStream_t st,
+             psell_error* err);
+}  // namespace psell

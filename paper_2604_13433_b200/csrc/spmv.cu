@@ -1,0 +1,437 @@
+// K2 — PackSELL SpMV and K5 — PackSELL -> CSR decode, sm_100a.
+//
+// Replaces packsell_spmv (reference packed.py:242-271), unpack_words
+// (codec.py:227-250) and packsell_to_csr (packed.py:274-303).
+//
+// Mapping (one thread per row): thread <-> storage row.
+// For C = 32 a warp owns one slice, so step q of all 32 lanes is one
+// contiguous 128 B line of `pack` (column-major slices, packed.py:224).  The
+// fast kernel streams those lines with L1::no_allocate + L2 evict_first
+// loads, U steps per batch, double buffered in registers so 2U lines per warp
+// are in flight; it decodes branch-free (flag/delta/value with SEL+LOP), runs
+// the column cursor as a 32-bit register prefix, gathers x through the
+// read-only path with an L2 evict_last policy (x stays L2 resident while the
+// 2 GB pack streams past it) and accumulates with FP32 FMA.  REF_ORDER
+// switches to numpy's rounding (value cast to x dtype, separately rounded
+// product and sum) for bitwise parity.  Generic C uses the same thread/row
+// mapping without the warp-uniform fast path.
+#include "psell_internal.cuh"
+
+namespace psell {
+
+struct SpmvArgs {
+  const void* pack;
+  const int64_t* offset;
+  const void* perm;
+  const void* x;
+  void* y;
+  const float* p_own;
+  double* partials;
+  const int32_t* skip;
+  long long n_rows, n_cols, n_slices, row0, k_left;
+  int c, se, sigma, mode, d, perm_bytes;
+};
+
+template <int CODEC> struct WordOf { using T = uint32_t; };
+template <> struct WordOf<PSELL_FP32EMBED> { using T = uint64_t; };
+
+// ---- value decode: returns the value as f32 (exact for every codec) and,
+//      for REF mode with half x, the value rounded to half.
+template <int CODEC, typename W>
+__device__ __forceinline__ float word_value(W w, int d) {
+  if constexpr (CODEC == PSELL_FP16) return __half2float(fp16_value((uint32_t)w));
+  else if constexpr (CODEC == PSELL_E8MY) return e8my_value((uint32_t)w, d);
+  else return fp32e_value((uint64_t)w);
+}
+
+template <int CODEC, typename W>
+__device__ __forceinline__ __half word_value_h(W w, int d) {
+  if constexpr (CODEC == PSELL_FP16) return fp16_value((uint32_t)w);
+  else return __float2half_rn(word_value<CODEC, W>(w, d));
+}
+
+template <int CODEC>
+__device__ __forceinline__ int word_dbits(int d) {
+  if constexpr (CODEC == PSELL_FP16) return 15;
+  else return d;
+}
+
+// Accumulator policy.  REF: numpy order in the x dtype.  Fast: FP32 FMA (FP64 for f64 x).
+template <typename XT, bool REF> struct Acc;
+template <> struct Acc<__half, true> {
+  using T = __half;
+  __device__ static T zero() { return __ushort_as_half(0); }
+  template <int CODEC, typename W>
+  __device__ static T step(T acc, W w, int d, __half xv) {
+    return __hadd_rn(acc, __hmul_rn(word_value_h<CODEC, W>(w, d), xv));
+  }
+  __device__ static __half out(T a) { return a; }
+  __device__ static float as_f(T a) { return __half2float(a); }
+};
+template <> struct Acc<__half, false> {
+  using T = float;
+  __device__ static T zero() { return 0.f; }
+  template <int CODEC, typename W>
+  __device__ static T step(T acc, W w, int d, __half xv) {
+    return fmaf(word_value<CODEC, W>(w, d), __half2float(xv), acc);
+  }
+  __device__ static __half out(T a) { return __float2half_rn(a); }
+};
+template <> struct Acc<float, true> {
+  using T = float;
+  __device__ static T zero() { return 0.f; }
+  template <int CODEC, typename W>
+  __device__ static T step(T acc, W w, int d, float xv) {
+    return __fadd_rn(acc, __fmul_rn(word_value<CODEC, W>(w, d), xv));
+  }
+  __device__ static float out(T a) { return a; }
+};
+template <> struct Acc<float, false> {
+  using T = float;
+  __device__ static T zero() { return 0.f; }
+  template <int CODEC, typename W>
+  __device__ static T step(T acc, W w, int d, float xv) {
+    return fmaf(word_value<CODEC, W>(w, d), xv, acc);
+  }
+  __device__ static float out(T a) { return a; }
+};
+template <> struct Acc<double, true> {
+  using T = double;
+  __device__ static T zero() { return 0.0; }
+  template <int CODEC, typename W>
+  __device__ static T step(T acc, W w, int d, double xv) {
+    return __dadd_rn(acc, __dmul_rn((double)word_value<CODEC, W>(w, d), xv));
+  }
+  __device__ static double out(T a) { return a; }
+};
+template <> struct Acc<double, false> {
+  using T = double;
+  __device__ static T zero() { return 0.0; }
+  template <int CODEC, typename W>
+  __device__ static T step(T acc, W w, int d, double xv) {
+    return fma((double)word_value<CODEC, W>(w, d), xv, acc);
+  }
+  __device__ static double out(T a) { return a; }
+};
+
+template <typename XT> __device__ __forceinline__ float to_f(XT v);
+template <> __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<double>(double v) { return (float)v; }
+
+__device__ __forceinline__ long long storage_base(long long s_global, int se, long long k_left,
+                                                  long long n_cols) {
+  const long long blk = (s_global / se) * se;
+  long long d = blk > k_left ? blk - k_left : 0;
+  const long long cmax = n_cols > 0 ? n_cols - 1 : 0;
+  return d < cmax ? d : cmax;
+}
+
+__device__ __forceinline__ long long out_row(const SpmvArgs& a, long long s) {
+  if (a.mode != PSELL_MODE_IMPLICIT) return s;
+  const long long blk = (s / a.sigma) * a.sigma;
+  const int p = a.perm_bytes == 1 ? (int)static_cast<const uint8_t*>(a.perm)[s]
+                                  : (int)static_cast<const uint16_t*>(a.perm)[s];
+  return blk + p;
+}
+
+template <bool DOT>
+__device__ __forceinline__ void finish_dot(const SpmvArgs& a, double v) {
+  if constexpr (DOT) {
+    __shared__ double sh[kBlock / 32];
+    const double t = block_sum<kBlock>(v, sh);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
+  }
+}
+
+// ---- fast path: C == 32, warp == slice
+template <int CODEC, typename XT, bool REF, bool DOT, int U>
+__global__ void __launch_bounds__(kBlock) spmv_c32_kernel(const SpmvArgs a) {
+  using W = typename WordOf<CODEC>::T;
+  using A = Acc<XT, REF>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long k = s >> 5;
+  const int lane = threadIdx.x & 31;
+  double dotv = 0.0;
+  if (k < a.n_slices) {
+    const long long o0 = a.offset[k];
+    const int width = (int)((a.offset[k + 1] - o0) >> 5);
+    const W* p = static_cast<const W*>(a.pack) + o0 + lane;
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint64_t pol_s = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int dbits = word_dbits<CODEC>(a.d);
+    int cursor = (int)storage_base(a.row0 + s, a.se, a.k_left, a.n_cols);
+    typename A::T acc = A::zero();
+    W cur[U], nxt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = (u < width) ? ld_stream(p + u * 32, pol_s) : W(0);
+    for (int q = 0; q < width; q += U) {
+      const W* pn = p + (q + U) * 32;
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = (q + U + u < width) ? ld_stream(pn + u * 32, pol_s) : W(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cursor += (int)unpack_delta<W>(cur[u], dbits);
+        const XT xv = ld_keep(x + cursor, pol_x);
+        acc = A::template step<CODEC, W>(acc, cur[u], a.d, xv);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
+    if (s < a.n_rows) {
+      const long long o = out_row(a, s);
+      const XT yv = A::out(acc);
+      static_cast<XT*>(a.y)[o] = yv;
+      if constexpr (DOT) dotv = (double)a.p_own[o] * (double)to_f<XT>(yv);
+    }
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
+// ---- generic C: thread per storage row, slice k = s / C
+template <int CODEC, typename XT, bool REF, bool DOT>
+__global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const SpmvArgs a) {
+  using W = typename WordOf<CODEC>::T;
+  using A = Acc<XT, REF>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  double dotv = 0.0;
+  if (s < a.n_rows) {
+    const long long k = s / a.c;
+    const long long lane = s - k * a.c;
+    const long long o0 = a.offset[k];
+    const long long width = (a.offset[k + 1] - o0) / a.c;
+    const W* p = static_cast<const W*>(a.pack) + o0 + lane;
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint64_t pol_x = policy_evict_last();
+    const int dbits = word_dbits<CODEC>(a.d);
+    long long cursor = storage_base(a.row0 + s, a.se, a.k_left, a.n_cols);
+    typename A::T acc = A::zero();
+    for (long long q = 0; q < width; ++q) {
+      const W w = p[q * a.c];
+      cursor += (long long)unpack_delta<W>(w, dbits);
+      const XT xv = ld_keep(x + cursor, pol_x);
+      acc = A::template step<CODEC, W>(acc, w, a.d, xv);
+    }
+    const long long o = out_row(a, s);
+    const XT yv = A::out(acc);
+    static_cast<XT*>(a.y)[o] = yv;
+    if constexpr (DOT) dotv = (double)a.p_own[o] * (double)to_f<XT>(yv);
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
+template <int CODEC, typename XT, bool REF, bool DOT>
+static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
+  if (a.c == 32) {
+    const long long rows = a.n_slices * 32;
+    const unsigned grid = (unsigned)ceil_div(rows, kBlock);
+    constexpr int U = sizeof(typename WordOf<CODEC>::T) == 4 ? 8 : 4;
+    spmv_c32_kernel<CODEC, XT, REF, DOT, U><<<grid, kBlock, 0, st>>>(a);
+  } else {
+    const unsigned grid = (unsigned)ceil_div(a.n_rows, kBlock);
+    spmv_generic_kernel<CODEC, XT, REF, DOT><<<grid, kBlock, 0, st>>>(a);
+  }
+}
+
+template <int CODEC, typename XT>
+static void dispatch_ref(const SpmvArgs& a, bool ref, cudaStream_t st) {
+  if (ref) launch_spmv<CODEC, XT, true, false>(a, st);
+  else launch_spmv<CODEC, XT, false, false>(a, st);
+}
+
+template <int CODEC>
+static int dispatch_x(const SpmvArgs& a, int xdt, bool ref, cudaStream_t st) {
+  switch (xdt) {
+    case PSELL_DT_F16: dispatch_ref<CODEC, __half>(a, ref, st); return 0;
+    case PSELL_DT_F32: dispatch_ref<CODEC, float>(a, ref, st); return 0;
+    case PSELL_DT_F64: dispatch_ref<CODEC, double>(a, ref, st); return 0;
+  }
+  return 1;
+}
+
+static int make_args(const psell_desc* d, const void* pack, const int64_t* offset,
+                     const void* perm, SpmvArgs& a, psell_error* err) {
+  if (!d) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null descriptor");
+  if (!fmt_valid(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid PackFormat");
+  if (d->c < 1) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid C");
+  if (d->mode == PSELL_MODE_IMPLICIT && (!perm || d->sigma < 1))
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "implicit mode needs perm");
+  if (d->n_cols >= (1ll << 31) || d->n_rows >= (1ll << 31))
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "dimensions exceed 32-bit indexing");
+  a.pack = pack;
+  a.offset = offset;
+  a.perm = perm;
+  a.x = nullptr;
+  a.y = nullptr;
+  a.p_own = nullptr;
+  a.partials = nullptr;
+  a.skip = nullptr;
+  a.n_rows = d->n_rows;
+  a.n_cols = d->n_cols;
+  a.n_slices = ceil_div(d->n_rows, d->c);
+  a.row0 = d->row0;
+  a.k_left = d->k_left < 0 ? 0 : d->k_left;
+  a.c = d->c;
+  a.se = d->mode == PSELL_MODE_NONE ? 1 : d->sigma;
+  a.sigma = d->sigma;
+  a.mode = d->mode;
+  a.d = d->d;
+  a.perm_bytes = d->sigma <= 256 ? 1 : 2;
+  return PSELL_OK;
+}
+
+// ---------------------------------------------------------------- K5 decode
+__device__ __forceinline__ long long raw_base(long long s_global, int se, long long k_left) {
+  const long long blk = (s_global / se) * se;
+  return blk > k_left ? blk - k_left : 0;
+}
+
+template <typename W>
+__global__ void to_csr_count_kernel(const SpmvArgs a, long long* __restrict__ counts) {
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (s >= a.n_rows) return;
+  const long long k = s / a.c, lane = s - k * a.c;
+  const long long o0 = a.offset[k];
+  const long long width = (a.offset[k + 1] - o0) / a.c;
+  const W* p = static_cast<const W*>(a.pack) + o0 + lane;
+  long long cnt = 0;
+  for (long long q = 0; q < width; ++q) cnt += (long long)(p[q * a.c] & W(1));
+  counts[out_row(a, s)] = cnt;
+}
+
+template <int CODEC>
+__global__ void to_csr_fill_kernel(const SpmvArgs a, const int64_t* __restrict__ row_ptr,
+                                   int32_t* __restrict__ col_idx, double* __restrict__ values) {
+  using W = typename WordOf<CODEC>::T;
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (s >= a.n_rows) return;
+  const long long k = s / a.c, lane = s - k * a.c;
+  const long long o0 = a.offset[k];
+  const long long width = (a.offset[k + 1] - o0) / a.c;
+  const W* p = static_cast<const W*>(a.pack) + o0 + lane;
+  const int dbits = word_dbits<CODEC>(a.d);
+  long long cursor = raw_base(a.row0 + s, a.se, a.k_left);  // unclamped (packed.py:285-288)
+  long long t = row_ptr[out_row(a, s)];
+  for (long long q = 0; q < width; ++q) {
+    const W w = p[q * a.c];
+    cursor += (long long)unpack_delta<W>(w, dbits);
+    if (w & W(1)) {
+      col_idx[t] = (int32_t)cursor;
+      values[t] = (double)word_value<CODEC, W>(w, a.d);
+      ++t;
+    }
+  }
+}
+
+}  // namespace psell
+
+using namespace psell;
+
+extern "C" {
+
+int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
+               const void* x, int32_t x_dtype, void* y, int32_t flags, void* stream,
+               psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  a.x = x;
+  a.y = y;
+  if (a.n_rows == 0) return ok(err);
+  cudaStream_t st = as_stream(stream);
+  const bool ref = (flags & PSELL_SPMV_REF_ORDER) != 0;
+  int bad = 1;
+  switch (d->codec) {
+    case PSELL_FP16: bad = dispatch_x<PSELL_FP16>(a, x_dtype, ref, st); break;
+    case PSELL_E8MY: bad = dispatch_x<PSELL_E8MY>(a, x_dtype, ref, st); break;
+    case PSELL_FP32EMBED: bad = dispatch_x<PSELL_FP32EMBED>(a, x_dtype, ref, st); break;
+  }
+  if (bad) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "unsupported x dtype");
+  PSELL_CHECK_LAUNCH(err, "psell_spmv");
+  return ok(err);
+}
+
+int64_t psell_spmv_dot_partials(const psell_desc* d) {
+  if (!d || d->n_rows <= 0 || d->c < 1) return 1;
+  if (d->c == 32) return ceil_div(ceil_div(d->n_rows, 32) * 32, kBlock);
+  return ceil_div(d->n_rows, kBlock);
+}
+
+int psell_spmv_dot(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
+                   const float* x, float* y, const float* p_own, double* partials,
+                   const int32_t* skip_flag, void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  a.x = x;
+  a.y = y;
+  a.p_own = p_own;
+  a.partials = partials;
+  a.skip = skip_flag;
+  cudaStream_t st = as_stream(stream);
+  if (a.n_rows == 0) {
+    PSELL_CUDA(cudaMemsetAsync(partials, 0, sizeof(double), st), err);
+    return ok(err);
+  }
+  switch (d->codec) {
+    case PSELL_FP16: launch_spmv<PSELL_FP16, float, false, true>(a, st); break;
+    case PSELL_E8MY: launch_spmv<PSELL_E8MY, float, false, true>(a, st); break;
+    case PSELL_FP32EMBED: launch_spmv<PSELL_FP32EMBED, float, false, true>(a, st); break;
+  }
+  PSELL_CHECK_LAUNCH(err, "psell_spmv_dot");
+  return ok(err);
+}
+
+size_t psell_to_csr_workspace_bytes(const psell_desc* d) {
+  if (!d) return 0;
+  const long long n = d->n_rows > 0 ? d->n_rows : 0;
+  return align_up(8 * (size_t)n) + align_up(8 * (size_t)(ceil_div(n, 4096) + 4096 + 1));
+}
+
+int psell_to_csr_plan(const psell_desc* d, const void* pack, const int64_t* offset,
+                      const void* perm, void* ws, size_t ws_bytes, int64_t* row_ptr,
+                      int64_t* nnz_host, void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  if (ws_bytes < psell_to_csr_workspace_bytes(d) || !ws)
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  long long* counts = static_cast<long long*>(ws);
+  long long* tmp = reinterpret_cast<long long*>(static_cast<char*>(ws) + align_up(8 * (size_t)a.n_rows));
+  if (a.n_rows > 0) {
+    const unsigned grid = (unsigned)ceil_div(a.n_rows, kBlock);
+    if (d->w == 32) to_csr_count_kernel<uint32_t><<<grid, kBlock, 0, st>>>(a, counts);
+    else to_csr_count_kernel<uint64_t><<<grid, kBlock, 0, st>>>(a, counts);
+    PSELL_CHECK_LAUNCH(err, "to_csr_count");
+  }
+  if (int rc = scan_i64(counts, a.n_rows, tmp, reinterpret_cast<long long*>(row_ptr), st, err)) return rc;
+  long long nnz = 0;
+  PSELL_CUDA(cudaMemcpyAsync(&nnz, row_ptr + a.n_rows, 8, cudaMemcpyDeviceToHost, st), err);
+  PSELL_CUDA(cudaStreamSynchronize(st), err);
+  *nnz_host = nnz;
+  return ok(err);
+}
+
+int psell_to_csr_fill(const psell_desc* d, const void* pack, const int64_t* offset,
+                      const void* perm, const int64_t* row_ptr, int32_t* col_idx, double* values,
+                      void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  if (a.n_rows == 0) return ok(err);
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = (unsigned)ceil_div(a.n_rows, kBlock);
+  switch (d->codec) {
+    case PSELL_FP16: to_csr_fill_kernel<PSELL_FP16><<<grid, kBlock, 0, st>>>(a, row_ptr, col_idx, values); break;
+    case PSELL_E8MY: to_csr_fill_kernel<PSELL_E8MY><<<grid, kBlock, 0, st>>>(a, row_ptr, col_idx, values); break;
+    default: to_csr_fill_kernel<PSELL_FP32EMBED><<<grid, kBlock, 0, st>>>(a, row_ptr, col_idx, values); break;
+  }
+  PSELL_CHECK_LAUNCH(err, "to_csr_fill");
+  return ok(err);
+}
+
+}  // extern "C"

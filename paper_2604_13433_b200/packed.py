@@ -1,0 +1,365 @@
+"""PackSELL format: builder, SpMV, decode — drop-in for reference `packsell.packed`.
+
+Same names and signatures as the reference (packed.py:23-327).  The matrix
+lives in HBM; `build_packsell` runs the K1 CUDA pipeline (psell_build_plan +
+psell_build_fill), `packsell_spmv` the K2 kernel, `packsell_to_csr` the K5
+decode.  `PackSellMatrix` exposes the reference's numpy fields (`pack`,
+`offset`, `perm` with the reference dtypes) as lazily downloaded, cached
+host copies so reference-style tests and the .psell container keep working,
+and accepts host arrays in its constructor (uploaded once).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import NamedTuple, Optional
+
+import numpy as np
+
+from . import codec
+from .matrix import CsrMatrix, DeviceCsrMatrix
+from .sell import _check_layout_params, perm_dtype
+
+MODES = ("none", "explicit", "implicit")
+
+
+class DeltaEntry(NamedTuple):
+    delta: int
+    value: Optional[float]  # None marks a dummy word
+
+
+class StorageCounts(NamedTuple):
+    nnz_real: int
+    n_dummy: int
+    n_padding: int
+
+
+class FootprintReport(NamedTuple):
+    pack_bits: int
+    sell_equiv_bits: int
+    ratio: float
+
+
+def leftmost_offset(i: int, sigma: int, k_left: int) -> int:
+    """Eq. 4 base column of row i (packed.py:40-47)."""
+    start = (i // sigma) * sigma
+    return start - k_left if k_left < start else 0
+
+
+def _leftmost_offsets(n: int, sigma: int, k_left: int, row0: int = 0) -> np.ndarray:
+    start = ((np.arange(n, dtype=np.int64) + row0) // sigma) * sigma
+    return np.where(k_left < start, start - k_left, 0)
+
+
+def build_delta_stream(row_cols, row_vals, d_i: int, fmt: codec.PackFormat) -> list:
+    """Per-row delta stream with dummy insertion (packed.py:55-80), scalar test helper."""
+    cols = [int(c) for c in row_cols]
+    if cols and cols[0] < d_i:
+        raise ValueError(
+            f"first column {cols[0]} is left of the row base offset {d_i}; "
+            "the lower bandwidth used to derive the offset is inconsistent"
+        )
+    out: list = []
+    prev = d_i
+    for col, val in zip(cols, row_vals):
+        gap = col - prev
+        if gap >= 1 << fmt.d:
+            while gap > fmt.max_dummy_delta:
+                out.append(DeltaEntry(fmt.max_dummy_delta, None))
+                gap -= fmt.max_dummy_delta
+            out.append(DeltaEntry(gap, None))
+            gap = 0
+        out.append(DeltaEntry(gap, float(val)))
+        prev = col
+    return out
+
+
+def _is_tensor(a) -> bool:
+    try:
+        import torch
+        return isinstance(a, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+class PackSellMatrix:
+    """HBM-resident packed words + slice offsets + perm + bandwidth metadata (packed.py:83-142).
+
+    `pack`, `offset`, `perm` are host numpy views (downloaded on first access);
+    `d_pack`, `d_offset`, `d_perm` are the device tensors the kernels read.
+    `row0` is the global index of local storage row 0 for a rank's slab.
+    """
+
+    def __init__(self, n_rows, n_cols, c, sigma, mode, fmt, pack, offset,
+                 perm=None, k_left=0, counts=StorageCounts(0, 0, 0), *, row0: int = 0):
+        from . import _dev
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.c = int(c)
+        self.sigma = int(sigma)
+        self.mode = mode
+        self.fmt = fmt
+        self.k_left = int(k_left)
+        self.counts = StorageCounts(*counts)
+        self.row0 = int(row0)
+        self._h = {}
+        if _is_tensor(pack):
+            self.d_pack = pack
+        else:
+            p = np.asarray(pack, dtype=fmt.word_dtype)
+            self._h["pack"] = p
+            self.d_pack = _dev.upload(p)
+        if _is_tensor(offset):
+            self.d_offset = offset
+        else:
+            o = np.asarray(offset, dtype=np.int64)
+            self._h["offset"] = o
+            self.d_offset = _dev.upload(o)
+        self._perm_dtype = None
+        if perm is None:
+            self.d_perm = None
+            self._h["perm"] = None
+        elif _is_tensor(perm):
+            self.d_perm = perm
+            self._perm_dtype = perm_dtype(self.sigma)
+        else:
+            pp = np.asarray(perm)
+            self._h["perm"] = pp
+            self._perm_dtype = pp.dtype
+            self.d_perm = _dev.upload(pp.astype(perm_dtype(self.sigma)))
+        self._out_idx = None
+        self._n_stored = int(self.d_pack.numel())
+        self._n_slices = int(self.d_offset.numel()) - 1
+
+    # -- reference numpy fields (lazy host copies)
+    @property
+    def pack(self) -> np.ndarray:
+        if "pack" not in self._h:
+            from . import _dev
+            self._h["pack"] = _dev.download(self.d_pack, self.fmt.word_dtype)
+        return self._h["pack"]
+
+    @property
+    def offset(self) -> np.ndarray:
+        if "offset" not in self._h:
+            from . import _dev
+            self._h["offset"] = _dev.download(self.d_offset, np.int64)
+        return self._h["offset"]
+
+    @property
+    def perm(self) -> Optional[np.ndarray]:
+        if "perm" not in self._h:
+            from . import _dev
+            self._h["perm"] = _dev.download(self.d_perm, self._perm_dtype)
+        return self._h["perm"]
+
+    @property
+    def n_slices(self) -> int:
+        return self._n_slices
+
+    @property
+    def n_stored(self) -> int:
+        return self._n_stored
+
+    @property
+    def effective_sigma(self) -> int:
+        return 1 if self.mode == "none" else self.sigma
+
+    def output_index(self) -> np.ndarray:
+        """Original row of each storage row (packed.py:128-136)."""
+        if self._out_idx is None:
+            s = np.arange(self.n_rows, dtype=np.int64)
+            if self.mode == "implicit":
+                self._out_idx = (s // self.sigma) * self.sigma + self.perm[:self.n_rows].astype(np.int64)
+            else:
+                self._out_idx = s
+        return self._out_idx
+
+    def storage_base_offsets(self) -> np.ndarray:
+        """Block-uniform base offsets per storage row (packed.py:138-142)."""
+        return _leftmost_offsets(self.n_slices * self.c, self.effective_sigma, self.k_left, self.row0)
+
+    # -- device side
+    def desc(self):
+        from . import _lib
+        d = _lib.PsellDesc()
+        d.w, d.d, d.codec = self.fmt.w, self.fmt.d, _lib.CODEC_IDS[self.fmt.codec]
+        d.c, d.sigma, d.mode = self.c, self.sigma, _lib.MODE_IDS[self.mode]
+        d.n_rows, d.n_cols, d.row0 = self.n_rows, self.n_cols, self.row0
+        d.k_left, d.nnz = self.k_left, self.counts.nnz_real
+        return d
+
+    def spmv_bytes(self, x_itemsize: int, y_itemsize: Optional[int] = None, with_perm: bool = True,
+                   x_elems: Optional[int] = None) -> int:
+        """Algorithmic bytes of one SpMV: words + slice offsets + x once + y (+ perm)."""
+        y_itemsize = x_itemsize if y_itemsize is None else y_itemsize
+        b = (self.fmt.w // 8) * self.n_stored + 8 * (self.n_slices + 1)
+        b += x_itemsize * (self.n_cols if x_elems is None else x_elems) + y_itemsize * self.n_rows
+        if with_perm and self.mode == "implicit":
+            b += np.dtype(perm_dtype(self.sigma)).itemsize * self.n_rows
+        return int(b)
+
+
+def lower_bandwidth(A, c: int = 32, sigma: int = 256, mode: str = "implicit") -> int:
+    """Device k_left of a (slab) CSR: max(0, max_i(row0 + i - first_col_i)) (matrix.py:334-339).
+
+    Ranks of a row-partitioned build all-reduce MAX of this value and pass it
+    as `_k_left_override` so every slab uses the global lower bandwidth.
+    """
+    from . import _dev, _lib
+    lib = _lib.lib()
+    D = A.to_device()
+    d = _lib.PsellDesc()
+    d.w, d.d, d.codec = 32, 15, 0
+    d.c, d.sigma, d.mode = int(c), int(sigma), _lib.MODE_IDS[mode]
+    d.n_rows, d.n_cols, d.row0, d.k_left, d.nnz = D.n_rows, D.n_cols, D.row0, -1, D.nnz
+    ws = _dev.workspace(lib.psell_build_workspace_bytes(d))
+    out = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    rc = lib.psell_lower_bandwidth(d, _lib.ptr(D.row_ptr), _lib.ptr(D.col_idx), _lib.ptr(ws), ws.numel(),
+                                   ctypes.byref(out), _lib.stream_handle(), err)
+    _lib.check(rc, err)
+    return int(out.value)
+
+
+def build_packsell(A, c: int = 32, sigma: int = 256,
+                   fmt: codec.PackFormat = codec.PackFormat(),
+                   mode: str = "implicit", _k_left_override: Optional[int] = None) -> PackSellMatrix:
+    """CSR -> PackSELL on the GPU (packed.py:176-239), byte-identical to the reference.
+
+    `A` is a CsrMatrix (uploaded once and cached on the matrix) or a
+    DeviceCsrMatrix (used in place; a rank slab when its row0 > 0, in which
+    case pass the global k_left as `_k_left_override`).
+    """
+    from . import _dev, _lib
+    _check_layout_params(c, sigma, mode)
+    lib = _lib.lib()
+    D = A.to_device()
+    if _k_left_override is not None and int(_k_left_override) < 0:
+        raise ValueError("negative k_left override is not supported")
+    d = _lib.PsellDesc()
+    d.w, d.d, d.codec = fmt.w, fmt.d, _lib.CODEC_IDS[fmt.codec]
+    d.c, d.sigma, d.mode = int(c), int(sigma), _lib.MODE_IDS[mode]
+    d.n_rows, d.n_cols, d.row0 = D.n_rows, D.n_cols, D.row0
+    d.k_left = -1 if _k_left_override is None else int(_k_left_override)
+    d.nnz = D.nnz
+    ws = _dev.workspace(lib.psell_build_workspace_bytes(d))
+    n_slices = -(-D.n_rows // int(c))
+    offset = _dev.empty(n_slices + 1, np.int64)
+    perm = _dev.empty(D.n_rows, perm_dtype(sigma)) if mode == "implicit" else None
+    out = (ctypes.c_int64 * 3)()
+    err = _lib.PsellError()
+    st = _lib.stream_handle()
+    rc = lib.psell_build_plan(d, _lib.ptr(D.row_ptr), _lib.ptr(D.col_idx), _lib.ptr(ws), ws.numel(),
+                              _lib.ptr(offset), _lib.ptr(perm), out, st, err)
+    _lib.check(rc, err, fmt)
+    k_left, n_stored, n_dummy = int(out[0]), int(out[1]), int(out[2])
+    d.k_left = k_left
+    pack = _dev.empty(n_stored, fmt.word_dtype)
+    rc = lib.psell_build_fill(d, _lib.ptr(D.row_ptr), _lib.ptr(D.col_idx), _lib.ptr(D.values),
+                              _lib.ptr(ws), ws.numel(), _lib.ptr(offset), _lib.ptr(pack), st, err)
+    _lib.check(rc, err, fmt)
+    nnz = D.nnz
+    counts = StorageCounts(nnz, n_dummy, n_stored - nnz - n_dummy)
+    return PackSellMatrix(D.n_rows, D.n_cols, c, sigma, mode, fmt, pack, offset, perm, k_left,
+                          counts, row0=D.row0)
+
+
+def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool):
+    from . import _dev, _lib
+    lib = _lib.lib()
+    err = _lib.PsellError()
+    rc = lib.psell_spmv(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                        _lib.ptr(xd), _dev.T_DT_CODE[xd.dtype], _lib.ptr(y),
+                        _lib.SPMV_REF_ORDER if ref_order else 0, _lib.stream_handle(), err)
+    _lib.check(rc, err, M.fmt)
+    return y
+
+
+def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None):
+    """y = M x with on-the-fly unpacking (packed.py:242-271), y in x's dtype.
+
+    x: numpy array (returns numpy, the reference call), CUDA tensor (returns a
+    CUDA tensor, no host traffic), or CPU tensor (ideally pinned; copied in,
+    result copied back into `out` or a new CPU tensor, stream synchronised).
+    Accumulation is FP32 FMA (FP64 for f64 x); `ref_order=True` reproduces the
+    reference's numpy rounding bit for bit.
+    """
+    import torch
+    from . import _dev
+    if _is_tensor(x):
+        if len(x) != M.n_cols:
+            raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
+        if x.dtype not in _dev.T_DT_CODE:
+            raise TypeError(f"unsupported x dtype {x.dtype}")
+        if x.is_cuda:
+            y = out if out is not None else torch.empty(M.n_rows, dtype=x.dtype, device=x.device)
+            return _spmv_device(M, x, y, ref_order)
+        xd = x.to(_dev.DEVICE, non_blocking=True)
+        yd = torch.empty(M.n_rows, dtype=x.dtype, device=_dev.DEVICE)
+        _spmv_device(M, xd, yd, ref_order)
+        if out is None:
+            out = torch.empty(M.n_rows, dtype=x.dtype, pin_memory=True)
+        out.copy_(yd, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
+    x = np.asarray(x)
+    if len(x) != M.n_cols:
+        raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
+    if x.dtype not in _dev.DT_CODE:
+        raise TypeError(f"unsupported x dtype {x.dtype}")
+    xd = _dev.upload(x)
+    y = _dev.empty(M.n_rows, x.dtype)
+    _spmv_device(M, xd, y, ref_order)
+    return _dev.download(y, x.dtype)
+
+
+def packsell_to_csr(M: PackSellMatrix) -> CsrMatrix:
+    """Decode every delta chain back to the quantised CSR, logical row order (packed.py:274-303)."""
+    from . import _dev, _lib
+    lib = _lib.lib()
+    d = M.desc()
+    ws = _dev.workspace(lib.psell_to_csr_workspace_bytes(d))
+    row_ptr = _dev.empty(M.n_rows + 1, np.int64)
+    nnz = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    st = _lib.stream_handle()
+    rc = lib.psell_to_csr_plan(d, _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                               _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr), ctypes.byref(nnz), st, err)
+    _lib.check(rc, err, M.fmt)
+    col = _dev.empty(nnz.value, np.int32)
+    val = _dev.empty(nnz.value, np.float64)
+    rc = lib.psell_to_csr_fill(d, _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                               _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(val), st, err)
+    _lib.check(rc, err, M.fmt)
+    return CsrMatrix(M.n_rows, M.n_cols, _dev.download(row_ptr, np.int64),
+                     _dev.download(col, np.int32), _dev.download(val, np.float64))
+
+
+def footprint_bits(M: PackSellMatrix) -> FootprintReport:
+    """Packed vs like-for-like sliced storage bits (packed.py:306-327).
+
+    The sliced side needs only the decoded row lengths: its padding is the
+    SELL-C-sigma layout of those lengths (sell.py:124-147), computed here from
+    the K5 decode's row pointer.
+    """
+    value_bits = 16 if M.fmt.codec == codec.FP16 else 32
+    perm_bits = 0 if M.perm is None else M.perm.dtype.itemsize * 8 * len(M.perm)
+    pack_bits = M.fmt.w * M.n_stored + 64 * (M.n_slices + 1) + perm_bits
+    A = packsell_to_csr(M)
+    sell_mode = "none" if M.mode == "explicit" else M.mode
+    lens = A.row_lengths()
+    n = A.n_rows
+    if sell_mode == "none":
+        ordered = lens
+    else:
+        from .sell import row_sort_order
+        ordered = lens[row_sort_order(lens, M.sigma)]
+    n_sl = -(-n // M.c)
+    padded = np.zeros(n_sl * M.c, dtype=np.int64)
+    padded[:n] = ordered
+    sell_stored = int((padded.reshape(n_sl, M.c).max(axis=1) * M.c).sum()) if n_sl else 0
+    sell_perm_bits = 8 * np.dtype(perm_dtype(M.sigma)).itemsize * n if sell_mode == "implicit" else 0
+    sell_bits = (value_bits + 32) * sell_stored + 64 * (n_sl + 1) + sell_perm_bits
+    ratio = pack_bits / sell_bits if sell_bits else 1.0
+    return FootprintReport(int(pack_bits), int(sell_bits), float(ratio))

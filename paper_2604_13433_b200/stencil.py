@@ -1,0 +1,188 @@
+"""Synthetic matrix generators for the BASELINE configs.
+
+Host generators return a `CsrMatrix` (numpy) identical to what the reference
+builds for the same problem:
+
+* `poisson2d` / `poisson3d` — Dirichlet Laplacians, diagonal 2*ndim, -1
+  neighbours, row-major ordering (reference stencil.py:10-52);
+* `stencil27` — the HPCG 27-point box stencil (diag 26, off -1), the paper's
+  HPCG_k_k_k matrices (BASELINE config 2/3);
+* `powerlaw` — the config-4 irregular matrix (SURVEY.md §8d proposal).
+
+Device generators write the same CSR directly into HBM (psell_gen_stencil),
+optionally only the row range of one rank's slab and optionally with the
+sym_diag_scale / row_sum_scale preprocessing fused — bitwise equal to the
+host generator followed by the host scaling (tests/test_gpu_generators.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .matrix import CooMatrix, CsrMatrix, to_csr
+
+
+def _grid_stencil(dims, box: bool, diag: float, row_begin: int = 0, row_end: int = None) -> CsrMatrix:
+    dims = [int(d) for d in dims]
+    if any(d < 1 for d in dims):
+        raise ValueError(f"grid dimensions must be positive, got {dims}")
+    n = int(np.prod(dims))
+    if n > 2**31 - 1:
+        raise ValueError(f"grid of {n} points overflows 32-bit indexing")
+    if row_begin != 0 or (row_end is not None and row_end != n):
+        return _grid_rows(dims, box, diag, int(row_begin), n if row_end is None else int(row_end))
+    nd = len(dims)
+    # neighbour offsets in lexicographic order => ascending column order per row
+    strides = np.cumprod([1] + dims[::-1][:-1])[::-1].astype(np.int64)
+    if box:
+        offs = np.array(np.meshgrid(*([[-1, 0, 1]] * nd), indexing="ij")).reshape(nd, -1).T
+    else:
+        eye = np.eye(nd, dtype=np.int64)
+        offs = np.concatenate([-eye, np.zeros((1, nd), np.int64), eye])
+    # ascending flat column delta => ascending columns in every row
+    offs = offs[np.argsort(offs @ strides, kind="stable")]
+    coords = np.stack(np.meshgrid(*[np.arange(d) for d in dims], indexing="ij"), -1).reshape(-1, nd)
+    cols, vals, lens = [], [], np.zeros(n, dtype=np.int64)
+    for o in offs:
+        nb = coords + o
+        ok = np.all((nb >= 0) & (nb < np.array(dims)), axis=1)
+        c = np.where(ok, nb @ strides, -1)
+        v = diag if not np.any(o) else -1.0
+        cols.append(c)
+        vals.append(np.where(ok, v, 0.0))
+        lens += ok
+    C = np.stack(cols, 1)
+    V = np.stack(vals, 1)
+    keep = C >= 0
+    row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return CsrMatrix(n, n, row_ptr, C[keep].astype(np.int32), V[keep])
+
+
+def _grid_rows(dims, box, diag, r0, r1) -> CsrMatrix:
+    """Rows [r0, r1) of the stencil as a local CSR (n_cols global) — a rank slab / CPU sample."""
+    nd = len(dims)
+    n = int(np.prod(dims))
+    strides = np.cumprod([1] + dims[::-1][:-1])[::-1].astype(np.int64)
+    if box:
+        offs = np.array(np.meshgrid(*([[-1, 0, 1]] * nd), indexing="ij")).reshape(nd, -1).T
+    else:
+        eye = np.eye(nd, dtype=np.int64)
+        offs = np.concatenate([-eye, np.zeros((1, nd), np.int64), eye])
+    offs = offs[np.argsort(offs @ strides, kind="stable")]
+    coords = np.stack(np.unravel_index(np.arange(r0, r1, dtype=np.int64), dims), -1)
+    cols, vals = [], []
+    lens = np.zeros(r1 - r0, dtype=np.int64)
+    for o in offs:
+        nb = coords + o
+        ok = np.all((nb >= 0) & (nb < np.array(dims)), axis=1)
+        cols.append(np.where(ok, nb @ strides, -1))
+        vals.append(np.where(ok, diag if not np.any(o) else -1.0, 0.0))
+        lens += ok
+    C = np.stack(cols, 1)
+    V = np.stack(vals, 1)
+    keep = C >= 0
+    row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return CsrMatrix(r1 - r0, n, row_ptr, C[keep].astype(np.int32), V[keep])
+
+
+def stencil_rows(kind: str, nx: int, row_begin: int, row_end: int) -> CsrMatrix:
+    """Host rows [row_begin, row_end) of poisson2d/poisson3d/stencil27 on an nx^d grid."""
+    if kind == "poisson2d":
+        return _grid_rows([nx, nx], False, 4.0, row_begin, row_end)
+    if kind == "poisson3d":
+        return _grid_rows([nx, nx, nx], False, 6.0, row_begin, row_end)
+    if kind == "stencil27":
+        return _grid_rows([nx, nx, nx], True, 26.0, row_begin, row_end)
+    raise ValueError(f"unknown stencil {kind!r}")
+
+
+def poisson2d(nx: int, ny: int = None) -> CsrMatrix:
+    """5-point Laplacian, diagonal 4 (reference stencil.py:45-47)."""
+    return _grid_stencil([nx, nx if ny is None else ny], box=False, diag=4.0)
+
+
+def poisson3d(nx: int, ny: int = None, nz: int = None) -> CsrMatrix:
+    """7-point Laplacian, diagonal 6 (reference stencil.py:50-52)."""
+    return _grid_stencil([nx, nx if ny is None else ny, nx if nz is None else nz], box=False, diag=6.0)
+
+
+def stencil27(nx: int, ny: int = None, nz: int = None) -> CsrMatrix:
+    """HPCG 27-point box stencil on nx*ny*nz, z slowest (diag 26, off-diagonal -1)."""
+    return _grid_stencil([nx, nx if ny is None else ny, nx if nz is None else nz], box=True, diag=26.0)
+
+
+def powerlaw(n: int = 2**23, seed: int = 2604, alpha: float = 1.5, lmax: int = 8192,
+             local_frac: float = 0.8, spread: float = 4096.0) -> CsrMatrix:
+    """Irregular power-law row lengths (config 4).
+
+    L_i = min(lmax, floor(4 U^(-1/alpha))) (Pareto, mean ~12); 80 % of a row's
+    columns are i + round(N(0, spread)) clipped to [0, n), 20 % uniform; sorted,
+    unique; values U[0.01, 1) * +-1.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    u = rng.random(n)
+    lens = np.minimum(lmax, np.floor(4.0 * u ** (-1.0 / alpha))).astype(np.int64)
+    lens = np.maximum(lens, 1)
+    tot = int(lens.sum())
+    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
+    local = rng.random(tot) < local_frac
+    near = np.clip(rows + np.rint(rng.normal(0.0, spread, tot)).astype(np.int64), 0, n - 1)
+    far = rng.integers(0, n, tot)
+    cols = np.where(local, near, far)
+    key = rows * n + cols
+    key = np.unique(key)
+    r = key // n
+    c = key - r * n
+    vals = rng.uniform(0.01, 1.0, len(key)) * rng.choice([-1.0, 1.0], len(key))
+    counts = np.bincount(r, minlength=n)
+    row_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return CsrMatrix(n, n, row_ptr, c.astype(np.int32), vals)
+
+
+_SCALES = {None: 0, "none": 0, "sym": 1, "rowsum": 2}
+
+
+def stencil_device(kind: str, nx: int, ny: int = None, nz: int = None, *, scale=None,
+                   row_begin: int = 0, row_end: int = None):
+    """Generate rows [row_begin, row_end) of a stencil matrix directly in HBM.
+
+    kind: "poisson2d" (5-pt, diag 4), "poisson3d" (7-pt, diag 6) or "stencil27"
+    (27-pt box, diag 26).  scale: None, "sym" (sym_diag_scale) or "rowsum"
+    (row_sum_scale).  Returns a DeviceCsrMatrix whose row0 = row_begin and whose
+    n_cols is the global matrix size.
+    """
+    import ctypes
+    from . import _dev, _lib
+    from .matrix import DeviceCsrMatrix
+    lib = _lib.lib()
+    if kind == "poisson2d":
+        dims, box, diag = (1, nx, nx if ny is None else ny), 0, 4.0
+    elif kind == "poisson3d":
+        dims, box, diag = (nx, nx if ny is None else ny, nx if nz is None else nz), 0, 6.0
+    elif kind == "stencil27":
+        dims, box, diag = (nx, nx if ny is None else ny, nx if nz is None else nz), 1, 26.0
+    else:
+        raise ValueError(f"unknown stencil {kind!r}")
+    n = int(np.prod(dims))
+    if n > 2**31 - 1:
+        raise ValueError(f"grid of {n} points overflows 32-bit indexing")
+    r1 = n if row_end is None else int(row_end)
+    r0 = int(row_begin)
+    rows = r1 - r0
+    ws = _dev.workspace(lib.psell_gen_workspace_bytes(rows))
+    row_ptr = _dev.empty(rows + 1, np.int64)
+    nnz = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    st = _lib.stream_handle()
+    rc = lib.psell_gen_stencil_plan(dims[0], dims[1], dims[2], box, diag, r0, r1, _lib.ptr(ws),
+                                    ws.numel(), _lib.ptr(row_ptr), ctypes.byref(nnz), st, err)
+    _lib.check(rc, err)
+    col = _dev.empty(nnz.value, np.int32)
+    val = _dev.empty(nnz.value, np.float64)
+    rc = lib.psell_gen_stencil_fill(dims[0], dims[1], dims[2], box, diag, _SCALES[scale], r0, r1,
+                                    _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(val), st, err)
+    _lib.check(rc, err)
+    return DeviceCsrMatrix(rows, n, row_ptr, col, val, row0=r0)
+
+
+__all__ = ["poisson2d", "poisson3d", "stencil27", "powerlaw", "stencil_device"]

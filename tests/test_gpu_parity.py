@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference fixtures and the oracle.
+
+Bar: pack / offset / perm / k_left / counts byte-identical;
+REF_ORDER SpMV bitwise equal to the reference; production FMA SpMV within
+    e_rel = ||y - y_ref||_inf / (||A_q||_inf ||x||_inf) <= 2 * L_max * 2^-24  (f32 / f64 x),
+    e_rel <= 2^-11 + 2 * L_max * 2^-24 vs the f32-widened reference       (f16 x),
+with L_max the maximum stored words per row.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2604_13433_b200 as P
+from conftest import case_csr, golden_x, random_csr_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(z, i, m):
+    rp, ci, v = case_csr(z, i)
+    return P.CsrMatrix(m["n_rows"], m["n_cols"], rp, ci, v)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def test_build_bit_exact_vs_reference(golden_build):
+    z, meta = golden_build
+    for i, m in enumerate(meta):
+        A = _csr(z, i, m)
+        M = P.build_packsell(A, m["c"], m["sigma"], P.parse_format(m["preset"]), m["mode"],
+                             _k_left_override=m["k_left_override"])
+        assert M.pack.dtype == z[f"c{i}_pack"].dtype
+        assert np.array_equal(M.pack, z[f"c{i}_pack"]), i
+        assert np.array_equal(M.offset, z[f"c{i}_offset"]), i
+        if m["perm_dtype"]:
+            assert M.perm.dtype.name == m["perm_dtype"] and np.array_equal(M.perm, z[f"c{i}_perm"]), i
+        else:
+            assert M.perm is None
+        assert M.k_left == m["k_left"] and list(M.counts) == m["counts"], i
+        assert (M.n_slices, M.n_stored) == (m["n_slices"], m["n_stored"])
+
+
+def test_decode_vs_reference(golden_build):
+    z, meta = golden_build
+    for i, m in enumerate(meta):
+        M = P.build_packsell(_csr(z, i, m), m["c"], m["sigma"], P.parse_format(m["preset"]), m["mode"],
+                             _k_left_override=m["k_left_override"])
+        R = P.packsell_to_csr(M)
+        assert np.array_equal(R.row_ptr, z[f"c{i}_dec_row_ptr"]), i
+        assert np.array_equal(R.col_idx, z[f"c{i}_dec_col_idx"]), i
+        assert np.array_equal(_bits(R.values), _bits(z[f"c{i}_dec_values"])), i
+
+
+def test_spmv_ref_order_bitwise_and_fma_tolerance(golden_build):
+    z, meta = golden_build
+    for i, m in enumerate(meta):
+        A = _csr(z, i, m)
+        fmt = P.parse_format(m["preset"])
+        M = P.build_packsell(A, m["c"], m["sigma"], fmt, m["mode"], _k_left_override=m["k_left_override"])
+        lmax = max(1, int(np.max(np.diff(M.offset) // m["c"])) if M.n_slices else 1)
+        aq = np.abs(P.quantize(fmt, A.values)) if A.nnz else np.zeros(0)
+        rows = np.repeat(np.arange(A.n_rows), A.row_lengths())
+        anorm = np.bincount(rows, aq, minlength=A.n_rows).max() if A.nnz else 0.0
+        for dt in (np.float16, np.float32, np.float64):
+            x = golden_x(i, m["n_cols"], dt)
+            want = z[f"c{i}_y_{np.dtype(dt).name}"]
+            y = P.packsell_spmv(M, x, ref_order=True)
+            assert y.dtype == want.dtype and np.array_equal(_bits(y), _bits(want)), (i, dt)
+            yf = P.packsell_spmv(M, x)
+            assert yf.dtype == want.dtype
+            if A.nnz == 0 or anorm == 0:
+                assert not np.any(yf)
+                continue
+            xw = x.astype(np.float32) if dt == np.float16 else x
+            ref = P.packsell_spmv(M, xw, ref_order=True).astype(np.float64)
+            den = anorm * max(np.abs(x.astype(np.float64)).max(), 1e-300)
+            err = np.abs(yf.astype(np.float64) - ref).max() / den
+            bound = 2 * lmax * 2.0 ** -24 + (2.0 ** -11 if dt == np.float16 else 0.0)
+            assert err <= bound, (i, dt, err, bound)
+
+
+def test_csr_spmv_bitwise(golden_build):
+    z, meta = golden_build
+    for i, m in enumerate(meta):
+        A = _csr(z, i, m)
+        for dt in (np.float16, np.float32, np.float64):
+            x = golden_x(i, m["n_cols"], dt)
+            y = P.csr_spmv(A, x, dt)
+            assert np.array_equal(_bits(y), _bits(z[f"c{i}_csr_{np.dtype(dt).name}"])), (i, dt)
+
+
+def test_errors_match_reference(golden_errors):
+    def check(name, fn):
+        g = golden_errors[name]
+        if g["exc"] is None:
+            fn()
+            return
+        with pytest.raises(Exception) as ei:
+            fn()
+        assert type(ei.value).__name__ == g["exc"], name
+        assert str(ei.value) == g["msg"], name
+
+    fp16, e14, e20, f32 = (P.parse_format(s) for s in ("fp16", "e8m14", "e8m20", "fp32embed"))
+    A = P.to_csr(P.CooMatrix(3, 300, [0, 1, 2], [0, 0, 1], [1.0, 2.0, 3.0]))
+    check("first_gap", lambda: P.build_packsell(A, 1, 1, fp16, "implicit", _k_left_override=0))
+    B = P.to_csr(P.CooMatrix(600, 600, [300, 301, 599], [0, 3, 10], [1.0, 2.0, 3.0]))
+    check("first_gap_argmin", lambda: P.build_packsell(B, 4, 8, e14, "implicit", _k_left_override=5))
+    C = P.CsrMatrix(2, 5, [0, 2, 3], [0, 3, 1], [1.0, np.nan, np.inf])
+    check("nonfinite", lambda: P.build_packsell(C, 1, 1, fp16, "none"))
+    D = P.CsrMatrix(2, 5, [0, 2, 3], [0, 3, 1], [1.0, 7e4, 1e6])
+    check("overflow_fp16", lambda: P.build_packsell(D, 1, 1, fp16, "none"))
+    E = P.CsrMatrix(2, 5, [0, 2, 3], [0, 3, 1], [1.0, 3.5e38, 1e300])
+    check("overflow_e8m20", lambda: P.build_packsell(E, 1, 1, e20, "none"))
+    check("overflow_fp32", lambda: P.build_packsell(E, 1, 1, f32, "none"))
+    F = P.CsrMatrix(2, 5, [0, 2, 3], [0, 3, 1], [1e6, np.nan, 1.0])
+    check("nonfinite_before_overflow", lambda: P.build_packsell(F, 1, 1, fp16, "none"))
+    check("layout_before_codec", lambda: P.build_packsell(
+        P.CsrMatrix(2, 9, [0, 1, 2], [0, 0], [np.nan, 1.0]), 1, 1, fp16, "implicit", _k_left_override=0))
+    G = P.to_csr(P.CooMatrix(2, 2 ** 31 - 1, [0, 0], [0, 2 ** 31 - 2], [1.0, 2.0]))
+    check("no_gap_range_w32", lambda: P.build_packsell(G, 1, 1, fp16, "none"))
+    check("bad_mode", lambda: P.build_packsell(A, 1, 1, fp16, "sorted"))
+    check("bad_sigma", lambda: P.build_packsell(A, 4, 6, fp16, "implicit"))
+    check("encode_nan", lambda: P.encode_values(e14, [1.0, float("nan")]))
+    check("encode_over", lambda: P.encode_values(fp16, [1.0, 2.0, -1e9]))
+    check("spmv_len", lambda: P.packsell_spmv(P.build_packsell(A, 1, 1, fp16, "none"), np.ones(3, np.float32)))
+
+
+@pytest.mark.parametrize("name", ["fp16", "fp32embed"] + [f"e8m{y}" for y in range(1, 22)])
+def test_codec_vs_reference(golden_codec, name):
+    fmt = P.parse_format(name)
+    pat = P.encode_values(fmt, golden_codec[f"{name}_values"])
+    want = golden_codec[f"{name}_patterns"]
+    assert pat.dtype == want.dtype and np.array_equal(pat, want)
+    dec = P.decode_patterns(fmt, pat)
+    assert np.array_equal(_bits(dec), _bits(O.decode(O.preset(name), want)))
+    v, d, fl = P.unpack_words(fmt, golden_codec[f"{name}_words"])
+    assert np.array_equal(_bits(v), _bits(golden_codec[f"{name}_unpack_values"]))
+    assert np.array_equal(d, golden_codec[f"{name}_unpack_deltas"]) and d.dtype == fmt.word_dtype
+    assert np.array_equal(fl, golden_codec[f"{name}_unpack_flags"])
+    n = len(pat)
+    deltas = np.arange(n) % (fmt.max_delta + 1)
+    w = P.pack_words(fmt, pat, deltas, np.ones(n, bool))
+    assert np.array_equal(w, O.pack_words(O.preset(name), pat, deltas, np.ones(n, bool)))
+
+
+def test_scalar_pack_unpack_goldens():
+    fmt = P.PackFormat(32, 15, "fp16")
+    assert P.pack(fmt, 1.0, 3) == 0x3C000007
+    assert P.unpack(fmt, 0x3C000007) == P.UnpackedEntry(1.0, 3, True)
+    assert P.pack(fmt, None, 70000) == 0x000222E0
+    assert P.unpack(fmt, 0) == P.UnpackedEntry(0.0, 0, False)
+    assert P.encode_value(P.PackFormat(32, 2, "e8my"), 0.1) << 3 == 0x3DCCCCD0
+
+
+def test_random_sweep_vs_oracle(rng):
+    """c03-style sweep: modes x C x sigma x codecs, bit-exact build + REF SpMV vs the oracle."""
+    presets = ["fp16", "e8m14", "e8m20", "e8m3", "fp32embed"]
+    for it in range(80):
+        n = int(rng.integers(1, 600))
+        m = int(rng.integers(1, 600))
+        dens = float(np.exp(rng.uniform(np.log(0.001), np.log(0.2))))
+        rp, ci, v = random_csr_arrays(rng, n, m, dens, banded=(it % 3 == 0))
+        A = P.CsrMatrix(n, m, rp, ci, v)
+        mode = ["none", "explicit", "implicit"][it % 3]
+        c = [1, 2, 4, 16, 32, 64][it % 6]
+        sigma = c * [1, 8, 2][it % 3]
+        if sigma > 65536:
+            sigma = c
+        pre = presets[it % len(presets)]
+        M = P.build_packsell(A, c, sigma, P.parse_format(pre), mode)
+        OM = O.build(rp, ci, v, m, c, sigma, O.preset(pre), mode)
+        assert np.array_equal(M.pack, OM.pack) and np.array_equal(M.offset, OM.offset), it
+        assert M.k_left == OM.k_left and tuple(M.counts) == OM.counts
+        if mode == "implicit":
+            assert np.array_equal(M.perm, OM.perm)
+        x = rng.uniform(-1, 1, m).astype(np.float32)
+        assert np.array_equal(_bits(P.packsell_spmv(M, x, ref_order=True)), _bits(O.spmv(OM, x))), it
+
+
+@pytest.mark.parametrize("sigma", [1, 3, 32, 256, 1024, 2048, 4096, 65536])
+def test_row_sort_order_vs_oracle(rng, sigma):
+    n = 200_000
+    counts = rng.integers(0, 40, n) * (rng.random(n) < 0.9) + (rng.random(n) < 0.01) * 5000
+    assert np.array_equal(P.row_sort_order(counts, sigma), O.sort_order(counts, sigma))
+
+
+@pytest.mark.parametrize("kind,dims,scale", [("poisson2d", (9, 7), None), ("poisson3d", (6, 5, 4), "sym"),
+                                             ("stencil27", (7, 6, 5), None), ("stencil27", (5, 5, 5), "rowsum"),
+                                             ("poisson3d", (10, 10, 10), None)])
+def test_device_generators_equal_host(kind, dims, scale):
+    host = {"poisson2d": P.poisson2d, "poisson3d": P.poisson3d, "stencil27": P.stencil27}[kind](*dims)
+    if scale == "sym":
+        host = P.sym_diag_scale(host)
+    elif scale == "rowsum":
+        host = P.row_sum_scale(host)
+    D = P.stencil_device(kind, *dims, scale=scale).to_host()
+    assert np.array_equal(D.row_ptr, host.row_ptr)
+    assert np.array_equal(D.col_idx, host.col_idx)
+    assert np.array_equal(_bits(D.values), _bits(host.values))
+    n = host.n_rows
+    r0, r1 = n // 3, 2 * n // 3
+    S = P.stencil_device(kind, *dims, scale=scale, row_begin=r0, row_end=r1).to_host()
+    assert np.array_equal(S.row_ptr, host.row_ptr[r0:r1 + 1] - host.row_ptr[r0])
+    assert np.array_equal(S.col_idx, host.col_idx[host.row_ptr[r0]:host.row_ptr[r1]])
+
+
+def test_slab_builds_concatenate_to_global(rng):
+    """Rank slabs (sigma-aligned row ranges, global k_left) concatenate to the global pack."""
+    A = P.stencil27(12)
+    fmt = P.parse_format("fp16")
+    G = P.build_packsell(A, 32, 256, fmt, "implicit")
+    n = A.n_rows
+    bounds = [0, 256, 768, n]
+    packs, perms, base = [], [], 0
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    yg = P.packsell_spmv(G, x, ref_order=True)
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        S = P.stencil_device("stencil27", 12, row_begin=a, row_end=b)
+        M = P.build_packsell(S, 32, 256, fmt, "implicit", _k_left_override=G.k_left)
+        packs.append(M.pack)
+        perms.append(M.perm)
+        k0 = a // 32
+        assert np.array_equal(M.offset + base, G.offset[k0:k0 + M.n_slices + 1])
+        base += M.n_stored
+        ys = P.packsell_spmv(M, x, ref_order=True)
+        assert np.array_equal(_bits(ys), _bits(yg[a:b]))
+    assert np.array_equal(np.concatenate(packs), G.pack)
+    assert np.array_equal(np.concatenate(perms), G.perm)

@@ -1,0 +1,118 @@
+"""Host-side logic and the C ABI surface (CPU only, no kernel launches)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2604_13433_b200 as P
+from paper_2604_13433_b200 import _lib
+from paper_2604_13433_b200.sell import _check_layout_params
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _raises_like(fn, golden):
+    if golden["exc"] is None:
+        fn()
+        return
+    with pytest.raises(Exception) as ei:
+        fn()
+    assert type(ei.value).__name__ == golden["exc"]
+    assert str(ei.value) == golden["msg"]
+
+
+@pytest.mark.parametrize("w,d,cd", [(16, 4, "fp16"), (32, 0, "e8my"), (32, 31, "e8my"), (32, 14, "fp16"),
+                                    (64, 15, "e8my"), (32, 22, "e8my"), (32, 15, "fp32embed"),
+                                    (64, 40, "fp32embed"), (32, 15, "bogus")])
+def test_packformat_validation_messages(golden_errors, w, d, cd):
+    _raises_like(lambda: P.PackFormat(w, d, cd), golden_errors[f"fmt_{w}_{d}_{cd}"])
+
+
+@pytest.mark.parametrize("name", ["q5", "e8mx", "E8M14", "FP16"])
+def test_parse_format(golden_errors, name):
+    _raises_like(lambda: P.parse_format(name), golden_errors[f"parse_{name}"])
+
+
+def test_presets():
+    assert P.parse_format("fp16") == P.PackFormat(32, 15, "fp16")
+    assert P.parse_format("e8m14") == P.PackFormat(32, 8, "e8my")
+    assert P.parse_format("e8m14").name == "e8m14"
+    assert P.parse_format("fp32embed").word_dtype == np.uint64
+    f = P.PackFormat()
+    assert (f.max_delta, f.max_dummy_delta, f.v) == (2 ** 15 - 1, 2 ** 31 - 1, 16)
+
+
+@pytest.mark.parametrize("name,c,sigma,mode", [("bad_mode", 1, 1, "sorted"), ("bad_c", 0, 1, "none"),
+                                               ("bad_sigma", 4, 6, "implicit"), ("big_sigma", 4, 65540, "implicit")])
+def test_layout_param_messages(golden_errors, name, c, sigma, mode):
+    _raises_like(lambda: _check_layout_params(c, sigma, mode), golden_errors[name])
+
+
+def test_leftmost_offset_and_delta_stream():
+    assert P.leftmost_offset(300, 256, 10) == 246
+    assert P.leftmost_offset(300, 256, 256) == 0
+    fmt = P.PackFormat(32, 2, "e8my")
+    s = P.build_delta_stream([1, 5], [1.0, 2.0], 0, fmt)
+    assert s == [P.DeltaEntry(1, 1.0), P.DeltaEntry(4, None), P.DeltaEntry(0, 2.0)]
+    gap = 2 ** 31 + 5
+    s = P.build_delta_stream([0, gap], [1.0, 2.0], 0, P.PackFormat())
+    assert sum(e.delta for e in s if e.value is None) == gap
+
+
+def test_host_generators_shapes():
+    A = P.stencil27(6)
+    assert A.nnz == (3 * 6 - 2) ** 3
+    assert np.all(np.diff(A.col_idx[A.row_ptr[0]:A.row_ptr[1]]) > 0)
+    assert np.all(A.values[A.col_idx == np.repeat(np.arange(A.n_rows), A.row_lengths())] == 26.0)
+    B = P.poisson3d(5)
+    assert B.nnz == 5 ** 3 * 7 - 6 * 5 ** 2
+    C = P.powerlaw(4096, seed=3)
+    assert C.n_rows == 4096 and C.nnz > 4096
+    lens = C.row_lengths()
+    assert lens.max() > 10 * lens.mean()
+
+
+def test_csr_validation():
+    with pytest.raises(ValueError):
+        P.CsrMatrix(2, 2, [0, 1], [0], [1.0])
+    with pytest.raises(ValueError):
+        P.CsrMatrix(2, 2, [0, 2, 1], [0, 1], [1.0, 2.0])
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "psell.h")).read()
+    return sorted(set(re.findall(r"PSELL_API\s+[\w\s\*]+?\b(psell_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    """libpsell.so loads (no GPU needed) and exports every function include/psell.h declares."""
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    decl = _header_functions()
+    assert len(decl) >= 30
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.exported_symbols()) == decl
+    l2 = _lib.load(require_gpu=False)
+    assert l2.psell_abi_version() == 1
+    assert b"sm_100a" in l2.psell_version()
+
+
+def test_workspace_sizing_is_host_only():
+    l = _lib.load(require_gpu=False)
+    d = _lib.PsellDesc()
+    d.w, d.d, d.codec, d.c, d.sigma, d.mode = 32, 15, 0, 32, 256, 2
+    d.n_rows, d.n_cols, d.row0, d.k_left, d.nnz = 1 << 24, 1 << 24, 0, -1, 449455096
+    ws = l.psell_build_workspace_bytes(d)
+    assert 3 * 4 * (1 << 24) <= ws < 64 * (1 << 24)
+    assert l.psell_spmv_dot_partials(d) == (1 << 24) // 256
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.encode_values(P.PackFormat(), [1.0])
