@@ -200,14 +200,14 @@ PSELL_API int psell_dot(const void* a, const void* b, int32_t dtype, int64_t n, 
  * iflags[0]=breakdown iflags[1]=done */
 PSELL_API int psell_ipcg_begin(int64_t n, const double* r64, float* x, float* r, float* z, float* p,
                      const float* inv_diag, double* partials, double* local_out, void* stream);
-PSELL_API int psell_ipcg_set_rz(const double* parts, int32_t n_parts, double* scal, int32_t* iflags,
+PSELL_API int psell_ipcg_set_rz(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                       void* stream);
-PSELL_API int psell_ipcg_alpha(const double* parts, int32_t n_parts, double* scal, int32_t* iflags,
+PSELL_API int psell_ipcg_alpha(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                      void* stream);
 PSELL_API int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
                       const float* inv_diag, const double* scal, const int32_t* iflags,
                       double* partials, double* local_out, void* stream);
-PSELL_API int psell_ipcg_beta(const double* parts, int32_t n_parts, double* scal, int32_t* iflags,
+PSELL_API int psell_ipcg_beta(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                     void* stream);
 PSELL_API int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal,
                          const int32_t* iflags, void* stream);

@@ -74,19 +74,19 @@ __global__ void __launch_bounds__(kBlock) ipcg_begin_kernel(long long n, const d
 }
 
 // scal: [0]=rz [1]=pq [2]=alpha [3]=beta [4]=rz_new ; iflags: [0]=breakdown [1]=done
-__global__ void ipcg_set_rz_kernel(const double* parts, int np, double* scal, int32_t* iflags) {
+__global__ void ipcg_set_rz_kernel(const double* parts, int np, int stride, double* scal, int32_t* iflags) {
   double s = 0.0;
-  for (int i = 0; i < np; ++i) s += parts[i];
+  for (int i = 0; i < np; ++i) s += parts[(long long)i * stride];
   scal[0] = s;
   iflags[0] = 0;
   iflags[1] = 0;
 }
 
 // solvers.py:295-299
-__global__ void ipcg_alpha_kernel(const double* parts, int np, double* scal, int32_t* iflags) {
+__global__ void ipcg_alpha_kernel(const double* parts, int np, int stride, double* scal, int32_t* iflags) {
   if (iflags[0]) return;
   double pq = 0.0;
-  for (int i = 0; i < np; ++i) pq += parts[i];
+  for (int i = 0; i < np; ++i) pq += parts[(long long)i * stride];
   scal[1] = pq;
   if (pq <= 0.0 || !isfinite(pq) || scal[0] == 0.0) {
     iflags[0] = 1;
@@ -123,10 +123,10 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
 }
 
 // solvers.py:304-306
-__global__ void ipcg_beta_kernel(const double* parts, int np, double* scal, int32_t* iflags) {
+__global__ void ipcg_beta_kernel(const double* parts, int np, int stride, double* scal, int32_t* iflags) {
   if (iflags[0]) return;
   double s = 0.0;
-  for (int i = 0; i < np; ++i) s += parts[i];
+  for (int i = 0; i < np; ++i) s += parts[(long long)i * stride];
   scal[4] = s;
   scal[3] = s / scal[0];
   scal[0] = s;
@@ -311,13 +311,13 @@ int psell_ipcg_begin(int64_t n, const double* r64, float* x, float* r, float* z,
   return LAUNCH_OK();
 }
 
-int psell_ipcg_set_rz(const double* parts, int32_t n_parts, double* scal, int32_t* iflags, void* stream) {
-  ipcg_set_rz_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, scal, iflags);
+int psell_ipcg_set_rz(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags, void* stream) {
+  ipcg_set_rz_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, stride, scal, iflags);
   return LAUNCH_OK();
 }
 
-int psell_ipcg_alpha(const double* parts, int32_t n_parts, double* scal, int32_t* iflags, void* stream) {
-  ipcg_alpha_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, scal, iflags);
+int psell_ipcg_alpha(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags, void* stream) {
+  ipcg_alpha_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, stride, scal, iflags);
   return LAUNCH_OK();
 }
 
@@ -330,8 +330,8 @@ int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, c
   return LAUNCH_OK();
 }
 
-int psell_ipcg_beta(const double* parts, int32_t n_parts, double* scal, int32_t* iflags, void* stream) {
-  ipcg_beta_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, scal, iflags);
+int psell_ipcg_beta(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags, void* stream) {
+  ipcg_beta_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, stride, scal, iflags);
   return LAUNCH_OK();
 }
 

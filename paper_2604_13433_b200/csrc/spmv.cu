@@ -192,6 +192,135 @@ __global__ void __launch_bounds__(kBlock) spmv_c32_kernel(const SpmvArgs a) {
   finish_dot<DOT>(a, dotv);
 }
 
+// ---- fast production path (C == 32, FMA accumulation)
+//
+// Per word: flag predicate, cursor2 += w & mask (cursor2 = 2 * column, so for
+// f16 x it is already the byte offset), one gather, one predicated FMA.  The
+// fp16 codec with f16 x uses the sm_100 mixed-precision FMA (FHFMA: f16 x f16
+// + f32), so neither the value nor x is converted.  Dummy and padding words
+// only move the cursor (FMA predicated off).
+template <typename XT>
+__device__ __forceinline__ const char* xbyte(const XT* x, uint32_t c2) {
+  return reinterpret_cast<const char*>(x) + (size_t)c2 * (sizeof(XT) / 2);
+}
+
+template <int CODEC, typename XT> struct FastStep;
+
+template <> struct FastStep<PSELL_FP16, __half> {
+  using Acc = float;
+  __device__ static void run(uint32_t w, uint32_t& c2, const __half* x, float& acc, uint32_t, uint32_t) {
+    const uint32_t f = w & 1u;
+    c2 += w & (f ? 0xFFFEu : 0xFFFFFFFEu);
+    const unsigned short xb = __ldg(reinterpret_cast<const unsigned short*>(xbyte(x, c2)));
+    asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
+        " @p fma.rn.f32.f16 %0, hi, %3, %0;\n}" : "+f"(acc) : "r"(f), "r"(w), "h"(xb));
+  }
+};
+template <> struct FastStep<PSELL_FP16, float> {
+  using Acc = float;
+  __device__ static void run(uint32_t w, uint32_t& c2, const float* x, float& acc, uint32_t, uint32_t) {
+    const uint32_t f = w & 1u;
+    c2 += w & (f ? 0xFFFEu : 0xFFFFFFFEu);
+    const float xv = __ldg(reinterpret_cast<const float*>(xbyte(x, c2)));
+    asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n .reg .f32 v;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
+        " cvt.f32.f16 v, hi;\n @p fma.rn.f32 %0, v, %3, %0;\n}" : "+f"(acc) : "r"(f), "r"(w), "f"(xv));
+  }
+};
+template <> struct FastStep<PSELL_E8MY, float> {
+  using Acc = float;
+  // m_real = 2^(D+1) - 2 (delta field << 1), vmask = ~(2^(D+1) - 1) (value bits)
+  __device__ static void run(uint32_t w, uint32_t& c2, const float* x, float& acc, uint32_t m_real,
+                             uint32_t vmask) {
+    const uint32_t f = w & 1u;
+    c2 += w & (f ? m_real : 0xFFFFFFFEu);
+    const float xv = __ldg(reinterpret_cast<const float*>(xbyte(x, c2)));
+    const float v = __uint_as_float(w & vmask);
+    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
+        : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
+  }
+};
+template <> struct FastStep<PSELL_E8MY, __half> {
+  using Acc = float;
+  __device__ static void run(uint32_t w, uint32_t& c2, const __half* x, float& acc, uint32_t m_real,
+                             uint32_t vmask) {
+    const uint32_t f = w & 1u;
+    c2 += w & (f ? m_real : 0xFFFFFFFEu);
+    const float xv = __half2float(__ldg(reinterpret_cast<const __half*>(xbyte(x, c2))));
+    const float v = __uint_as_float(w & vmask);
+    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
+        : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
+  }
+};
+
+template <int CODEC, typename XT> struct FastPolicy {
+  static constexpr bool kHave = false;
+};
+template <> struct FastPolicy<PSELL_FP16, __half> { static constexpr bool kHave = true; };
+template <> struct FastPolicy<PSELL_FP16, float> { static constexpr bool kHave = true; };
+template <> struct FastPolicy<PSELL_E8MY, float> { static constexpr bool kHave = true; };
+template <> struct FastPolicy<PSELL_E8MY, __half> { static constexpr bool kHave = true; };
+
+template <int CODEC, typename XT, bool DOT, int U>
+__global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) {
+  using S = FastStep<CODEC, XT>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long k = s >> 5;
+  const int lane = threadIdx.x & 31;
+  double dotv = 0.0;
+  if (k < a.n_slices) {
+    const long long o0 = a.offset[k];
+    const int width = (int)((a.offset[k + 1] - o0) >> 5);
+    const uint32_t* p = static_cast<const uint32_t*>(a.pack) + o0 + lane;
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+    uint32_t c2 = 2u * (uint32_t)storage_base(a.row0 + s, a.se, a.k_left, a.n_cols);
+    float acc = 0.f;
+    uint32_t cur[U], nxt[U];
+    int q = 0;
+    if (width >= U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = __ldcs(p + u * 32);
+      // full chunks with the next full chunk in flight
+      for (; q + 2 * U <= width; q += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = __ldcs(p + (q + U + u) * 32);
+#pragma unroll
+        for (int u = 0; u < U; ++u) S::run(cur[u], c2, x, acc, m_real, vmask);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      }
+      // last full chunk, with the (partial) tail chunk in flight
+      const int rem = width - (q + U);
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = (u < rem) ? __ldcs(p + (q + U + u) * 32) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) S::run(cur[u], c2, x, acc, m_real, vmask);
+      q += U;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = (u < width) ? __ldcs(p + u * 32) : 0u;
+    }
+    if (q < width) {
+      // tail: zero words beyond the width only advance nothing (delta 0, FMA off)
+#pragma unroll
+      for (int u = 0; u < U; ++u) S::run(nxt[u], c2, x, acc, m_real, vmask);
+    }
+    if (s < a.n_rows) {
+      const long long o = out_row(a, s);
+      XT yv;
+      if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+      else yv = acc;
+      static_cast<XT*>(a.y)[o] = yv;
+      if constexpr (DOT) dotv = (double)a.p_own[o] * (double)to_f<XT>(yv);
+    }
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
 // ---- generic C: thread per storage row, slice k = s / C
 template <int CODEC, typename XT, bool REF, bool DOT>
 __global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const SpmvArgs a) {
@@ -233,7 +362,10 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
     const long long rows = a.n_slices * 32;
     const unsigned grid = (unsigned)ceil_div(rows, kBlock);
     constexpr int U = sizeof(typename WordOf<CODEC>::T) == 4 ? 8 : 4;
-    spmv_c32_kernel<CODEC, XT, REF, DOT, U><<<grid, kBlock, 0, st>>>(a);
+    if constexpr (!REF && FastPolicy<CODEC, XT>::kHave)
+      spmv_fast_kernel<CODEC, XT, DOT, 8><<<grid, kBlock, 0, st>>>(a);
+    else
+      spmv_c32_kernel<CODEC, XT, REF, DOT, U><<<grid, kBlock, 0, st>>>(a);
   } else {
     const unsigned grid = (unsigned)ceil_div(a.n_rows, kBlock);
     spmv_generic_kernel<CODEC, XT, REF, DOT><<<grid, kBlock, 0, st>>>(a);
@@ -261,7 +393,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   if (!d) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null descriptor");
   if (!fmt_valid(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid PackFormat");
   if (d->c < 1) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid C");
-  if (d->mode == PSELL_MODE_IMPLICIT && (!perm || d->sigma < 1))
+  if (d->mode == PSELL_MODE_IMPLICIT && d->n_rows > 0 && (!perm || d->sigma < 1))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "implicit mode needs perm");
   if (d->n_cols >= (1ll << 31) || d->n_rows >= (1ll << 31))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "dimensions exceed 32-bit indexing");
