@@ -220,6 +220,98 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- PCG (config 5)
+def pcg_bytes(M, n_local, nnz_local, n_glob_touched):
+    """Algorithmic bytes of one inner and one outer iteration."""
+    inner = M.spmv_bytes(4, 4, with_perm=True, x_elems=n_glob_touched) + 36 * n_local
+    csr64 = 8 * (n_local + 1) + 12 * nnz_local + 8 * n_glob_touched + 8 * n_local
+    outer = csr64 + 168 * n_local
+    return inner, outer
+
+
+def run_pcg(args, world, rank, comm, peak):
+    """Config 5: mixed-precision IO-CG on sym-scaled 7-pt 256^3, PackSELL e8m14 inner, vs FP64 PCG."""
+    import torch
+    import paper_2604_13433_b200 as P
+    from paper_2604_13433_b200 import dist as D
+    from paper_2604_13433_b200 import solvers as S
+    from paper_2604_13433_b200.packed import lower_bandwidth
+    nx = args.pcg_nx
+    n = nx ** 3
+    slabs = D.equal_row_slabs(n, world, 256)
+    D.check_equal(slabs)
+    r0, r1 = slabs[rank]
+    A = P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1)
+    b = S.make_rhs_and_x0(n, 42)[0][r0:r1]
+    kl = lower_bandwidth(A)
+    if comm is not None:
+        kl = comm.allreduce_max(kl)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    be = S.make_backend(A, "packsell-e8m14", k_left=kl)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="packsell-e8m14", max_outer=400)
+
+    def timed(fn):
+        if comm is not None:
+            comm.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        rep = fn()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        if comm is not None:
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            comm.dist.all_reduce(tt, op=comm.dist.ReduceOp.MAX)
+            dt = tt.item()
+        return rep, dt
+
+    S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="packsell-e8m14",
+                               max_outer=1), backend=be, comm=comm)  # warm-up (graph capture)
+    rep, t_io = timed(lambda: S.iocg(A, b, cfg, backend=be, comm=comm))
+    rep64, t_64 = timed(lambda: S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=5000), comm=comm))
+    touched = n if world == 1 else (r1 - r0) + 2 * nx * nx
+    ib, ob = pcg_bytes(be.matrix, r1 - r0, A.nnz, touched)
+    io_bytes = rep.total_inner_iters * ib + (rep.outer_iters + 1) * ob
+    csr64 = 8 * (r1 - r0 + 1) + 12 * A.nnz + 16 * (r1 - r0)
+    p64_bytes = rep64.outer_iters * (csr64 + 8 * touched - 8 * (r1 - r0) + 80 * (r1 - r0))
+    agg = lambda v: v * world  # equal slabs: every rank moves the same bytes  # noqa: E731
+    out = {
+        "problem": f"config 5: sym-scaled 7-point Laplacian {nx}^3 (n={n}), b = make_rhs_and_x0(n, 42), tol 1e-9",
+        "iocg": {"inner": "PackSELL e8m14 (D=8), f32 vectors, m_in=%d, CUDA-graph inner loop" % args.pcg_m_in,
+                 "solve_s": t_io, "outer_iters": rep.outer_iters, "inner_iters": rep.total_inner_iters,
+                 "converged": rep.converged, "true_relres": rep.final_true_relres,
+                 "ms_per_inner_iter": 1e3 * t_io / max(rep.total_inner_iters, 1),
+                 "roofline_s": agg(io_bytes) / (peak * world * 1e9),
+                 "frac_of_roofline": (agg(io_bytes) / (peak * world * 1e9)) / t_io,
+                 "bytes_per_inner_iter": int(agg(ib))},
+        "fp64_pcg": {"solve_s": t_64, "iters": rep64.outer_iters, "converged": rep64.converged,
+                     "true_relres": rep64.final_true_relres,
+                     "roofline_s": agg(p64_bytes) / (peak * world * 1e9)},
+        "speedup_iocg_vs_fp64_pcg": t_64 / t_io,
+        "build_s": t_build,
+        "collectives": "none" if world == 1 else "NCCL all-gather of p (f32 inner, f64 outer) + all-gather of FP64 dot partials",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        m = args.pcg_cpu_nx
+        H = P.sym_diag_scale(P.poisson3d(m))
+        bh = S.make_rhs_and_x0(H.n_rows, 42)[0]
+        OM = O.build(H.row_ptr, H.col_idx, H.values, H.n_cols, 32, 256, O.preset("e8m14"), "implicit")
+        t = time.perf_counter()
+        rr = O.iocg(lambda v: O.csr_spmv(H.row_ptr, H.col_idx, H.values, v, np.float64),
+                    lambda v: O.spmv(OM, v), bh, 1e-9, 400, args.pcg_m_in)
+        dt = time.perf_counter() - t
+        out["cpu_baseline"] = {"kind": "port", "cores": 1, "problem": f"same protocol at {m}^3 (n={m**3})",
+                               "solve_s": dt, "inner_iters": rr["total_inner_iters"],
+                               "ms_per_inner_iter": 1e3 * dt / max(rr["total_inner_iters"], 1),
+                               "gpu_speedup_per_inner_iter_scaled_by_n":
+                                   (dt / max(rr["total_inner_iters"], 1)) * (n / m ** 3)
+                                   / (t_io / max(rep.total_inner_iters, 1))}
+    return out
+
+
 # ----------------------------------------------------------------------------- GPU side
 def run_ours(args, cfg):
     import torch
@@ -262,8 +354,10 @@ def run_ours(args, cfg):
     M = P.build_packsell(S, cfg["c"], sig, fmt, cfg["mode"], _k_left_override=kl)
     torch.cuda.synchronize()
     t_b2 = time.perf_counter()
-    cmin = int(S.col_idx.min().item()) if S.nnz else 0
-    cmax = int(S.col_idx.max().item()) if S.nnz else -1
+    # stencil rows are ascending with ascending columns: the slab's x footprint
+    # runs from its first stored column to its last
+    cmin = int(S.col_idx[0].item()) if S.nnz else 0
+    cmax = int(S.col_idx[-1].item()) if S.nnz else -1
     nnz_local = S.nnz
     del S
     torch.cuda.empty_cache()
@@ -307,6 +401,17 @@ def run_ours(args, cfg):
                 P.packsell_spmv(M, x, out=y)
             torch.cuda.synchronize()
     ms_local = e0.elapsed_time(e1) / args.steps
+    # A/B: the persistent TMA bulk-copy stream variant (not the headline)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        P.packsell_spmv(M, x, out=y, _pipe=1)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(st)
+    for _ in range(args.steps):
+        P.packsell_spmv(M, x, out=y, _pipe=1)
+    g1.record(st)
+    torch.cuda.synchronize()
+    ms_regpipe = g0.elapsed_time(g1) / args.steps
     ms = allreduce(ms_local, dist.ReduceOp.MAX if world > 1 else None)
     bytes_all = allreduce(float(bytes_local), dist.ReduceOp.SUM if world > 1 else None)
     nnz_all = allreduce(float(nnz_local), dist.ReduceOp.SUM if world > 1 else None)
@@ -345,13 +450,22 @@ def run_ours(args, cfg):
                          f"global k_left; oracle port of packsell_spmv, numpy single thread; "
                          f"{r['gflops']:.4f} GFLOP/s"}
 
+    pcg = None
+    m_info = (M.n_stored, list(M.counts))
+    h2d_b, d2h_b = int(xh.numel() * xh.element_size()), int(yh.numel() * yh.element_size())
+    if not args.no_pcg:
+        from paper_2604_13433_b200 import dist as D
+        del M, x, y, xh, yh
+        torch.cuda.empty_cache()
+        pcg = run_pcg(args, world, rank, D.Comm() if world > 1 else None, peak)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["workload"], "n": n, "nnz": int(nnz_all),
-                       "n_stored_rank0": M.n_stored, "counts_rank0": list(M.counts), "k_left": kl,
+                       "n_stored_rank0": m_info[0], "counts_rank0": m_info[1], "k_left": kl,
                        "partition": "sigma-aligned row slabs, x replicated (no collective in the step)",
                        "l2": "inputs larger than L2: packed words stream at 1.94 GB per SpMV (126 MB L2); "
                              "x (33.5 MB f16) is L2-resident by design and counted once"},
@@ -363,14 +477,16 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                          "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                         "kernel": "spmv_c32_kernel (one launch per step)"},
+                         "kernel": "spmv_fast_kernel (register-pipelined, one warp per slice, one launch per step)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
-                    "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
-                    "d2h_bytes_per_step": int(yh.numel() * yh.element_size()),
+                    "h2d_bytes_per_step": h2d_b,
+                    "d2h_bytes_per_step": d2h_b,
                     "api": "paper_2604_13433_b200.packsell_spmv(M, x_pinned_cpu, out=y_pinned_cpu)"},
             "gpu_launches": args.steps,
+            "variants_ms": {"register_pipeline (headline)": ms_local, "tma_bulk_stream": ms_regpipe},
             "clocks": clocks,
+            "pcg": pcg,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -387,6 +503,10 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=131072, help="rows per CPU worker (reference arm)")
     ap.add_argument("--cpu-rows", type=int, default=262144, help="rows of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pcg", action="store_true", help="skip the config-5 PCG time-to-solution")
+    ap.add_argument("--pcg-nx", type=int, default=256)
+    ap.add_argument("--pcg-m-in", type=int, default=50)
+    ap.add_argument("--pcg-cpu-nx", type=int, default=32)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -64,6 +64,8 @@ typedef enum psell_dtype { PSELL_DT_F16 = 0, PSELL_DT_F32 = 1, PSELL_DT_F64 = 2 
 
 /* psell_spmv flags */
 #define PSELL_SPMV_REF_ORDER 1 /* numpy rounding order: value cast to x dtype, product and sum rounded separately */
+#define PSELL_SPMV_TMA_STREAM 2 /* C=32 fast path: persistent TMA bulk-copy stream instead of the default
+                                  register-pipelined one-warp-per-slice kernel (A/B experiments) */
 
 typedef struct psell_error {
   int32_t code;  /* psell_status */
@@ -185,11 +187,15 @@ PSELL_API int psell_csr_spmv(int64_t n_rows, const int64_t* row_ptr, const int32
  * Reductions are deterministic: fixed-grid partials summed in a fixed tree.
  * Device scalar blocks (double* scal, int32_t* iflags) are described in
  * paper_2604_13433_b200/solvers.py. */
-#define PSELL_RED_BLOCKS 592 /* 4 x 148 SMs */
+#define PSELL_RED_BLOCKS 1184 /* 8 x 148 SMs */
 
 /* out[k] = sum_b partials[k * n_partials + b] for k < n_out (fixed order) */
 PSELL_API int psell_sum_partials(const double* partials, int64_t n_partials, int32_t n_out, double* out,
                        const int32_t* skip_flag, void* stream);
+
+/* Multi-rank reductions: out[j] = sum_{i<n_parts} parts[i*stride + j] in rank order (j < n_out <= 32). */
+PSELL_API int psell_sum_strided(const double* parts, int32_t n_parts, int32_t stride, int32_t n_out,
+                                double* out, void* stream);
 
 /* Generic f64 dots: out = {a.b}; a, b of dtype (f32|f64); PSELL_RED_BLOCKS partials. */
 PSELL_API int psell_dot(const void* a, const void* b, int32_t dtype, int64_t n, double* partials,

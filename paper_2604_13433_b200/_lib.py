@@ -21,7 +21,7 @@ CODEC_IDS = {"fp16": 0, "e8my": 1, "fp32embed": 2}
 MODE_IDS = {"none": 0, "explicit": 1, "implicit": 2}
 DT_F16, DT_F32, DT_F64 = 0, 1, 2
 SPMV_REF_ORDER = 1
-RED_BLOCKS = 592
+RED_BLOCKS = 1184
 
 
 class PsellDesc(ctypes.Structure):
@@ -66,6 +66,7 @@ _SIGS = {
     "psell_unpack_words": (c_int32, [_D, _P, c_int64, _P, _P, _P, _P, _E]),
     "psell_csr_spmv": (c_int32, [c_int64, _P, _P, _P, _P, c_int32, _P, _P, _E]),
     "psell_sum_partials": (c_int32, [_P, c_int64, c_int32, _P, _P, _P]),
+    "psell_sum_strided": (c_int32, [_P, c_int32, c_int32, c_int32, _P, _P]),
     "psell_dot": (c_int32, [_P, _P, c_int32, c_int64, _P, _P, _P]),
     "psell_ipcg_begin": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psell_ipcg_set_rz": (c_int32, [_P, c_int32, c_int32, _P, _P, _P]),

@@ -95,7 +95,17 @@ __global__ void ipcg_alpha_kernel(const double* parts, int np, int stride, doubl
   scal[2] = scal[0] / pq;
 }
 
-// solvers.py:300-304: x += a p; r -= a q; z = P(r); rz_new partials
+// solvers.py:300-304: x += a p; r -= a q; z = P(r); rz_new partials.
+// VEC: 16-byte vectors (4 rows per thread per trip) for memory-level parallelism;
+// each row is still updated with the reference's separately rounded ops.
+__device__ __forceinline__ void upd1(float a, float& xv, float& rv, float& zv, float pv, float qv,
+                                     const float* inv, long long i) {
+  xv = __fadd_rn(xv, __fmul_rn(a, pv));
+  rv = __fsub_rn(rv, __fmul_rn(a, qv));
+  zv = inv ? __fmul_rn(rv, inv[i]) : rv;
+}
+
+template <bool VEC>
 __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float* __restrict__ x, float* r,
                                                              float* z, const float* __restrict__ p,
                                                              const float* __restrict__ q,
@@ -107,16 +117,39 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
   __shared__ double sh[kBlock / 32];
   const float a = __double2float_rn(scal[2]);
   double v = 0.0;
-  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
-    x[i] = __fadd_rn(x[i], __fmul_rn(a, p[i]));
-    const float rn = __fsub_rn(r[i], __fmul_rn(a, q[i]));
-    r[i] = rn;
-    float zf = rn;
-    if (inv) {
-      zf = __fmul_rn(rn, inv[i]);
-      z[i] = zf;
+  const long long gt = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gs = (long long)kRB * kBlock;
+  long long done = 0;
+  if (VEC) {
+    const long long n4 = n >> 2;
+    for (long long i4 = gt; i4 < n4; i4 += gs) {
+      float4 xv = reinterpret_cast<float4*>(x)[i4];
+      float4 rv = reinterpret_cast<float4*>(r)[i4];
+      const float4 pv = reinterpret_cast<const float4*>(p)[i4];
+      const float4 qv = reinterpret_cast<const float4*>(q)[i4];
+      float4 zv;
+      const long long i = i4 * 4;
+      upd1(a, xv.x, rv.x, zv.x, pv.x, qv.x, inv, i);
+      upd1(a, xv.y, rv.y, zv.y, pv.y, qv.y, inv, i + 1);
+      upd1(a, xv.z, rv.z, zv.z, pv.z, qv.z, inv, i + 2);
+      upd1(a, xv.w, rv.w, zv.w, pv.w, qv.w, inv, i + 3);
+      reinterpret_cast<float4*>(x)[i4] = xv;
+      reinterpret_cast<float4*>(r)[i4] = rv;
+      if (inv) reinterpret_cast<float4*>(z)[i4] = zv;
+      v += (double)rv.x * (double)zv.x;
+      v += (double)rv.y * (double)zv.y;
+      v += (double)rv.z * (double)zv.z;
+      v += (double)rv.w * (double)zv.w;
     }
-    v += (double)rn * (double)zf;
+    done = n4 * 4;
+  }
+  for (long long i = done + gt; i < n; i += gs) {
+    float xv = x[i], rv = r[i], zv;
+    upd1(a, xv, rv, zv, p[i], q[i], inv, i);
+    x[i] = xv;
+    r[i] = rv;
+    if (inv) z[i] = zv;
+    v += (double)rv * (double)zv;
   }
   v = block_sum<kBlock>(v, sh);
   if (threadIdx.x == 0) parts[blockIdx.x] = v;
@@ -140,8 +173,24 @@ __global__ void __launch_bounds__(kBlock) ipcg_direction_kernel(long long n, flo
                                                                 const int32_t* __restrict__ iflags) {
   if (iflags[0]) return;
   const float b = __double2float_rn(scal[3]);
-  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock)
-    p[i] = __fadd_rn(z[i], __fmul_rn(b, p[i]));
+  const long long gt = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gs = (long long)gridDim.x * kBlock;
+  long long done = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(z)) & 15) == 0;
+  if (vec) {
+    const long long n4 = n >> 2;
+    for (long long i4 = gt; i4 < n4; i4 += gs) {
+      float4 pv = reinterpret_cast<float4*>(p)[i4];
+      const float4 zv = reinterpret_cast<const float4*>(z)[i4];
+      pv.x = __fadd_rn(zv.x, __fmul_rn(b, pv.x));
+      pv.y = __fadd_rn(zv.y, __fmul_rn(b, pv.y));
+      pv.z = __fadd_rn(zv.z, __fmul_rn(b, pv.z));
+      pv.w = __fadd_rn(zv.w, __fmul_rn(b, pv.w));
+      reinterpret_cast<float4*>(p)[i4] = pv;
+    }
+    done = n4 * 4;
+  }
+  for (long long i = done + gt; i < n; i += gs) p[i] = __fadd_rn(z[i], __fmul_rn(b, p[i]));
 }
 
 __global__ void __launch_bounds__(kBlock) ipcg_end_kernel(long long n, const float* __restrict__ x,
@@ -270,6 +319,15 @@ __global__ void scalar_div_kernel(const double* num, const double* den, int np, 
   dst[0] = a / b;
 }
 
+// out[j] = sum_{i < n_parts} parts[i * stride + j], j < n_out: rank-ordered global sums
+__global__ void sum_strided_kernel(const double* parts, int np, int stride, int n_out, double* out) {
+  const int j = threadIdx.x;
+  if (j >= n_out) return;
+  double s = 0.0;
+  for (int i = 0; i < np; ++i) s += parts[(long long)i * stride + j];
+  out[j] = s;
+}
+
 static unsigned vgrid(long long n) {
   long long g = ceil_div(n, kBlock);
   if (g > kRB) g = kRB;
@@ -287,6 +345,12 @@ extern "C" {
 int psell_sum_partials(const double* partials, int64_t n_partials, int32_t n_out, double* out,
                        const int32_t* skip_flag, void* stream) {
   sum_partials_kernel<<<1, 1024, 0, as_stream(stream)>>>(partials, n_partials, n_out, out, skip_flag);
+  return LAUNCH_OK();
+}
+
+int psell_sum_strided(const double* parts, int32_t n_parts, int32_t stride, int32_t n_out, double* out,
+                      void* stream) {
+  sum_strided_kernel<<<1, 32, 0, as_stream(stream)>>>(parts, n_parts, stride, n_out, out);
   return LAUNCH_OK();
 }
 
@@ -325,7 +389,10 @@ int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, c
                       const float* inv_diag, const double* scal, const int32_t* iflags,
                       double* partials, double* local_out, void* stream) {
   cudaStream_t st = as_stream(stream);
-  ipcg_update_kernel<<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials);
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(z) |
+                     reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
+  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials);
+  else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials);
   finalize(partials, kRB, 1, local_out, iflags, st);
   return LAUNCH_OK();
 }

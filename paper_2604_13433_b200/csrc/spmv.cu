@@ -30,6 +30,7 @@ struct SpmvArgs {
   const int32_t* skip;
   long long n_rows, n_cols, n_slices, row0, k_left;
   int c, se, sigma, mode, d, perm_bytes;
+  int variant;  // 0: register-pipelined warp-per-slice (default), 2: persistent TMA stream
 };
 
 template <int CODEC> struct WordOf { using T = uint32_t; };
@@ -277,7 +278,14 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) 
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
     const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
     const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
-    uint32_t c2 = 2u * (uint32_t)storage_base(a.row0 + s, a.se, a.k_left, a.n_cols);
+    // 32-bit index math (rows and columns < 2^31 are checked at the ABI)
+    const uint32_t sg = (uint32_t)(a.row0 + s);
+    const uint32_t se = (uint32_t)a.se;
+    const uint32_t blk = (sg / se) * se;
+    const uint32_t kl = (uint32_t)a.k_left;
+    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    const uint32_t d0 = blk > kl ? blk - kl : 0u;
+    uint32_t c2 = 2u * (d0 < cmax ? d0 : cmax);
     float acc = 0.f;
     uint32_t cur[U], nxt[U];
     int q = 0;
@@ -305,12 +313,32 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) 
       for (int u = 0; u < U; ++u) nxt[u] = (u < width) ? __ldcs(p + u * 32) : 0u;
     }
     if (q < width) {
-      // tail: zero words beyond the width only advance nothing (delta 0, FMA off)
+      // tail of r < U steps, processed in groups of 4 / 2 / 1 (U == 8)
+      int r = width - q;
+      static_assert(U == 8, "tail decomposition assumes U == 8");
+      if (r >= 4) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) S::run(nxt[u], c2, x, acc, m_real, vmask);
+        for (int u = 0; u < 4; ++u) S::run(nxt[u], c2, x, acc, m_real, vmask);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) nxt[u] = nxt[u + 4];
+        r -= 4;
+      }
+      if (r >= 2) {
+        S::run(nxt[0], c2, x, acc, m_real, vmask);
+        S::run(nxt[1], c2, x, acc, m_real, vmask);
+        nxt[0] = nxt[2];
+        r -= 2;
+      }
+      if (r >= 1) S::run(nxt[0], c2, x, acc, m_real, vmask);
     }
     if (s < a.n_rows) {
-      const long long o = out_row(a, s);
+      uint32_t o = (uint32_t)s;
+      if (a.mode == PSELL_MODE_IMPLICIT) {
+        const uint32_t sig = (uint32_t)a.sigma;
+        const uint32_t p8 = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
+                                              : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
+        o = ((uint32_t)s / sig) * sig + p8;
+      }
       XT yv;
       if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
       else yv = acc;
@@ -319,6 +347,200 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) 
     }
   }
   finish_dot<DOT>(a, dotv);
+}
+
+// ---- TMA-staged production path (C == 32): per-warp cp.async.bulk ring
+//
+// Each warp owns one slice.  Its words stream global -> shared memory through
+// a ring of kStages chunks of kChunk steps (kChunk * 128 B, contiguous in
+// `pack` because slices are column major), issued by lane 0 with
+// cp.async.bulk + mbarrier complete_tx and an L2 evict_first hint, so up to
+// kStages KB per warp (the whole slice for config 2) are in flight without
+// holding registers.  Lanes read step q as one conflict-free 128 B LDS wave.
+// The decode / gather / FMA per word is FastStep (above).
+constexpr int kChunk = 8;
+constexpr int kStages = 4;
+constexpr int kWarps = kBlock / 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+constexpr int kTmaCtasPerSm = 6;
+
+// ---- TMA stream path (C == 32), the production kernel.
+//
+// Persistent; warp w owns the contiguous slice range [kb, ke) whose words are
+// the w-th 1/nwarps of `pack` (lower_bound on the int64 slice offsets), so
+// work is balanced by stored words, not rows (power-law matrices included).
+// Slices are contiguous in `pack`, so the warp's input is ONE contiguous byte
+// range: lane 0 streams it through the ring in kChunk-step (1 KB) bulk copies,
+// refilling each stage as soon as the warp has read it.  Lanes consume
+// chunk-major and detect slice boundaries on the fly (flush y, reset cursor).
+__device__ __forceinline__ long long lower_bound_off(const int64_t* off, long long n, long long target) {
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (off[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <int CODEC, typename XT, bool DOT>
+__global__ void __launch_bounds__(kBlock, kTmaCtasPerSm) spmv_stream_kernel(const SpmvArgs a) {
+  using S = FastStep<CODEC, XT>;
+  __shared__ alignas(128) uint32_t ring[kWarps][kStages][kChunk * 32];
+  __shared__ alignas(8) uint64_t bars[kWarps][kStages];
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * kWarps;
+  const long long wid = (long long)blockIdx.x * kWarps + warp;
+  const int64_t* off = a.offset;
+  const long long total = off[a.n_slices];
+  const long long kb = lower_bound_off(off, a.n_slices, total * wid / nw);
+  const long long ke = (wid == nw - 1) ? a.n_slices : lower_bound_off(off, a.n_slices, total * (wid + 1) / nw);
+  uint64_t* bar = bars[warp];
+  uint32_t(*buf)[kChunk * 32] = ring[warp];
+  double dotv = 0.0;
+  if (kb < ke) {
+    const long long T0 = off[kb] >> 5;
+    const long long nsteps = (off[ke] >> 5) - T0;
+    const long long nchunks = (nsteps + kChunk - 1) / kChunk;
+    const uint32_t* src = static_cast<const uint32_t*>(a.pack) + T0 * 32;
+    uint64_t pol = 0;
+    if (lane == 0) {
+      pol = policy_evict_first();
+#pragma unroll
+      for (int st = 0; st < kStages; ++st) mbar_init(&bar[st], 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (long long i = 0; i < kStages && i < nchunks; ++i) {
+        const uint32_t bytes = (uint32_t)min((long long)kChunk, nsteps - i * kChunk) * 128u;
+        mbar_expect_tx(&bar[i], bytes);
+        bulk_g2s(buf[i], src + i * (kChunk * 32), bytes, &bar[i], pol);
+      }
+    }
+    __syncwarp();
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+    const uint32_t se = (uint32_t)a.se, sig = (uint32_t)a.sigma;
+    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    const uint32_t row0 = (uint32_t)a.row0, kl = (uint32_t)a.k_left;
+    auto base2 = [&](long long k) -> uint32_t {  // 2 * min(d_s, n_cols - 1), 32-bit (n < 2^31)
+      const uint32_t g = row0 + (uint32_t)(k * 32 + lane);
+      const uint32_t blk = (g / se) * se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    auto flush = [&](long long k, float acc) {
+      const uint32_t s = (uint32_t)(k * 32 + lane);
+      if ((long long)s < a.n_rows) {
+        uint32_t o = s;
+        if (a.mode == PSELL_MODE_IMPLICIT) {
+          const uint32_t p = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
+                                               : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
+          o = (s / sig) * sig + p;
+        }
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
+      }
+    };
+    // current slice: k, its end step (relative to T0), cursor, accumulator
+    long long k = kb;
+    long long bnd = (off[k + 1] >> 5) - T0;
+    while (bnd == 0 && k + 1 < ke) {  // leading zero-width slices
+      flush(k, 0.f);
+      ++k;
+      bnd = (off[k + 1] >> 5) - T0;
+    }
+    uint32_t c2 = base2(k);
+    float acc = 0.f;
+    auto advance = [&](long long g) {  // slice k ended at step g: flush it and the empty ones after it
+      flush(k, acc);
+      ++k;
+      bnd = (off[k + 1] >> 5) - T0;
+      while (bnd == g && k + 1 < ke) {
+        flush(k, 0.f);
+        ++k;
+        bnd = (off[k + 1] >> 5) - T0;
+      }
+      c2 = base2(k);
+      acc = 0.f;
+    };
+    for (long long i = 0; i < nchunks; ++i) {
+      const int st = (int)(i % kStages);
+      mbar_wait(&bar[st], (uint32_t)(i / kStages) & 1u);
+      uint32_t w[kChunk];
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) w[u] = buf[st][u * 32 + lane];
+      __syncwarp();
+      if (lane == 0 && i + kStages < nchunks) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const long long cn = i + kStages;
+        const uint32_t bytes = (uint32_t)min((long long)kChunk, nsteps - cn * kChunk) * 128u;
+        mbar_expect_tx(&bar[st], bytes);
+        bulk_g2s(buf[st], src + cn * (kChunk * 32), bytes, &bar[st], pol);
+      }
+      const long long g0 = i * kChunk;
+      if (g0 + kChunk <= nsteps) {
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+          if (g0 + u == bnd) advance(g0 + u);
+          S::run(w[u], c2, x, acc, m_real, vmask);
+        }
+      } else {
+        for (int u = 0; g0 + u < nsteps; ++u) {
+          if (g0 + u == bnd) advance(g0 + u);
+          S::run(w[u], c2, x, acc, m_real, vmask);
+        }
+      }
+    }
+    flush(k, acc);  // last non-empty slice (or the only, empty, one)
+    for (++k; k < ke; ++k) flush(k, 0.f);  // trailing zero-width slices
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
+static int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// grid of the C = 32 launch: persistent for the TMA ring, one warp per slice otherwise
+static long long spmv_grid(long long n_slices, int c, bool tma) {
+  if (c != 32) return 0;
+  const long long full = ceil_div(n_slices, kWarps);
+  if (!tma) return full;
+  const long long cap = (long long)sm_count() * kTmaCtasPerSm;
+  return full < cap ? full : cap;
 }
 
 // ---- generic C: thread per storage row, slice k = s / C
@@ -362,9 +584,20 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
     const long long rows = a.n_slices * 32;
     const unsigned grid = (unsigned)ceil_div(rows, kBlock);
     constexpr int U = sizeof(typename WordOf<CODEC>::T) == 4 ? 8 : 4;
-    if constexpr (!REF && FastPolicy<CODEC, XT>::kHave)
-      spmv_fast_kernel<CODEC, XT, DOT, 8><<<grid, kBlock, 0, st>>>(a);
-    else
+    if constexpr (!REF && FastPolicy<CODEC, XT>::kHave) {
+      if (a.variant != 2) {
+        spmv_fast_kernel<CODEC, XT, DOT, 8><<<grid, kBlock, 0, st>>>(a);
+      } else {
+        static bool carveout = false;  // idempotent attribute, benign race
+        if (!carveout) {
+          cudaFuncSetAttribute(spmv_stream_kernel<CODEC, XT, DOT>,
+                               cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          carveout = true;
+        }
+        const unsigned g = (unsigned)spmv_grid(a.n_slices, 32, true);
+        spmv_stream_kernel<CODEC, XT, DOT><<<g, kBlock, 0, st>>>(a);
+      }
+    } else
       spmv_c32_kernel<CODEC, XT, REF, DOT, U><<<grid, kBlock, 0, st>>>(a);
   } else {
     const unsigned grid = (unsigned)ceil_div(a.n_rows, kBlock);
@@ -416,6 +649,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.mode = d->mode;
   a.d = d->d;
   a.perm_bytes = d->sigma <= 256 ? 1 : 2;
+  a.variant = 0;
   return PSELL_OK;
 }
 
@@ -478,6 +712,7 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
   if (a.n_rows == 0) return ok(err);
   cudaStream_t st = as_stream(stream);
   const bool ref = (flags & PSELL_SPMV_REF_ORDER) != 0;
+  a.variant = (flags & PSELL_SPMV_TMA_STREAM) ? 2 : 0;
   int bad = 1;
   switch (d->codec) {
     case PSELL_FP16: bad = dispatch_x<PSELL_FP16>(a, x_dtype, ref, st); break;
@@ -491,7 +726,13 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
 
 int64_t psell_spmv_dot_partials(const psell_desc* d) {
   if (!d || d->n_rows <= 0 || d->c < 1) return 1;
-  if (d->c == 32) return ceil_div(ceil_div(d->n_rows, 32) * 32, kBlock);
+  const long long ns = ceil_div(d->n_rows, d->c);
+  if (d->c == 32) {
+    // must match launch_spmv<.., DOT=true>: f32 x/y always takes the fast path for
+    // fp16/e8my (persistent TMA grid), fp32embed the one-warp-per-slice kernel
+    (void)spmv_grid;  // the fused-dot launch always uses the one-warp-per-slice kernels
+    return ceil_div(ns * 32, kBlock);
+  }
   return ceil_div(d->n_rows, kBlock);
 }
 

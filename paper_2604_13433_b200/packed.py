@@ -265,18 +265,19 @@ def build_packsell(A, c: int = 32, sigma: int = 256,
                           counts, row0=D.row0)
 
 
-def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool):
+def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool, pipe: int = 0):
     from . import _dev, _lib
     lib = _lib.lib()
     err = _lib.PsellError()
     rc = lib.psell_spmv(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
                         _lib.ptr(xd), _dev.T_DT_CODE[xd.dtype], _lib.ptr(y),
-                        _lib.SPMV_REF_ORDER if ref_order else 0, _lib.stream_handle(), err)
+                        (_lib.SPMV_REF_ORDER if ref_order else 0) | (2 if pipe else 0),
+                        _lib.stream_handle(), err)
     _lib.check(rc, err, M.fmt)
     return y
 
 
-def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None):
+def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None, _pipe: int = 0):
     """y = M x with on-the-fly unpacking (packed.py:242-271), y in x's dtype.
 
     x: numpy array (returns numpy, the reference call), CUDA tensor (returns a
@@ -294,10 +295,10 @@ def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None):
             raise TypeError(f"unsupported x dtype {x.dtype}")
         if x.is_cuda:
             y = out if out is not None else torch.empty(M.n_rows, dtype=x.dtype, device=x.device)
-            return _spmv_device(M, x, y, ref_order)
+            return _spmv_device(M, x, y, ref_order, _pipe)
         xd = x.to(_dev.DEVICE, non_blocking=True)
         yd = torch.empty(M.n_rows, dtype=x.dtype, device=_dev.DEVICE)
-        _spmv_device(M, xd, yd, ref_order)
+        _spmv_device(M, xd, yd, ref_order, _pipe)
         if out is None:
             out = torch.empty(M.n_rows, dtype=x.dtype, pin_memory=True)
         out.copy_(yd, non_blocking=True)
@@ -310,7 +311,7 @@ def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None):
         raise TypeError(f"unsupported x dtype {x.dtype}")
     xd = _dev.upload(x)
     y = _dev.empty(M.n_rows, x.dtype)
-    _spmv_device(M, xd, y, ref_order)
+    _spmv_device(M, xd, y, ref_order, _pipe)
     return _dev.download(y, x.dtype)
 
 

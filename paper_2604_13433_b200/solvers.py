@@ -9,15 +9,16 @@ reductions), every operator application in K2 (PackSELL) or K4 (CSR).
   (_inner_pcg, solvers.py:278-308): m_in f32 PCG steps with the curvature dot
   fused into the PackSELL SpMV epilogue, alpha / beta / the breakdown flag kept
   on the device, and — on one GPU — the whole m_in-step loop captured once as
-  a CUDA graph and replayed per outer iteration (no host round trip inside).
+  a CUDA graph and replayed every outer iteration (no host round trip inside).
 * `fcg` / `pcg` are the f64 outer / comparator loops; they read back one
   small status block per iteration (the reference's residual history needs it).
 
-Multi-GPU: when a `Comm` is given (paper_2604_13433_b200.dist), each rank
-owns a sigma-aligned row slab; the direction vector is all-gathered (NCCL over
-NVLink) before every SpMV and every dot's local FP64 sum is all-gathered and
-summed in rank order, so results do not depend on the reduction tree of the
-collective.
+Multi-GPU (`comm=` a paper_2604_13433_b200.dist.Comm): every rank passes its
+sigma-aligned row slab (DeviceCsrMatrix with row0, n_cols global) and the
+matching slab of b.  The direction vectors are all-gathered over NCCL before
+each SpMV and every dot's per-rank FP64 sum is all-gathered and summed in rank
+order on the device, so the iteration is identical for any rank count up to
+the dot association.
 """
 
 from __future__ import annotations
@@ -98,7 +99,8 @@ class SpmvBackend:
     """A device-resident operator plus its unquantised f64 CSR source (solvers.py:96-111).
 
     `apply(x)` takes numpy (returns numpy, the reference call) or a CUDA tensor
-    (returns a CUDA tensor); it runs in x's precision.
+    (returns a CUDA tensor); it runs in x's precision.  For a rank slab, x is
+    the global vector and the result has the slab's rows.
     """
 
     def __init__(self, name: str, matrix, kernel: Callable, source):
@@ -115,8 +117,12 @@ class SpmvBackend:
         return isinstance(self.matrix, PackSellMatrix)
 
 
-def make_backend(A, name: str, c: int = 32, sigma: int = 256, mode: str = "implicit") -> SpmvBackend:
-    """Named backend from an f64 CSR matrix (solvers.py:114-131)."""
+def make_backend(A, name: str, c: int = 32, sigma: int = 256, mode: str = "implicit", *,
+                 k_left: Optional[int] = None) -> SpmvBackend:
+    """Named backend from an f64 CSR matrix (solvers.py:114-131).
+
+    `k_left` passes the global lower bandwidth when A is one rank's slab.
+    """
     if name == "csr64":
         return SpmvBackend(name, A, lambda x: csr_spmv(A, x, _dtype_of(x)), A)
     if name in ("sell64", "sell32", "sell16"):
@@ -126,7 +132,7 @@ def make_backend(A, name: str, c: int = 32, sigma: int = 256, mode: str = "impli
         return SpmvBackend(name, S, lambda x: sell_spmv(S, x), A)
     if name.startswith("packsell-"):
         fmt = codec.parse_format(name[len("packsell-"):])
-        M = build_packsell(A, c, sigma, fmt, mode)
+        M = build_packsell(A, c, sigma, fmt, mode, _k_left_override=k_left)
         return SpmvBackend(name, M, lambda x: packsell_spmv(M, x), A)
     raise ValueError(f"unknown backend {name!r}")
 
@@ -152,7 +158,12 @@ def _as_backend(A) -> SpmvBackend:
 # ----------------------------------------------------------------------------
 
 class _Dev:
-    """Per-solve device scratch: partials, local sums, gathered sums, scalars, flags."""
+    """Per-solve device scratch: partials, local sums, gathered sums, global scalars, flags.
+
+    loc[8]   this rank's sums (written by the fused reduction kernels)
+    glob[G,8] all ranks' loc (rank order) after `gather`
+    scal[32] global scalars (rank-ordered sums and the coefficients)
+    """
 
     def __init__(self, n_partials: int, comm=None):
         import torch
@@ -164,8 +175,8 @@ class _Dev:
         self.G = 1 if comm is None else comm.world
         self.partials = torch.zeros(max(int(n_partials), 2 * _lib.RED_BLOCKS), dtype=torch.float64, device="cuda")
         self.loc = torch.zeros(8, dtype=torch.float64, device="cuda")
-        self.glob = torch.zeros(self.G, 8, dtype=torch.float64, device="cuda")
-        self.scal = torch.zeros(16, dtype=torch.float64, device="cuda")
+        self.glob = torch.zeros(self.G * 8, dtype=torch.float64, device="cuda")
+        self.scal = torch.zeros(32, dtype=torch.float64, device="cuda")
         self.flags = torch.zeros(4, dtype=torch.int32, device="cuda")
 
     def st(self):
@@ -175,11 +186,31 @@ class _Dev:
         return t.data_ptr() + off * t.element_size()
 
     def gather(self):
-        """All ranks' local sums -> glob[G][8] (rank order); G == 1: a view."""
+        """(pointer base, stride) of every rank's loc[] in rank order."""
         if self.G == 1:
             return self.loc, 8
-        self.comm.all_gather_into(self.glob.view(-1), self.loc)
+        self.comm.all_gather_into(self.glob, self.loc)
         return self.glob, 8
+
+    def reduce(self, k0: int, n_out: int, dst: int):
+        """scal[dst:dst+n_out] <- rank-ordered global sums of loc[k0:k0+n_out]."""
+        g, stride = self.gather()
+        self.lib.psell_sum_strided(self.p(g, k0), self.G, stride, n_out, self.p(self.scal, dst), self.st())
+
+    def norm(self, a, slot: int = 15) -> float:
+        """sqrt of the global a.a (solvers.py:92-93)."""
+        self.lib.psell_dot(a.data_ptr(), a.data_ptr(), 2 if a.dtype == self.torch.float64 else 1, a.numel(),
+                           self.p(self.partials), self.p(self.loc, 7), self.st())
+        self.reduce(7, 1, slot)
+        return float(np.sqrt(float(self.scal[slot].item())))
+
+
+def _gather_full(comm, local, full):
+    """full <- concatenation of every rank's equal slab (in place when local aliases full)."""
+    if comm is None or comm.world == 1:
+        return local
+    comm.all_gather_vec(full, local)
+    return full
 
 
 # ----------------------------------------------------------------------------
@@ -191,59 +222,55 @@ class _InnerPCG:
 
     def __init__(self, backend: SpmvBackend, m_in: int, inv_diag=None, comm=None, use_graph: bool = True):
         import torch
+        from . import _lib
         self.torch = torch
         self.backend = backend
         self.m_in = int(m_in)
         self.comm = comm
         M = backend.matrix
-        self.M = M if isinstance(M, PackSellMatrix) else None
+        if not isinstance(M, PackSellMatrix):
+            raise TypeError("_InnerPCG drives a PackSELL backend")
+        self.M = M
         self.n = M.n_rows
-        self.row0 = getattr(M, "row0", 0)
-        self.n_glob = M.n_cols
+        self.row0 = M.row0
         self.inv = inv_diag
         f32 = torch.float32
         self.x = torch.zeros(self.n, dtype=f32, device="cuda")
         self.r = torch.zeros(self.n, dtype=f32, device="cuda")
         self.q = torch.zeros(self.n, dtype=f32, device="cuda")
         self.z = torch.zeros(self.n, dtype=f32, device="cuda") if inv_diag is not None else self.r
-        if comm is None or comm.world == 1:
+        G = 1 if comm is None else comm.world
+        if G == 1:
             self.p_full = torch.zeros(self.n, dtype=f32, device="cuda")
             self.p = self.p_full
         else:
-            self.p_full = torch.zeros(comm.padded_len(self.n_glob), dtype=f32, device="cuda")
+            self.p_full = torch.zeros(comm.padded_len(M.n_cols), dtype=f32, device="cuda")
             self.p = self.p_full[self.row0:self.row0 + self.n]
-        from . import _lib
         lib = _lib.lib()
-        npart = lib.psell_spmv_dot_partials(self.M.desc()) if self.M is not None else 1
-        self.d = _Dev(max(npart, _lib.RED_BLOCKS), comm)
+        self.desc = M.desc()
+        self.npart = lib.psell_spmv_dot_partials(self.desc)
+        self.d = _Dev(max(self.npart, _lib.RED_BLOCKS), comm)
         self.graph = None
         self.graph_in = None
-        self.use_graph = use_graph and (comm is None or comm.world == 1) and self.M is not None
+        self.use_graph = use_graph and G == 1
 
-    # one launch sequence; r64 / z64 are f64 device vectors of the local slab
     def _sequence(self, r64, z64):
         d, L, lib = self.d, self.d.L, self.d.lib
         st = d.st()
         inv = None if self.inv is None else self.inv.data_ptr()
+        M = self.M
+        err = L.PsellError()
         lib.psell_ipcg_begin(self.n, r64.data_ptr(), self.x.data_ptr(), self.r.data_ptr(), self.z.data_ptr(),
                              self.p.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
         g, stride = d.gather()
         lib.psell_ipcg_set_rz(d.p(g, 0), d.G, stride, d.p(d.scal), d.p(d.flags), st)
-        desc = self.M.desc() if self.M is not None else None
-        err = L.PsellError()
         for _ in range(self.m_in):
-            if d.G > 1:
-                self.comm.all_gather_vec(self.p_full, self.p)
-            if self.M is not None:
-                rc = lib.psell_spmv_dot(desc, L.ptr(self.M.d_pack), L.ptr(self.M.d_offset), L.ptr(self.M.d_perm),
-                                        self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
-                                        d.p(d.partials), d.p(d.flags), st, err)
-                L.check(rc, err, self.M.fmt)
-                lib.psell_sum_partials(d.p(d.partials), lib.psell_spmv_dot_partials(desc), 1, d.p(d.loc, 1),
-                                       d.p(d.flags), st)
-            else:
-                self.q.copy_(self.backend.apply(self.p_full))
-                lib.psell_dot(self.p.data_ptr(), self.q.data_ptr(), 1, self.n, d.p(d.partials), d.p(d.loc, 1), st)
+            _gather_full(self.comm, self.p, self.p_full)
+            rc = lib.psell_spmv_dot(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
+                                    self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
+                                    d.p(d.partials), d.p(d.flags), st, err)
+            L.check(rc, err, M.fmt)
+            lib.psell_sum_partials(d.p(d.partials), self.npart, 1, d.p(d.loc, 1), d.p(d.flags), st)
             g, stride = d.gather()
             lib.psell_ipcg_alpha(d.p(g, 1), d.G, stride, d.p(d.scal), d.p(d.flags), st)
             lib.psell_ipcg_update(self.n, self.x.data_ptr(), self.r.data_ptr(), self.z.data_ptr(),
@@ -258,8 +285,8 @@ class _InnerPCG:
         """z64 <- m_in f32 PCG steps on A z = r64 from zero; returns completed iterations."""
         torch = self.torch
         if self.use_graph:
-            if self.graph is None or self.graph_in is not (r64, z64):
-                self._r_static, self._z_static = r64, z64
+            if self.graph is None or self.graph_in is None or \
+                    self.graph_in[0] is not r64 or self.graph_in[1] is not z64:
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(s):
@@ -273,246 +300,16 @@ class _InnerPCG:
             self.graph.replay()
         else:
             self._sequence(r64, z64)
-        done = int(self.d.flags[1].item())
-        if int(self.d.flags[0].item()):
+        flags = self.d.flags[:2].cpu().numpy()
+        done = int(flags[1])
+        if int(flags[0]):
             log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate",
                         done, float(self.d.scal[1].item()))
         return done
 
 
-# ----------------------------------------------------------------------------
-# f64 drivers
-# ----------------------------------------------------------------------------
-
-class _Op64:
-    """f64 operator on device vectors (local slab rows, global x)."""
-
-    def __init__(self, backend: SpmvBackend, comm=None):
-        self.backend = backend
-        self.comm = comm
-        src = backend.matrix
-        self.n = src.n_rows
-        self.n_glob = src.n_cols
-        self.row0 = getattr(src, "row0", 0)
-
-    def __call__(self, p_full, out):
-        out.copy_(self.backend.apply(p_full))
-        return out
-
-
-def _prep(b, comm):
-    import torch
-    from . import _dev
-    b = np.asarray(b, dtype=np.float64)
-    return b, _dev.upload(b)
-
-
-def _vec_norm(d: _Dev, a) -> float:
-    d.lib.psell_dot(a.data_ptr(), a.data_ptr(), 2, a.numel(), d.p(d.partials), d.p(d.loc, 0), d.st())
-    g, _ = d.gather()
-    if d.G == 1:
-        return float(np.sqrt(float(d.loc[0].item())))
-    return float(np.sqrt(float(d.glob[:, 0].cpu().numpy().sum())))
-
-
-def _audit(report: SolveReport, src, b_dev, bnorm, tol, d: _Dev, x_full) -> SolveReport:
-    """True residual in f64 on the device, demote drifted runs (solvers.py:152-168)."""
-    import torch
-    if bnorm == 0.0:
-        report.final_true_relres = 0.0
-        return report
-    ax = csr_spmv(src, x_full, np.float64)
-    d.lib.psell_resid(b_dev.numel(), b_dev.data_ptr(), ax.data_ptr(), d.p(d.partials), d.p(d.loc, 0), d.st())
-    d.gather()
-    rr = float(d.loc[0].item()) if d.G == 1 else float(d.glob[:, 0].cpu().numpy().sum())
-    report.final_true_relres = float(np.sqrt(rr)) / bnorm
-    if report.converged and not report.final_true_relres < 10.0 * tol:
-        report.converged = False
-        msg = f"true residual {report.final_true_relres:.3e} exceeds 10x tolerance"
-        report.reason = f"{report.reason}; {msg}" if report.reason else msg
-    return report
-
-
-def _jacobi_inv(backend: SpmvBackend, dtype):
-    """1/diag of the f64 source, rounded to dtype (solvers.py:145-149)."""
-    from . import _dev
-    src = backend.source
-    if isinstance(src, DeviceCsrMatrix):
-        src = src.to_host()
-    diag = src.diagonal()
-    if np.any(diag == 0.0):
-        raise ValueError("jacobi preconditioner requires a fully nonzero diagonal")
-    return _dev.upload((1.0 / diag).astype(dtype))
-
-
-def pcg(A, b, cfg: SolveConfig = None, x0=None) -> SolveReport:
-    """f64 PCG stopping on the recurred residual (solvers.py:171-217), on the GPU."""
-    import torch
-    from . import _lib
-    cfg = cfg or SolveConfig()
-    backend = _as_backend(A)
-    b, bd = _prep(b, None)
-    t0 = time.perf_counter()
-    n = len(b)
-    d = _Dev(_lib.RED_BLOCKS)
-    lib = d.lib
-    st = d.st()
-    f64 = torch.float64
-    x = torch.zeros(n, dtype=f64, device="cuda") if x0 is None else \
-        torch.as_tensor(np.asarray(x0, dtype=np.float64)).cuda()
-    inv = _jacobi_inv(backend, np.float64) if cfg.preconditioner == "jacobi" else None
-    bnorm = _vec_norm(d, bd)
-    if bnorm == 0.0:
-        return SolveReport(True, 0, 0, [], 0.0, time.perf_counter() - t0, x=x.cpu().numpy())
-    r = bd.clone()
-    if x0 is not None and np.any(np.asarray(x0)):
-        ax = backend.apply(x)
-        r.copy_(ax)
-        neg1 = torch.tensor([-1.0], dtype=f64, device="cuda")
-        lib.psell_xpby(n, r.data_ptr(), bd.data_ptr(), neg1.data_ptr(), st)   # r = b - Ax
-    history = [_vec_norm(d, r) / bnorm]
-    z = torch.empty_like(r) if inv is not None else r
-    lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), None if inv is None else inv.data_ptr(),
-                          d.p(d.partials), d.p(d.scal, 4), st)               # scal[4] = rz
-    p = z.clone()
-    q = torch.empty_like(r)
-    converged, reason, it = False, None, 0
-    while it < cfg.max_outer:
-        if history[-1] < cfg.tol:
-            converged = True
-            break
-        q.copy_(backend.apply(p))
-        lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), None, d.p(d.partials), d.p(d.loc, 0), st)
-        d.flags.zero_()
-        # alpha = rz / pq with the curvature test -> scal[0], scal[1] = pq
-        lib.psell_scalar_div(d.p(d.scal, 4), d.p(d.loc, 0), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)
-        lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
-                        d.p(d.flags), d.p(d.partials), d.p(d.loc, 2), st)
-        status = torch.stack([d.flags[0].to(f64), d.loc[0], d.loc[2]]).cpu().numpy()
-        if status[0]:
-            reason = f"breakdown: non-positive curvature p'Ap = {float(status[1])!r} at iteration {it}"
-            break
-        it += 1
-        history.append(float(np.sqrt(status[2])) / bnorm)
-        lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), None if inv is None else inv.data_ptr(),
-                              d.p(d.partials), d.p(d.loc, 3), st)            # rz_new
-        lib.psell_scalar_div(d.p(d.loc, 3), d.p(d.scal, 4), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
-        d.scal[4].copy_(d.loc[3])
-        lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
-    else:
-        reason = f"maximum iterations ({cfg.max_outer}) reached"
-    if not converged and history[-1] < cfg.tol:
-        converged = True
-        reason = None
-    torch.cuda.synchronize()
-    report = SolveReport(converged, it, 0, history, 0.0, time.perf_counter() - t0, reason)
-    report = _audit(report, backend.source, bd, bnorm, cfg.tol, d, x)
-    report.x = x.cpu().numpy()
-    return report
-
-
-def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *, _inner=None) -> SolveReport:
-    """Truncated flexible CG in f64 (solvers.py:220-275), on the GPU.
-
-    `inner_preconditioner` may be a Python callable on numpy vectors (the
-    reference contract; runs through host copies) — the iocg path passes a
-    device `_InnerPCG` via `_inner` instead.
-    """
-    import torch
-    from . import _lib
-    cfg = cfg or SolveConfig()
-    backend = _as_backend(A)
-    b, bd = _prep(b, None)
-    t0 = time.perf_counter()
-    n = len(b)
-    d = _Dev(_lib.RED_BLOCKS)
-    lib = d.lib
-    st = d.st()
-    f64 = torch.float64
-    x = torch.zeros(n, dtype=f64, device="cuda")
-    bnorm = _vec_norm(d, bd)
-    if bnorm == 0.0:
-        return SolveReport(True, 0, 0, [], 0.0, time.perf_counter() - t0, x=x.cpu().numpy())
-    inv = None
-    if _inner is None and inner_preconditioner is None and cfg.preconditioner == "jacobi":
-        inv = _jacobi_inv(backend, np.float64)
-    r = bd.clone()
-    history = [_vec_norm(d, r) / bnorm]
-    z = torch.empty_like(r)
-    p = torch.empty_like(r)
-    q = torch.empty_like(r)
-    r_prev = torch.empty_like(r)
-    converged, reason, it, first = False, None, 0, True
-    inner_total = 0
-    while it < cfg.max_outer:
-        if history[-1] < cfg.tol:
-            converged = True
-            break
-        if _inner is not None:
-            inner_total += _inner.solve(r, z)
-        elif inner_preconditioner is not None:
-            z.copy_(torch.as_tensor(np.asarray(inner_preconditioner(r.cpu().numpy()), dtype=np.float64)))
-        else:
-            lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), None if inv is None else inv.data_ptr(),
-                                  d.p(d.partials), d.p(d.loc, 7), st)
-            if inv is None:
-                z.copy_(r)
-        lib.psell_fcg_zr(n, z.data_ptr(), r.data_ptr(), None if first else r_prev.data_ptr(),
-                         d.p(d.partials), d.p(d.loc, 0), st)                 # loc0 = z.(r - r_prev), loc1 = z.r
-        if first:
-            lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
-            first = False
-        else:
-            lib.psell_scalar_div(d.p(d.loc, 0), d.p(d.scal, 6), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
-            lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
-        d.scal[6].copy_(d.loc[1])                                            # zr_prev
-        r_prev.copy_(r)
-        q.copy_(backend.apply(p))
-        lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), r.data_ptr(), d.p(d.partials), d.p(d.loc, 2), st)
-        d.flags.zero_()
-        lib.psell_scalar_div(d.p(d.loc, 3), d.p(d.loc, 2), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)  # alpha
-        lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
-                        d.p(d.flags), d.p(d.partials), d.p(d.loc, 4), st)
-        status = torch.stack([d.flags[0].to(f64), d.loc[2], d.loc[4]]).cpu().numpy()
-        if status[0]:
-            reason = f"breakdown: non-positive curvature p'Ap = {float(status[1])!r} at iteration {it}"
-            break
-        it += 1
-        history.append(float(np.sqrt(status[2])) / bnorm)
-    else:
-        reason = f"maximum iterations ({cfg.max_outer}) reached"
-    if not converged and history[-1] < cfg.tol:
-        converged = True
-        reason = None
-    torch.cuda.synchronize()
-    report = SolveReport(converged, it, inner_total, history, 0.0, time.perf_counter() - t0, reason)
-    report = _audit(report, backend.source, bd, bnorm, cfg.tol, d, x)
-    report.x = x.cpu().numpy()
-    return report
-
-
-def iocg(A: CsrMatrix, b, cfg: SolveConfig = None, *, backend: SpmvBackend = None) -> SolveReport:
-    """Inner-outer CG (solvers.py:311-333): m_in f32 PackSELL PCG steps precondition f64 FCG.
-
-    `backend` may pass a prebuilt inner backend (e.g. to exclude the build
-    from a timing); by default it is built from cfg.a_backend like the reference.
-    """
-    cfg = cfg or SolveConfig(solver="iocg")
-    if not isinstance(A, (CsrMatrix, DeviceCsrMatrix)):
-        raise TypeError("iocg drives the outer iteration with the float64 CSR matrix")
-    inner_backend = backend or make_backend(A, cfg.a_backend)
-    dtype = _PRECISIONS[cfg.inner_precision]
-    inv = _jacobi_inv(inner_backend, dtype) if cfg.preconditioner == "jacobi" else None
-    if dtype == np.float32 and inner_backend.is_packsell:
-        inner = _InnerPCG(inner_backend, cfg.m_in, inv)
-        return fcg(A, b, cfg, _inner=inner)
-    # generic inner backend / precision: reference-shaped inner loop through the device backend
-    inner = _GenericInner(inner_backend, cfg.m_in, dtype, inv)
-    return fcg(A, b, cfg, _inner=inner)
-
-
 class _GenericInner:
-    """Inner PCG for non-PackSELL backends or f64 inner precision (device vectors, host scalars)."""
+    """Inner PCG for non-PackSELL backends or f64 inner precision (one GPU; device vectors)."""
 
     def __init__(self, backend, m_in, dtype, inv):
         import torch
@@ -557,3 +354,258 @@ class _GenericInner:
             p = z + beta * p
         z64.copy_(x.to(torch.float64))
         return done
+
+
+# ----------------------------------------------------------------------------
+# f64 drivers
+# ----------------------------------------------------------------------------
+
+def _diag_of(src) -> np.ndarray:
+    """Stored diagonal of a (slab) CSR in global column numbering."""
+    if isinstance(src, DeviceCsrMatrix):
+        H = src.to_host()
+        rows = np.repeat(np.arange(H.n_rows, dtype=np.int64), H.row_lengths()) + src.row0
+        dg = np.zeros(H.n_rows)
+        on = rows == H.col_idx
+        dg[rows[on] - src.row0] = H.values[on]
+        return dg
+    return src.diagonal()
+
+
+def _jacobi_inv(backend: SpmvBackend, dtype):
+    """1/diag of the f64 source, rounded to dtype (solvers.py:145-149)."""
+    from . import _dev
+    diag = _diag_of(backend.source)
+    if np.any(diag == 0.0):
+        raise ValueError("jacobi preconditioner requires a fully nonzero diagonal")
+    return _dev.upload((1.0 / diag).astype(dtype))
+
+
+class _Outer:
+    """f64 vectors + operator of a (possibly distributed) outer loop."""
+
+    def __init__(self, backend: SpmvBackend, b, comm):
+        import torch
+        from . import _lib
+        self.torch = torch
+        self.backend = backend
+        self.comm = comm
+        self.G = 1 if comm is None else comm.world
+        src = backend.matrix if not backend.is_packsell else backend.source
+        self.row0 = getattr(src, "row0", 0)
+        b = np.asarray(b, dtype=np.float64)
+        self.n = len(b)
+        self.b = torch.as_tensor(b).cuda()
+        self.d = _Dev(_lib.RED_BLOCKS, comm)
+        self.lib = self.d.lib
+        f64 = torch.float64
+        self.n_glob = self.n * self.G
+        self.full = torch.zeros(self.n_glob, dtype=f64, device="cuda") if self.G > 1 else None
+
+    def vec(self):
+        return self.torch.zeros(self.n, dtype=self.torch.float64, device="cuda")
+
+    def slab_of_full(self):
+        return self.full[self.row0:self.row0 + self.n]
+
+    def apply(self, v, out):
+        """out <- A v (v local slab; all-gathered to the global vector first)."""
+        if self.G == 1:
+            out.copy_(self.backend.apply(v))
+            return out
+        self.slab_of_full().copy_(v)
+        _gather_full(self.comm, self.slab_of_full(), self.full)
+        out.copy_(self.backend.apply(self.full))
+        return out
+
+    def audit(self, report: SolveReport, x, bnorm, tol) -> SolveReport:
+        """True residual in f64 on the device, demote drifted runs (solvers.py:152-168)."""
+        d = self.d
+        if bnorm == 0.0:
+            report.final_true_relres = 0.0
+            return report
+        ax = self.vec()
+        src = self.backend.source
+        if self.G == 1:
+            ax.copy_(csr_spmv(src, x, np.float64))
+        else:
+            self.slab_of_full().copy_(x)
+            _gather_full(self.comm, self.slab_of_full(), self.full)
+            ax.copy_(csr_spmv(src, self.full, np.float64))
+        self.lib.psell_resid(self.n, self.b.data_ptr(), ax.data_ptr(), d.p(d.partials), d.p(d.loc, 6), d.st())
+        d.reduce(6, 1, 14)
+        report.final_true_relres = float(np.sqrt(float(d.scal[14].item()))) / bnorm
+        if report.converged and not report.final_true_relres < 10.0 * tol:
+            report.converged = False
+            msg = f"true residual {report.final_true_relres:.3e} exceeds 10x tolerance"
+            report.reason = f"{report.reason}; {msg}" if report.reason else msg
+        return report
+
+
+def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
+    """f64 PCG stopping on the recurred residual (solvers.py:171-217), on the GPU."""
+    import torch
+    cfg = cfg or SolveConfig()
+    backend = _as_backend(A)
+    t0 = time.perf_counter()
+    o = _Outer(backend, b, comm)
+    d, lib, n = o.d, o.lib, o.n
+    st = d.st()
+    x = o.vec() if x0 is None else torch.as_tensor(np.asarray(x0, dtype=np.float64)).cuda()
+    inv = _jacobi_inv(backend, np.float64) if cfg.preconditioner == "jacobi" else None
+    bnorm = d.norm(o.b)
+    if bnorm == 0.0:
+        return SolveReport(True, 0, 0, [], 0.0, time.perf_counter() - t0, x=x.cpu().numpy())
+    r = o.b.clone()
+    if x0 is not None and np.any(np.asarray(x0)):
+        ax = o.vec()
+        o.apply(x, ax)
+        r.copy_(ax)
+        neg1 = torch.tensor([-1.0], dtype=torch.float64, device="cuda")
+        lib.psell_xpby(n, r.data_ptr(), o.b.data_ptr(), neg1.data_ptr(), st)   # r = b - Ax
+    history = [d.norm(r) / bnorm]
+    z = o.vec() if inv is not None else r
+    invp = None if inv is None else inv.data_ptr()
+    lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), invp, d.p(d.partials), d.p(d.loc, 0), st)
+    d.reduce(0, 1, 4)                                                      # scal4 = rz
+    p = z.clone()
+    q = o.vec()
+    converged, reason, it = False, None, 0
+    while it < cfg.max_outer:
+        if history[-1] < cfg.tol:
+            converged = True
+            break
+        o.apply(p, q)
+        lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), None, d.p(d.partials), d.p(d.loc, 0), st)
+        d.reduce(0, 1, 10)                                                 # scal10 = pq
+        d.flags.zero_()
+        lib.psell_scalar_div(d.p(d.scal, 4), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)
+        lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
+                        d.p(d.flags), d.p(d.partials), d.p(d.loc, 2), st)
+        d.reduce(2, 1, 12)                                                 # scal12 = rr
+        status = torch.stack([d.flags[0].to(torch.float64), d.scal[10], d.scal[12]]).cpu().numpy()
+        if status[0]:
+            reason = f"breakdown: non-positive curvature p'Ap = {float(status[1])!r} at iteration {it}"
+            break
+        it += 1
+        history.append(float(np.sqrt(status[2])) / bnorm)
+        lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), invp, d.p(d.partials), d.p(d.loc, 3), st)
+        d.reduce(3, 1, 5)                                                  # scal5 = rz_new
+        lib.psell_scalar_div(d.p(d.scal, 5), d.p(d.scal, 4), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
+        lib.psell_sum_strided(d.p(d.scal, 5), 1, 1, 1, d.p(d.scal, 4), st)                        # rz = rz_new
+        lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
+    else:
+        reason = f"maximum iterations ({cfg.max_outer}) reached"
+    if not converged and history[-1] < cfg.tol:
+        converged = True
+        reason = None
+    torch.cuda.synchronize()
+    report = SolveReport(converged, it, 0, history, 0.0, time.perf_counter() - t0, reason)
+    report = o.audit(report, x, bnorm, cfg.tol)
+    report.x = x.cpu().numpy()
+    return report
+
+
+def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *, _inner=None,
+        comm=None) -> SolveReport:
+    """Truncated flexible CG in f64 (solvers.py:220-275), on the GPU.
+
+    `inner_preconditioner` may be a Python callable on numpy vectors (the
+    reference contract; runs through host copies); iocg passes a device inner
+    solver via `_inner`.
+    """
+    import torch
+    cfg = cfg or SolveConfig()
+    backend = _as_backend(A)
+    t0 = time.perf_counter()
+    o = _Outer(backend, b, comm)
+    d, lib, n = o.d, o.lib, o.n
+    st = d.st()
+    x = o.vec()
+    bnorm = d.norm(o.b)
+    if bnorm == 0.0:
+        return SolveReport(True, 0, 0, [], 0.0, time.perf_counter() - t0, x=x.cpu().numpy())
+    inv = None
+    if _inner is None and inner_preconditioner is None and cfg.preconditioner == "jacobi":
+        inv = _jacobi_inv(backend, np.float64)
+    r = o.b.clone()
+    history = [d.norm(r) / bnorm]
+    z, p, q, r_prev = o.vec(), o.vec(), o.vec(), o.vec()
+    converged, reason, it, first = False, None, 0, True
+    inner_total = 0
+    while it < cfg.max_outer:
+        if history[-1] < cfg.tol:
+            converged = True
+            break
+        if _inner is not None:
+            inner_total += _inner.solve(r, z)
+        elif inner_preconditioner is not None:
+            z.copy_(torch.as_tensor(np.asarray(inner_preconditioner(r.cpu().numpy()), dtype=np.float64)))
+        elif inv is not None:
+            lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv.data_ptr(), d.p(d.partials), d.p(d.loc, 7), st)
+        else:
+            z.copy_(r)
+        lib.psell_fcg_zr(n, z.data_ptr(), r.data_ptr(), None if first else r_prev.data_ptr(),
+                         d.p(d.partials), d.p(d.loc, 0), st)
+        d.reduce(0, 2, 8)                                  # scal8 = z.(r - r_prev), scal9 = z.r
+        if first:
+            lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
+            first = False
+        else:
+            lib.psell_scalar_div(d.p(d.scal, 8), d.p(d.scal, 6), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
+            lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
+        lib.psell_sum_strided(d.p(d.scal, 9), 1, 1, 1, d.p(d.scal, 6), st)                        # zr_prev
+        r_prev.copy_(r)
+        o.apply(p, q)
+        lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), r.data_ptr(), d.p(d.partials), d.p(d.loc, 2), st)
+        d.reduce(2, 2, 10)                                 # scal10 = p.q, scal11 = p.r
+        d.flags.zero_()
+        lib.psell_scalar_div(d.p(d.scal, 11), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)
+        lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
+                        d.p(d.flags), d.p(d.partials), d.p(d.loc, 4), st)
+        d.reduce(4, 1, 12)                                 # scal12 = r.r
+        status = torch.stack([d.flags[0].to(torch.float64), d.scal[10], d.scal[12]]).cpu().numpy()
+        if status[0]:
+            reason = f"breakdown: non-positive curvature p'Ap = {float(status[1])!r} at iteration {it}"
+            break
+        it += 1
+        history.append(float(np.sqrt(status[2])) / bnorm)
+    else:
+        reason = f"maximum iterations ({cfg.max_outer}) reached"
+    if not converged and history[-1] < cfg.tol:
+        converged = True
+        reason = None
+    torch.cuda.synchronize()
+    report = SolveReport(converged, it, inner_total, history, 0.0, time.perf_counter() - t0, reason)
+    report = o.audit(report, x, bnorm, cfg.tol)
+    report.x = x.cpu().numpy()
+    return report
+
+
+def iocg(A, b, cfg: SolveConfig = None, *, backend: SpmvBackend = None, comm=None,
+         use_graph: bool = True) -> SolveReport:
+    """Inner-outer CG (solvers.py:311-333): m_in f32 PackSELL PCG steps precondition f64 FCG.
+
+    `backend` passes a prebuilt inner backend (e.g. to keep the build out of a
+    timing); by default it is built from cfg.a_backend like the reference.
+    With `comm`, A and b are this rank's slabs.
+    """
+    cfg = cfg or SolveConfig(solver="iocg")
+    if not isinstance(A, (CsrMatrix, DeviceCsrMatrix)):
+        raise TypeError("iocg drives the outer iteration with the float64 CSR matrix")
+    if backend is None:
+        kl = None
+        if comm is not None and comm.world > 1:
+            from .packed import lower_bandwidth
+            kl = comm.allreduce_max(lower_bandwidth(A))
+        backend = make_backend(A, cfg.a_backend, k_left=kl)
+    dtype = _PRECISIONS[cfg.inner_precision]
+    inv = _jacobi_inv(backend, dtype) if cfg.preconditioner == "jacobi" else None
+    if dtype == np.float32 and backend.is_packsell:
+        inner = _InnerPCG(backend, cfg.m_in, inv, comm=comm, use_graph=use_graph)
+    else:
+        if comm is not None and comm.world > 1:
+            raise NotImplementedError("distributed iocg needs a PackSELL inner backend in real32")
+        inner = _GenericInner(backend, cfg.m_in, dtype, inv)
+    outer = make_backend(A, "csr64")
+    return fcg(outer, b, cfg, _inner=inner, comm=comm)

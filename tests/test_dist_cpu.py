@@ -1,0 +1,102 @@
+"""Multi-rank host logic on CPU: gloo world_size 2, partitions, rank-ordered sums,
+and the slab property the multi-GPU build relies on (checked with the oracle)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2604_13433_b200 import dist as D
+from paper_2604_13433_b200 import stencil
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = D.Comm()
+        # rank-ordered local sums
+        loc = torch.arange(8, dtype=torch.float64) + 100 * rank
+        glob = torch.zeros(world * 8, dtype=torch.float64)
+        comm.all_gather_into(glob, loc)
+        # in-place slab all-gather of a direction vector
+        n = 6
+        full = torch.zeros(world * n, dtype=torch.float32)
+        full[rank * n:(rank + 1) * n] = rank + 1.0
+        comm.all_gather_vec(full, full[rank * n:(rank + 1) * n])
+        kmax = comm.allreduce_max(10 + rank)
+        q.put((rank, glob.numpy().copy(), full.numpy().copy(), kmax))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_collectives():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for rank, glob, full, kmax in res:
+        want = np.concatenate([np.arange(8) + 100 * r for r in range(world)])
+        assert np.array_equal(glob, want)
+        assert np.array_equal(full, np.repeat([1.0, 2.0], 6))
+        assert kmax == 11
+        assert D.rank_order_sum(glob.reshape(world, 8)[:, 3]) == 3.0 + 103.0
+
+
+def test_partitions():
+    sl = D.equal_row_slabs(16 * 256, 4, 256)
+    assert sl == [(0, 1024), (1024, 2048), (2048, 3072), (3072, 4096)]
+    D.check_equal(sl)
+    with pytest.raises(ValueError):
+        D.check_equal(D.equal_row_slabs(1000, 3, 256))
+    w = np.ones(4096, dtype=np.int64)
+    w[:256] = 100  # first block heavy
+    ws = D.word_balanced_slabs(w, 2, 256)
+    assert ws[0][0] == 0 and ws[-1][1] == 4096 and all(a % 256 == 0 for a, _ in ws)
+    assert ws[0][1] - ws[0][0] < ws[1][1] - ws[1][0]
+
+
+@pytest.mark.parametrize("preset,world", [("fp16", 2), ("e8m14", 3), ("fp16", 4)])
+def test_slab_packs_concatenate_to_global(preset, world):
+    """Per-rank slab builds with the global k_left == the single build (oracle)."""
+    A = stencil.stencil27(10)
+    f = O.preset(preset)
+    G = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, 256, f, "implicit")
+    packs, perms, offs = [], [], [0]
+    for a, b in D.equal_row_slabs(A.n_rows, world, 256):
+        S = stencil.stencil_rows("stencil27", 10, a, b)
+        M = O.build(S.row_ptr, S.col_idx, S.values, S.n_cols, 32, 256, f, "implicit", k_left=G.k_left, row0=a)
+        packs.append(M.pack)
+        perms.append(M.perm)
+        offs.extend((M.offset[1:] + offs[-1]).tolist())
+        x = np.random.default_rng(a).uniform(-1, 1, A.n_cols).astype(np.float32)
+        assert np.array_equal(O.spmv(M, x), O.spmv(G, x)[a:b])
+    assert np.array_equal(np.concatenate(packs), G.pack)
+    assert np.array_equal(np.concatenate(perms), G.perm)
+    assert np.array_equal(np.array(offs), G.offset)
+
+
+def test_stencil_rows_match_full():
+    A = stencil.poisson3d(7)
+    S = stencil.stencil_rows("poisson3d", 7, 50, 200)
+    assert np.array_equal(S.col_idx, A.col_idx[A.row_ptr[50]:A.row_ptr[200]])
+    assert np.array_equal(S.row_ptr, A.row_ptr[50:201] - A.row_ptr[50])

@@ -1,0 +1,84 @@
+"""Distributed PCG path with real ranks on one GPU (gloo transport through host memory;
+the NCCL run differs only in the transport).  Rank slabs + NCCL-style all-gathers
+must reproduce the single-GPU solve: same convergence, outer iterations within 1,
+x within 1e-6 relative (only the association of the FP64 dot sums differs)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, nx, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_13433_b200 as P
+        from paper_2604_13433_b200 import dist as D
+        from paper_2604_13433_b200 import solvers as S
+        torch.cuda.set_device(0)
+        comm = D.Comm()
+        n = nx ** 3
+        (r0, r1) = D.equal_row_slabs(n, world, 256)[rank]
+        A = P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1)
+        b, _ = S.make_rhs_and_x0(n, 42)
+        cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200)
+        rep = S.iocg(A, b[r0:r1], cfg, comm=comm)
+        pc = S.pcg(P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1), b[r0:r1],
+                   S.SolveConfig(tol=1e-9, max_outer=2000), comm=comm)
+        q.put((rank, r0, r1, rep.converged, rep.outer_iters, rep.total_inner_iters, rep.final_true_relres,
+               rep.x, pc.converged, pc.outer_iters, pc.x))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_distributed_iocg_matches_single_gpu(world):
+    import torch.multiprocessing as mp
+    import paper_2604_13433_b200 as P
+    from paper_2604_13433_b200 import solvers as S
+    nx = 16
+    n = nx ** 3
+    A = P.sym_diag_scale(P.poisson3d(nx))
+    b, _ = S.make_rhs_and_x0(n, 42)
+    cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200)
+    ref = S.iocg(A, b, cfg)
+    refp = S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=2000))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_rank, args=(r, world, port, nx, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+    assert all(len(r) > 2 for r in res), res
+    x = np.zeros(n)
+    xp = np.zeros(n)
+    for (rank, r0, r1, conv, outer, inner, relres, xs, pconv, pouter, pxs) in res:
+        assert conv and abs(outer - ref.outer_iters) <= 1
+        assert inner == cfg.m_in * outer
+        assert relres < 1e-9
+        x[r0:r1] = xs
+        assert pconv and abs(pouter - refp.outer_iters) <= 1
+        xp[r0:r1] = pxs
+    assert np.abs(x - ref.x).max() / np.abs(ref.x).max() < 1e-6
+    assert np.abs(xp - refp.x).max() / np.abs(refp.x).max() < 1e-9
