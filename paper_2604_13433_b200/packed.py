@@ -315,6 +315,57 @@ def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None, _p
     return _dev.download(y, x.dtype)
 
 
+def packsell_spmv_stream(M: PackSellMatrix, xs, outs=None, *, ref_order: bool = False):
+    """Pipelined SpMVs over a sequence of host vectors: y_i = M x_i.
+
+    The host<->device copies of consecutive calls overlap the SpMVs: x_{i+1}
+    uploads on a copy-in stream while y_i = M x_i computes and y_{i-1}
+    downloads on a copy-out stream (double-buffered device vectors, CUDA
+    events between the three streams).  `xs` are CPU tensors (pinned for
+    full-duplex DMA) or numpy arrays; results go to `outs` (CPU tensors) or
+    new pinned tensors.  Returns the list of outputs after a final sync.
+    """
+    import torch
+    from . import _dev
+    xs = [torch.from_numpy(np.ascontiguousarray(x)) if not _is_tensor(x) else x for x in xs]
+    if not xs:
+        return []
+    dt = xs[0].dtype
+    if dt not in _dev.T_DT_CODE:
+        raise TypeError(f"unsupported x dtype {dt}")
+    for x in xs:
+        if len(x) != M.n_cols:
+            raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
+    if outs is None:
+        outs = [torch.empty(M.n_rows, dtype=dt, pin_memory=True) for _ in xs]
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    xd = [torch.empty(M.n_cols, dtype=dt, device=_dev.DEVICE) for _ in range(2)]
+    yd = [torch.empty(M.n_rows, dtype=dt, device=_dev.DEVICE) for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    for i, x in enumerate(xs):
+        b = i & 1
+        with torch.cuda.stream(s_in):
+            if i >= 2:
+                s_in.wait_event(ev_cmp[b])        # x buffer b free (SpMV i-2 done)
+            xd[b].copy_(x, non_blocking=True)
+            ev_in[b].record(s_in)
+        comp.wait_event(ev_in[b])
+        if i >= 2:
+            comp.wait_event(ev_out[b])             # y buffer b drained (D2H i-2 done)
+        _spmv_device(M, xd[b], yd[b], ref_order)
+        ev_cmp[b].record(comp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_cmp[b])
+            outs[i].copy_(yd[b], non_blocking=True)
+            ev_out[b].record(s_out)
+    s_out.synchronize()
+    comp.wait_stream(s_out)
+    return outs
+
+
 def packsell_to_csr(M: PackSellMatrix) -> CsrMatrix:
     """Decode every delta chain back to the quantised CSR, logical row order (packed.py:274-303)."""
     from . import _dev, _lib

@@ -229,3 +229,17 @@ def test_slab_builds_concatenate_to_global(rng):
         assert np.array_equal(_bits(ys), _bits(yg[a:b]))
     assert np.array_equal(np.concatenate(packs), G.pack)
     assert np.array_equal(np.concatenate(perms), G.perm)
+
+
+def test_spmv_stream_equals_per_call(rng):
+    """The pipelined host-buffer API returns exactly the per-call results."""
+    import torch
+    A = P.stencil27(14)
+    M = P.build_packsell(A, 32, 256, P.parse_format("fp16"), "implicit")
+    xs = [torch.from_numpy(rng.uniform(-1, 1, A.n_cols).astype(np.float16)).pin_memory() for _ in range(5)]
+    outs = P.packsell_spmv_stream(M, xs)
+    for x, y in zip(xs, outs):
+        assert np.array_equal(_bits(y.numpy()), _bits(P.packsell_spmv(M, x.numpy())))
+    ys = P.packsell_spmv_stream(M, [x.numpy() for x in xs], ref_order=True)
+    for x, y in zip(xs, ys):
+        assert np.array_equal(_bits(y.numpy()), _bits(P.packsell_spmv(M, x.numpy(), ref_order=True)))
