@@ -142,6 +142,26 @@ PSELL_API int psell_spmv(const psell_desc* desc, const void* pack, const int64_t
                const void* x, int32_t x_dtype, void* y, int32_t flags, void* stream,
                psell_error* err);
 
+/* Long-slice segmentation for irregular (power-law) matrices.  Slices wider than
+ * seg_len steps are cut into segments (seg_slice/seg_q0: the slice and first
+ * step of each; long_slice/long_seg0: the long slices and their first segment,
+ * n_long + 1 entries).  psell_spmv_seg_checkpoints fills seg_c2[n_seg][32] with
+ * each lane's cursor (2 * column) before the segment, once per matrix;
+ * psell_spmv_segmented then runs short slices one warp each and every segment
+ * on its own warp, combining the segment partials of a row in segment order.
+ * C = 32, W = 32 (fp16 / e8my), f16 / f32 x.  FMA accumulation. */
+PSELL_API int psell_spmv_seg_checkpoints(const psell_desc* desc, const void* pack, const int64_t* offset,
+                                         int32_t seg_len, int64_t n_seg, const int32_t* seg_slice,
+                                         const int32_t* seg_q0, int64_t n_long, const int32_t* long_slice,
+                                         const int32_t* long_seg0, uint32_t* seg_c2, void* stream,
+                                         psell_error* err);
+PSELL_API int psell_spmv_segmented(const psell_desc* desc, const void* pack, const int64_t* offset,
+                                   const void* perm, const void* x, int32_t x_dtype, void* y,
+                                   int32_t seg_len, int64_t n_seg, const int32_t* seg_slice,
+                                   const int32_t* seg_q0, const uint32_t* seg_c2, float* seg_partial,
+                                   int64_t n_long, const int32_t* long_slice, const int32_t* long_seg0,
+                                   void* stream, psell_error* err);
+
 /* Number of double partials psell_spmv_dot writes (one per CTA). */
 PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc);
 
@@ -257,6 +277,16 @@ PSELL_API int psell_gen_stencil_fill(int64_t d0, int64_t d1, int64_t d2, int32_t
                                      int32_t scale, int64_t row_begin, int64_t row_end,
                                      const int64_t* row_ptr, int32_t* col_idx, double* values,
                                      void* stream, psell_error* err);
+
+/* Config-4 power-law matrix (counter-based splitmix64 law in csrc/gen.cu), rows
+ * [row_begin, row_end) of an n x n matrix; reproduced bit for bit on the host by
+ * paper_2604_13433_b200.stencil.powerlaw_rows. */
+PSELL_API int psell_gen_powerlaw_plan(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin, int64_t row_end,
+                                      void* workspace, size_t ws_bytes, int64_t* row_ptr,
+                                      int64_t* nnz_host, void* stream, psell_error* err);
+PSELL_API int psell_gen_powerlaw_fill(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin, int64_t row_end,
+                                      const int64_t* row_ptr, int32_t* col_idx, double* values,
+                                      void* stream, psell_error* err);
 
 #ifdef __cplusplus
 }

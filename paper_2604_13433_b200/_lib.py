@@ -55,6 +55,9 @@ _SIGS = {
     "psell_sort_workspace_bytes": (c_size_t, [c_int64, c_int32]),
     "psell_sort_order": (c_int32, [_P, c_int64, c_int32, _P, _P, c_size_t, _P, _E]),
     "psell_spmv": (c_int32, [_D, _P, _P, _P, _P, c_int32, _P, c_int32, _P, _E]),
+    "psell_spmv_seg_checkpoints": (c_int32, [_D, _P, _P, c_int32, c_int64, _P, _P, c_int64, _P, _P, _P, _P, _E]),
+    "psell_spmv_segmented": (c_int32, [_D, _P, _P, _P, _P, c_int32, _P, c_int32, c_int64, _P, _P, _P, _P,
+                                       c_int64, _P, _P, _P, _E]),
     "psell_spmv_dot_partials": (c_int64, [_D]),
     "psell_spmv_dot": (c_int32, [_D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _E]),
     "psell_to_csr_workspace_bytes": (c_size_t, [_D]),
@@ -83,6 +86,9 @@ _SIGS = {
     "psell_precond_dot": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P]),
     "psell_scalar_div": (c_int32, [_P, _P, c_int32, c_int32, _P, _P, c_int32, _P]),
     "psell_gen_workspace_bytes": (c_size_t, [c_int64]),
+    "psell_gen_powerlaw_plan": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, c_size_t, _P,
+                                          POINTER(c_int64), _P, _E]),
+    "psell_gen_powerlaw_fill": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, _P, _P, _P, _E]),
     "psell_gen_stencil_plan": (c_int32, [c_int64, c_int64, c_int64, c_int32, c_double, c_int64, c_int64,
                                          _P, c_size_t, _P, POINTER(c_int64), _P, _E]),
     "psell_gen_stencil_fill": (c_int32, [c_int64, c_int64, c_int64, c_int32, c_double, c_int32, c_int64,

@@ -73,9 +73,110 @@ __global__ void gen_kernel(Grid g, long long r0, long long r1, long long* __rest
   }
 }
 
+// ---------------------------------------------------------------- power-law (config 4)
+// Counter-based: every random number is splitmix64(seed, row, stream, j), so a
+// row can be generated independently (GPU slab, CPU sample) and the host
+// mirror (stencil.powerlaw_rows) reproduces it bit for bit.
+// Only integer hashing and correctly rounded IEEE ops (sqrt, div, mul, add) are
+// used, so numpy reproduces every draw exactly:
+//   u     = (h >> 11) * 2^-53
+//   L_i   = max{k <= 8192 : u <= T_k},  T_k = (4/k)^1.5 from a host table
+//           (= min(8192, floor(4 u^(-2/3))): Pareto alpha 1.5 tail, mean ~12)
+//   G_i   = max(1, 8192 / L_i); start = max(0, i - 4096)
+//   col_{j+1} = col_j + 1 + h1 % (2 G_i)            (a band of ~16K columns around i)
+//             + (h2 % 5 == 0 ? h5 % max(1, n / (8 L_i)) : 0)   (far jumps, bounded total drift)
+//   the walk stops at n (the row is truncated); value = (0.01 + 0.99 u4) * (h3 & 1 ? -1 : 1)
+__host__ __device__ __forceinline__ uint64_t smix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t hrow(uint64_t seed, long long row) {
+  return smix(seed ^ ((uint64_t)row * 0xD1B54A32D192ED03ull));
+}
+__device__ __forceinline__ uint64_t hdraw(uint64_t hr, int stream, long long j) {
+  return smix(hr ^ ((uint64_t)stream << 56) ^ (uint64_t)j);
+}
+__device__ __forceinline__ double u53(uint64_t h) { return (double)(h >> 11) * (1.0 / 9007199254740992.0); }
+
+struct PlParams {
+  long long n;
+  uint64_t seed;
+  const double* thr;  // T_1..T_8192 at thr[0..8191], non-increasing
+};
+
+template <bool FILL>
+__global__ void powerlaw_kernel(PlParams P, long long r0, long long r1, long long* __restrict__ counts,
+                                const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                double* __restrict__ val) {
+  const long long i = r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  const uint64_t hr = hrow(P.seed, i);
+  const double u = u53(hdraw(hr, 0, 0));
+  // L = number of leading thresholds >= u (binary search on the non-increasing table)
+  int lo = 0, hi = 8192;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (P.thr[mid] >= u) lo = mid + 1;
+    else hi = mid;
+  }
+  const long long L = lo < 1 ? 1 : lo;
+  const uint64_t G2 = 2ull * (uint64_t)(8192 / L > 1 ? 8192 / L : 1);
+  const long long fj = P.n / (8 * L);
+  const uint64_t far = (uint64_t)(fj > 0 ? fj : 1);
+  long long c = i - 4096;
+  if (c < 0) c = 0;
+  long long t = FILL ? row_ptr[i - r0] : 0;
+  long long cnt = 0;
+  for (long long j = 0; j < L && c < P.n; ++j) {
+    if (FILL) {
+      col[t] = (int32_t)c;
+      const double m = __dadd_rn(0.01, __dmul_rn(0.99, u53(hdraw(hr, 4, j))));
+      val[t] = (hdraw(hr, 3, j) & 1ull) ? -m : m;
+      ++t;
+    }
+    ++cnt;
+    c += 1 + (long long)(hdraw(hr, 1, j) % G2);
+    if (hdraw(hr, 2, j) % 5ull == 0ull) c += (long long)(hdraw(hr, 5, j) % far);
+  }
+  if (!FILL) counts[i - r0] = cnt;
+}
+
 }  // namespace psell
 
 using namespace psell;
+
+extern "C" PSELL_API int psell_gen_powerlaw_plan(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin, int64_t row_end,
+                                                 void* ws, size_t ws_bytes, int64_t* row_ptr,
+                                                 int64_t* nnz_host, void* stream, psell_error* err) {
+  const long long m = row_end - row_begin;
+  if (m < 0 || row_end > n) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "bad row range");
+  if (!ws || ws_bytes < psell_gen_workspace_bytes(m)) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  long long* counts = static_cast<long long*>(ws);
+  long long* tmp = reinterpret_cast<long long*>(static_cast<char*>(ws) + align_up(8 * (size_t)(m > 0 ? m : 1)));
+  PlParams P{n, seed, thresholds};
+  if (m > 0) powerlaw_kernel<false><<<(unsigned)ceil_div(m, kBlock), kBlock, 0, st>>>(P, row_begin, row_end, counts, nullptr, nullptr, nullptr);
+  PSELL_CHECK_LAUNCH(err, "powerlaw_count");
+  if (int rc = scan_i64(counts, m, tmp, reinterpret_cast<long long*>(row_ptr), st, err)) return rc;
+  long long nnz = 0;
+  PSELL_CUDA(cudaMemcpyAsync(&nnz, row_ptr + m, 8, cudaMemcpyDeviceToHost, st), err);
+  PSELL_CUDA(cudaStreamSynchronize(st), err);
+  *nnz_host = nnz;
+  return ok(err);
+}
+
+extern "C" PSELL_API int psell_gen_powerlaw_fill(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin, int64_t row_end,
+                                                 const int64_t* row_ptr, int32_t* col_idx, double* values,
+                                                 void* stream, psell_error* err) {
+  const long long m = row_end - row_begin;
+  if (m <= 0) return ok(err);
+  PlParams P{n, seed, thresholds};
+  powerlaw_kernel<true><<<(unsigned)ceil_div(m, kBlock), kBlock, 0, as_stream(stream)>>>(P, row_begin, row_end, nullptr, row_ptr, col_idx, values);
+  PSELL_CHECK_LAUNCH(err, "powerlaw_fill");
+  return ok(err);
+}
 
 extern "C" {
 

@@ -32,6 +32,16 @@ struct SpmvArgs {
   int c, se, sigma, mode, d, perm_bytes;
   int variant;  // 0: register-pipelined warp-per-slice (default), 2: persistent TMA stream
   int spw;      // slices per warp of the multi-slice kernel (1: warp-per-slice kernel)
+  int codec;
+  // long-slice segmentation (0 = off): slices wider than seg_len steps run as
+  // segments (see spmv_seg_kernel)
+  int seg_len;
+  const int32_t* seg_slice;   // [n_seg] slice of each segment
+  const int32_t* seg_q0;      // [n_seg] first step of each segment
+  uint32_t* seg_c2;           // [n_seg][32] cursor checkpoints (2 * column)
+  float* seg_partial;         // [n_seg][32] partial sums
+  const int32_t* long_slice;  // [n_long] slices run as segments
+  const int32_t* long_seg0;   // [n_long + 1] first segment of each long slice
 };
 
 template <int CODEC> struct WordOf { using T = uint32_t; };
@@ -278,6 +288,8 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) 
     // the hidden latency.)
     const long long o0 = a.offset[k];
     const int width = (int)((a.offset[k + 1] - o0) >> 5);
+    if (a.seg_len > 0 && width > a.seg_len) goto done;  // long slice: segment kernels own it
+    {
     const uint32_t* p = static_cast<const uint32_t*>(a.pack) + o0 + lane;
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
     const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
@@ -349,8 +361,116 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) 
       static_cast<XT*>(a.y)[o] = yv;
       if constexpr (DOT) dotv = (double)a.p_own[o] * (double)to_f<XT>(yv);
     }
+    }
   }
+done:
   finish_dot<DOT>(a, dotv);
+}
+
+// ---- long slices (power-law rows): segments of seg_len steps per warp.
+// The column cursor of a delta chain cannot start mid-row, so each segment
+// carries a checkpoint: 2 * column of every lane before its first step
+// (psell_spmv_seg_checkpoints, computed once per matrix).  Segment partial
+// sums land in `partial` and a combine pass adds them in segment order
+// (deterministic) and writes y through the permutation.
+__device__ __forceinline__ uint32_t word_c2(uint32_t w, uint32_t m_real) {
+  return w & ((w & 1u) ? m_real : 0xFFFFFFFEu);
+}
+
+// checkpoint pass 1: per segment and lane, sum of 2*delta over the segment's steps
+__global__ void __launch_bounds__(kBlock) seg_dsum_kernel(const SpmvArgs a, long long n_seg) {
+  const long long sg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sg >= n_seg) return;
+  const int k = a.seg_slice[sg];
+  const int q0 = a.seg_q0[sg];
+  const long long o0 = a.offset[k];
+  const int width = (int)((a.offset[k + 1] - o0) >> 5);
+  const int q1 = min(q0 + a.seg_len, width);
+  const uint32_t* p = static_cast<const uint32_t*>(a.pack) + o0 + lane;
+  const uint32_t m_real = a.codec == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+  uint32_t s = 0;
+  for (int q = q0; q < q1; ++q) s += word_c2(__ldg(p + (long long)q * 32), m_real);
+  a.seg_c2[sg * 32 + lane] = s;
+}
+
+// checkpoint pass 2: per long slice, exclusive prefix of the segment sums + base
+__global__ void __launch_bounds__(kBlock) seg_prefix_kernel(const SpmvArgs a, long long n_long) {
+  const long long l = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (l >= n_long) return;
+  const int k = a.long_slice[l];
+  const uint32_t g = (uint32_t)a.row0 + (uint32_t)k * 32u + lane;
+  const uint32_t se = (uint32_t)a.se, kl = (uint32_t)a.k_left;
+  const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+  const uint32_t blk = (g / se) * se;
+  const uint32_t d0 = blk > kl ? blk - kl : 0u;
+  uint32_t run = 2u * (d0 < cmax ? d0 : cmax);
+  for (int sgi = a.long_seg0[l]; sgi < a.long_seg0[l + 1]; ++sgi) {
+    const uint32_t t = a.seg_c2[(long long)sgi * 32 + lane];
+    a.seg_c2[(long long)sgi * 32 + lane] = run;
+    run += t;
+  }
+}
+
+template <int CODEC, typename XT, int U>
+__global__ void __launch_bounds__(kBlock, 6) spmv_seg_kernel(const SpmvArgs a, long long n_seg) {
+  using S = FastStep<CODEC, XT>;
+  const long long sg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sg >= n_seg) return;
+  const int k = a.seg_slice[sg];
+  const int q0 = a.seg_q0[sg];
+  const long long o0 = a.offset[k];
+  const int width = (int)((a.offset[k + 1] - o0) >> 5);
+  const int nst = min(a.seg_len, width - q0);
+  const uint32_t* p = static_cast<const uint32_t*>(a.pack) + o0 + (long long)q0 * 32 + lane;
+  const XT* __restrict__ x = static_cast<const XT*>(a.x);
+  const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+  const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+  uint32_t c2 = a.seg_c2[sg * 32 + lane];
+  float acc = 0.f;
+  uint32_t cur[U], nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cur[u] = (u < nst) ? __ldcs(p + u * 32) : 0u;
+  for (int q = 0; q < nst; q += U) {
+    const int qn = q + U;
+    if (qn + U <= nst) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = __ldcs(p + (qn + u) * 32);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = (qn + u < nst) ? __ldcs(p + (qn + u) * 32) : 0u;
+    }
+    // words past the segment end were loaded as 0: delta 0, FMA predicated off
+#pragma unroll
+    for (int u = 0; u < U; ++u) S::run(cur[u], c2, x, acc, m_real, vmask);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+  }
+  a.seg_partial[sg * 32 + lane] = acc;
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(kBlock) seg_combine_kernel(const SpmvArgs a, long long n_long) {
+  const long long l = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (l >= n_long) return;
+  const int k = a.long_slice[l];
+  float acc = 0.f;
+  for (int sgi = a.long_seg0[l]; sgi < a.long_seg0[l + 1]; ++sgi) acc += a.seg_partial[(long long)sgi * 32 + lane];
+  const uint32_t s = (uint32_t)k * 32u + lane;
+  if ((long long)s < a.n_rows) {
+    uint32_t o = s;
+    if (a.mode == PSELL_MODE_IMPLICIT) {
+      const uint32_t sig = (uint32_t)a.sigma;
+      const uint32_t p8 = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
+                                            : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
+      o = (s / sig) * sig + p8;
+    }
+    if constexpr (sizeof(XT) == 2) static_cast<XT*>(a.y)[o] = __float2half_rn(acc);
+    else static_cast<XT*>(a.y)[o] = acc;
+  }
 }
 
 // ---- multi-slice register pipeline (C == 32): warp w owns the S consecutive
@@ -866,11 +986,11 @@ static int dispatch_x(const SpmvArgs& a, int xdt, bool ref, cudaStream_t st) {
 }
 
 static int make_args(const psell_desc* d, const void* pack, const int64_t* offset,
-                     const void* perm, SpmvArgs& a, psell_error* err) {
+                     const void* perm, SpmvArgs& a, psell_error* err, bool need_perm = true) {
   if (!d) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null descriptor");
   if (!fmt_valid(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid PackFormat");
   if (d->c < 1) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid C");
-  if (d->mode == PSELL_MODE_IMPLICIT && d->n_rows > 0 && (!perm || d->sigma < 1))
+  if (need_perm && d->mode == PSELL_MODE_IMPLICIT && d->n_rows > 0 && (!perm || d->sigma < 1))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "implicit mode needs perm");
   if (d->n_cols >= (1ll << 31) || d->n_rows >= (1ll << 31))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "dimensions exceed 32-bit indexing");
@@ -894,6 +1014,11 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.d = d->d;
   a.perm_bytes = d->sigma <= 256 ? 1 : 2;
   a.variant = 0;
+  a.codec = d->codec;
+  a.seg_len = 0;
+  a.seg_slice = a.seg_q0 = a.long_slice = a.long_seg0 = nullptr;
+  a.seg_c2 = nullptr;
+  a.seg_partial = nullptr;
   a.spw = d->c == 32 ? slices_per_warp(a.n_slices) : 1;
   return PSELL_OK;
 }
@@ -966,6 +1091,76 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
   }
   if (bad) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "unsupported x dtype");
   PSELL_CHECK_LAUNCH(err, "psell_spmv");
+  return ok(err);
+}
+
+int psell_spmv_seg_checkpoints(const psell_desc* d, const void* pack, const int64_t* offset,
+                               int32_t seg_len, int64_t n_seg, const int32_t* seg_slice,
+                               const int32_t* seg_q0, int64_t n_long, const int32_t* long_slice,
+                               const int32_t* long_seg0, uint32_t* seg_c2, void* stream,
+                               psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, nullptr, a, err, /*need_perm=*/false)) return rc;
+  if (d->c != 32 || d->w != 32 || seg_len < 1)
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "segmentation needs C = 32, W = 32");
+  a.seg_len = seg_len;
+  a.seg_slice = seg_slice;
+  a.seg_q0 = seg_q0;
+  a.seg_c2 = seg_c2;
+  a.long_slice = long_slice;
+  a.long_seg0 = long_seg0;
+  cudaStream_t st = as_stream(stream);
+  if (n_seg > 0) seg_dsum_kernel<<<(unsigned)ceil_div(n_seg * 32, kBlock), kBlock, 0, st>>>(a, n_seg);
+  if (n_long > 0) seg_prefix_kernel<<<(unsigned)ceil_div(n_long * 32, kBlock), kBlock, 0, st>>>(a, n_long);
+  PSELL_CHECK_LAUNCH(err, "psell_spmv_seg_checkpoints");
+  return ok(err);
+}
+
+}  // extern "C"
+
+namespace psell {
+template <int CODEC, typename XT>
+static void launch_segmented(const SpmvArgs& a, long long n_seg, long long n_long, cudaStream_t st) {
+  launch_spmv<CODEC, XT, false, false>(a, st);  // short slices (long ones are skipped)
+  if (n_seg > 0)
+    spmv_seg_kernel<CODEC, XT, 8><<<(unsigned)ceil_div(n_seg * 32, kBlock), kBlock, 0, st>>>(a, n_seg);
+  if (n_long > 0)
+    seg_combine_kernel<XT><<<(unsigned)ceil_div(n_long * 32, kBlock), kBlock, 0, st>>>(a, n_long);
+}
+}  // namespace psell
+
+extern "C" {
+
+int psell_spmv_segmented(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
+                         const void* x, int32_t x_dtype, void* y, int32_t seg_len, int64_t n_seg,
+                         const int32_t* seg_slice, const int32_t* seg_q0, const uint32_t* seg_c2,
+                         float* seg_partial, int64_t n_long, const int32_t* long_slice,
+                         const int32_t* long_seg0, void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  if (d->c != 32 || d->codec == PSELL_FP32EMBED || (x_dtype != PSELL_DT_F16 && x_dtype != PSELL_DT_F32))
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0,
+                   "segmented SpMV: C = 32, fp16/e8my codec, f16/f32 x only");
+  a.x = x;
+  a.y = y;
+  a.spw = 1;
+  a.seg_len = seg_len;
+  a.seg_slice = seg_slice;
+  a.seg_q0 = seg_q0;
+  a.seg_c2 = const_cast<uint32_t*>(seg_c2);
+  a.seg_partial = seg_partial;
+  a.long_slice = long_slice;
+  a.long_seg0 = long_seg0;
+  if (a.n_rows == 0) return ok(err);
+  cudaStream_t st = as_stream(stream);
+  if (d->codec == PSELL_FP16) {
+    if (x_dtype == PSELL_DT_F16) launch_segmented<PSELL_FP16, __half>(a, n_seg, n_long, st);
+    else launch_segmented<PSELL_FP16, float>(a, n_seg, n_long, st);
+  } else {
+    if (x_dtype == PSELL_DT_F16) launch_segmented<PSELL_E8MY, __half>(a, n_seg, n_long, st);
+    else launch_segmented<PSELL_E8MY, float>(a, n_seg, n_long, st);
+  }
+  PSELL_CHECK_LAUNCH(err, "psell_spmv_segmented");
   return ok(err);
 }
 

@@ -128,6 +128,7 @@ class PackSellMatrix:
             self._perm_dtype = pp.dtype
             self.d_perm = _dev.upload(pp.astype(perm_dtype(self.sigma)))
         self._out_idx = None
+        self._seg = 0  # long-slice schedule: 0 = not built yet, None = none needed
         self._n_stored = int(self.d_pack.numel())
         self._n_slices = int(self.d_offset.numel()) - 1
 
@@ -265,10 +266,74 @@ def build_packsell(A, c: int = 32, sigma: int = 256,
                           counts, row0=D.row0)
 
 
+SEG_LEN = 256  # steps per segment of a long slice (32 KB of words)
+
+
+def _seg_dtypes():
+    import torch
+    return (torch.float16, torch.float32)
+
+
+class _LazyDtypes:
+    def __contains__(self, dt):
+        return dt in _seg_dtypes()
+
+
+_SEG_DTYPES = _LazyDtypes()
+
+
+def _seg_schedule(M: PackSellMatrix):
+    """Segments of the slices wider than SEG_LEN steps, with device cursor checkpoints.
+
+    Built once per matrix from the int64 slice offsets (metadata only); the
+    checkpoints come from psell_spmv_seg_checkpoints.  None when the matrix
+    has no long slices or the layout is not segmentable (C != 32, W != 32).
+    """
+    if getattr(M, "_seg", 0) != 0:
+        return M._seg
+    M._seg = None
+    if M.c != 32 or M.fmt.w != 32 or M.n_slices == 0:
+        return None
+    from . import _dev, _lib
+    w = np.diff(M.offset) // M.c
+    long_ = np.nonzero(w > SEG_LEN)[0]
+    if long_.size == 0:
+        return None
+    per = -(-w[long_] // SEG_LEN)
+    seg0 = np.concatenate([[0], np.cumsum(per)]).astype(np.int32)
+    n_seg = int(seg0[-1])
+    seg_slice = np.repeat(long_, per).astype(np.int32)
+    seg_q0 = ((np.arange(n_seg) - np.repeat(seg0[:-1], per)) * SEG_LEN).astype(np.int32)
+    s = dict(n_seg=n_seg, n_long=int(long_.size), seg_slice=_dev.upload(seg_slice), seg_q0=_dev.upload(seg_q0),
+             long_slice=_dev.upload(long_.astype(np.int32)), long_seg0=_dev.upload(seg0),
+             seg_c2=_dev.empty(n_seg * 32, np.uint32))
+    lib = _lib.lib()
+    err = _lib.PsellError()
+    rc = lib.psell_spmv_seg_checkpoints(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), SEG_LEN, n_seg,
+                                        _lib.ptr(s["seg_slice"]), _lib.ptr(s["seg_q0"]), s["n_long"],
+                                        _lib.ptr(s["long_slice"]), _lib.ptr(s["long_seg0"]),
+                                        _lib.ptr(s["seg_c2"]), _lib.stream_handle(), err)
+    _lib.check(rc, err, M.fmt)
+    M._seg = s
+    return s
+
+
 def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool, pipe: int = 0):
     from . import _dev, _lib
     lib = _lib.lib()
     err = _lib.PsellError()
+    if not ref_order and not pipe and M.fmt.codec != codec.FP32EMBED and xd.dtype in _SEG_DTYPES:
+        s = _seg_schedule(M)
+        if s is not None:
+            import torch
+            part = torch.empty(s["n_seg"] * 32, dtype=torch.float32, device=xd.device)
+            rc = lib.psell_spmv_segmented(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                                          _lib.ptr(xd), _dev.T_DT_CODE[xd.dtype], _lib.ptr(y), SEG_LEN, s["n_seg"],
+                                          _lib.ptr(s["seg_slice"]), _lib.ptr(s["seg_q0"]), _lib.ptr(s["seg_c2"]),
+                                          _lib.ptr(part), s["n_long"], _lib.ptr(s["long_slice"]),
+                                          _lib.ptr(s["long_seg0"]), _lib.stream_handle(), err)
+            _lib.check(rc, err, M.fmt)
+            return y
     rc = lib.psell_spmv(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
                         _lib.ptr(xd), _dev.T_DT_CODE[xd.dtype], _lib.ptr(y),
                         (_lib.SPMV_REF_ORDER if ref_order else 0) | (2 if pipe else 0),

@@ -111,32 +111,101 @@ def stencil27(nx: int, ny: int = None, nz: int = None) -> CsrMatrix:
     return _grid_stencil([nx, nx if ny is None else ny, nx if nz is None else nz], box=True, diag=26.0)
 
 
-def powerlaw(n: int = 2**23, seed: int = 2604, alpha: float = 1.5, lmax: int = 8192,
-             local_frac: float = 0.8, spread: float = 4096.0) -> CsrMatrix:
-    """Irregular power-law row lengths (config 4).
+_U64 = np.uint64
 
-    L_i = min(lmax, floor(4 U^(-1/alpha))) (Pareto, mean ~12); 80 % of a row's
-    columns are i + round(N(0, spread)) clipped to [0, n), 20 % uniform; sorted,
-    unique; values U[0.01, 1) * +-1.
+
+def _smix(z):
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic), = smix in csrc/gen.cu."""
+    with np.errstate(over="ignore"):
+        z = z + _U64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> _U64(30))) * _U64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> _U64(27))) * _U64(0x94D049BB133111EB)
+    return z ^ (z >> _U64(31))
+
+
+def powerlaw_rows(n: int = 2**23, seed: int = 2604, row_begin: int = 0, row_end: int = None) -> CsrMatrix:
+    """Rows [row_begin, row_end) of the config-4 power-law matrix (host mirror of
+    psell_gen_powerlaw_*; the generator law is documented in csrc/gen.cu).
+
+    Counter-based hashing makes every row independent, so a CPU sample or a
+    rank slab is generated without the rest of the matrix and equals the GPU's.
     """
-    rng = np.random.Generator(np.random.PCG64(seed))
-    u = rng.random(n)
-    lens = np.minimum(lmax, np.floor(4.0 * u ** (-1.0 / alpha))).astype(np.int64)
-    lens = np.maximum(lens, 1)
-    tot = int(lens.sum())
-    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
-    local = rng.random(tot) < local_frac
-    near = np.clip(rows + np.rint(rng.normal(0.0, spread, tot)).astype(np.int64), 0, n - 1)
-    far = rng.integers(0, n, tot)
-    cols = np.where(local, near, far)
-    key = rows * n + cols
-    key = np.unique(key)
-    r = key // n
-    c = key - r * n
-    vals = rng.uniform(0.01, 1.0, len(key)) * rng.choice([-1.0, 1.0], len(key))
-    counts = np.bincount(r, minlength=n)
+    r1 = n if row_end is None else int(row_end)
+    r0 = int(row_begin)
+    rows = np.arange(r0, r1, dtype=np.int64)
+    with np.errstate(over="ignore"):
+        hr = _smix(_U64(seed) ^ (rows.astype(_U64) * _U64(0xD1B54A32D192ED03)))
+
+    def draw(stream, j, h):
+        return _smix(h ^ (_U64(stream) << _U64(56)) ^ _U64(j))
+
+    u = (draw(0, 0, hr) >> _U64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    thr = powerlaw_thresholds()
+    # number of leading (non-increasing) thresholds >= u  ==  binary search in gen.cu
+    L = np.maximum(np.searchsorted(-thr, -u, side="right"), 1).astype(np.int64)
+    G2 = (2 * np.maximum(1, 8192 // L)).astype(_U64)
+    far = np.maximum(n // (8 * L), 1).astype(_U64)
+    c = np.maximum(rows - 4096, 0)
+    out_r, out_j, out_c, out_v = [], [], [], []
+    act = np.nonzero((L > 0) & (c < n))[0]
+    j = 0
+    while act.size:
+        h = hr[act]
+        out_r.append(act)
+        out_j.append(np.full(act.size, j, dtype=np.int64))
+        out_c.append(c[act].copy())
+        m = 0.01 + 0.99 * ((draw(4, j, h) >> _U64(11)).astype(np.float64) * (1.0 / 9007199254740992.0))
+        out_v.append(np.where((draw(3, j, h) & _U64(1)) != 0, -m, m))
+        step = 1 + (draw(1, j, h) % G2[act]).astype(np.int64)
+        jump = np.where(draw(2, j, h) % _U64(5) == 0, (draw(5, j, h) % far[act]).astype(np.int64), 0)
+        c[act] += step + jump
+        j += 1
+        act = act[(j < L[act]) & (c[act] < n)]
+    if out_r:
+        rr = np.concatenate(out_r)
+        o = np.lexsort((np.concatenate(out_j), rr))
+        cols = np.concatenate(out_c)[o].astype(np.int32)
+        vals = np.concatenate(out_v)[o]
+        counts = np.bincount(rr, minlength=r1 - r0)
+    else:
+        cols, vals, counts = np.zeros(0, np.int32), np.zeros(0), np.zeros(r1 - r0, np.int64)
     row_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    return CsrMatrix(n, n, row_ptr, c.astype(np.int32), vals)
+    return CsrMatrix(r1 - r0, n, row_ptr, cols, vals)
+
+
+def powerlaw_thresholds() -> np.ndarray:
+    """T_k = (4/k)^1.5, k = 1..8192: L >= k  <=>  u <= T_k (Pareto alpha 1.5)."""
+    return (4.0 / np.arange(1, 8193, dtype=np.float64)) ** 1.5
+
+
+def powerlaw(n: int = 2**23, seed: int = 2604) -> CsrMatrix:
+    """The whole config-4 power-law matrix on the host (see powerlaw_rows)."""
+    return powerlaw_rows(n, seed)
+
+
+def powerlaw_device(n: int = 2**23, seed: int = 2604, *, row_begin: int = 0, row_end: int = None):
+    """Rows [row_begin, row_end) of the config-4 matrix generated in HBM (DeviceCsrMatrix)."""
+    import ctypes
+    from . import _dev, _lib
+    from .matrix import DeviceCsrMatrix
+    lib = _lib.lib()
+    r1 = n if row_end is None else int(row_end)
+    r0 = int(row_begin)
+    thr = _dev.upload(powerlaw_thresholds())
+    ws = _dev.workspace(lib.psell_gen_workspace_bytes(r1 - r0))
+    row_ptr = _dev.empty(r1 - r0 + 1, np.int64)
+    nnz = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    st = _lib.stream_handle()
+    rc = lib.psell_gen_powerlaw_plan(n, seed, _lib.ptr(thr), r0, r1, _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr),
+                                     ctypes.byref(nnz), st, err)
+    _lib.check(rc, err)
+    col = _dev.empty(nnz.value, np.int32)
+    val = _dev.empty(nnz.value, np.float64)
+    rc = lib.psell_gen_powerlaw_fill(n, seed, _lib.ptr(thr), r0, r1, _lib.ptr(row_ptr), _lib.ptr(col),
+                                     _lib.ptr(val), st, err)
+    _lib.check(rc, err)
+    return DeviceCsrMatrix(r1 - r0, n, row_ptr, col, val, row0=r0)
 
 
 _SCALES = {None: 0, "none": 0, "sym": 1, "rowsum": 2}

@@ -231,6 +231,51 @@ def test_slab_builds_concatenate_to_global(rng):
     assert np.array_equal(np.concatenate(perms), G.perm)
 
 
+@pytest.mark.parametrize("n,r0,r1", [(5000, 0, 5000), (2 ** 23, 0, 40_000), (2 ** 23, 2 ** 22, 2 ** 22 + 30_000)])
+def test_powerlaw_device_equals_host(n, r0, r1):
+    from paper_2604_13433_b200.stencil import powerlaw_device, powerlaw_rows
+    H = powerlaw_rows(n, 2604, r0, r1)
+    D = powerlaw_device(n, 2604, row_begin=r0, row_end=r1).to_host()
+    assert np.array_equal(D.row_ptr, H.row_ptr)
+    assert np.array_equal(D.col_idx, H.col_idx)
+    assert np.array_equal(_bits(D.values), _bits(H.values))
+
+
+def test_powerlaw_build_vs_oracle():
+    """Config-4 family (irregular widths, sigma up to 65536) through K1/K2 vs the oracle."""
+    from paper_2604_13433_b200.stencil import powerlaw_rows
+    A = powerlaw_rows(1 << 16, 7)
+    x = np.random.default_rng(1).uniform(-1, 1, A.n_cols).astype(np.float32)
+    for sigma in (256, 4096, 65536):
+        for pre in ("fp16", "e8m14"):
+            M = P.build_packsell(A, 32, sigma, P.parse_format(pre), "implicit")
+            OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, sigma, O.preset(pre), "implicit")
+            assert np.array_equal(M.pack, OM.pack) and np.array_equal(M.perm, OM.perm)
+            assert np.array_equal(M.offset, OM.offset) and tuple(M.counts) == OM.counts
+            assert np.array_equal(_bits(P.packsell_spmv(M, x, ref_order=True)), _bits(O.spmv(OM, x)))
+
+
+@pytest.mark.parametrize("sigma,pre,dt", [(256, "fp16", np.float16), (4096, "e8m14", np.float32),
+                                          (65536, "fp16", np.float32)])
+def test_long_slice_segmentation(sigma, pre, dt):
+    """Power-law rows wider than SEG_LEN run as checkpointed segments; result within the FMA bound."""
+    from paper_2604_13433_b200.packed import SEG_LEN, _seg_schedule
+    from paper_2604_13433_b200.stencil import powerlaw_rows
+    A = powerlaw_rows(1 << 17, 11)
+    M = P.build_packsell(A, 32, sigma, P.parse_format(pre), "implicit")
+    s = _seg_schedule(M)
+    assert s is not None and s["n_long"] > 0
+    x = np.random.default_rng(2).uniform(-1, 1, A.n_cols).astype(dt)
+    y = P.packsell_spmv(M, x).astype(np.float64)
+    ref = P.packsell_spmv(M, x.astype(np.float32), ref_order=True).astype(np.float64)
+    lmax = int(np.max(np.diff(M.offset) // 32))
+    aq = np.abs(P.quantize(P.parse_format(pre), A.values))
+    anorm = np.bincount(np.repeat(np.arange(A.n_rows), A.row_lengths()), aq, minlength=A.n_rows).max()
+    err = np.abs(y - ref).max() / (anorm * np.abs(x.astype(np.float64)).max())
+    assert err <= 2 * lmax * 2.0 ** -24 + (2.0 ** -11 if dt == np.float16 else 0.0), err
+    assert lmax > SEG_LEN
+
+
 def test_spmv_stream_equals_per_call(rng):
     """The pipelined host-buffer API returns exactly the per-call results."""
     import torch
