@@ -48,16 +48,46 @@ CONFIGS = {
     "c1": dict(kind="poisson2d", nx=512, preset="fp16", xdt="float16", scale=None, c=32, sigma=256,
                mode="implicit",
                workload="config 1: 5-point Laplacian 512^2, PackSELL fp16, C=32, sigma=256, implicit; x, y f16"),
+    "c4": dict(kind="powerlaw", n=2 ** 23, seed=2604, nx=0, preset="fp16", xdt="float16", scale=None, c=32,
+               sigma=65536, mode="implicit",
+               workload="config 4: power-law rows (Pareto alpha 1.5, n=2^23, ~95M nnz, csrc/gen.cu), PackSELL fp16, "
+                        "C=32, sigma=65536 (--sigma), implicit; x, y f16; long slices segmented"),
 }
 
 
 def stencil_k_left(kind: str, nx: int) -> int:
-    """Lower bandwidth of the generated stencils (checked against the device in tests)."""
+    """Lower bandwidth of the generated matrices (checked against the device in tests)."""
     if kind == "stencil27":
         return nx * nx + nx + 1
     if kind == "poisson3d":
         return nx * nx
+    if kind == "powerlaw":
+        return 4096  # every row starts at max(0, i - 4096) (csrc/gen.cu)
     return nx
+
+
+def cfg_rows(cfg) -> int:
+    if cfg["kind"] == "powerlaw":
+        return cfg["n"]
+    return cfg["nx"] ** (2 if cfg["kind"] == "poisson2d" else 3)
+
+
+def partition(cfg, world):
+    """sigma-aligned row slabs: equal for stencils, nnz-balanced for the power-law matrix."""
+    from paper_2604_13433_b200 import dist as D
+    n = cfg_rows(cfg)
+    if cfg["kind"] != "powerlaw" or world == 1:
+        return D.equal_row_slabs(n, world, cfg["sigma"])
+    from paper_2604_13433_b200.stencil import powerlaw_row_lengths
+    return D.word_balanced_slabs(powerlaw_row_lengths(n, cfg["seed"]), world, cfg["sigma"])
+
+
+def make_slab(cfg, r0, r1):
+    import paper_2604_13433_b200 as P
+    if cfg["kind"] == "powerlaw":
+        from paper_2604_13433_b200.stencil import powerlaw_device
+        return powerlaw_device(cfg["n"], cfg["seed"], row_begin=r0, row_end=r1)
+    return P.stencil_device(cfg["kind"], cfg["nx"], scale=cfg["scale"], row_begin=r0, row_end=r1)
 
 
 def measured_peak():
@@ -136,7 +166,11 @@ def _cpu_worker(conn, cfg, r0, r1, k_left, seed):
     os.environ["OMP_NUM_THREADS"] = "1"
     import oracle as O
     from paper_2604_13433_b200.stencil import stencil_rows
-    A = stencil_rows(cfg["kind"], cfg["nx"], r0, r1)
+    if cfg["kind"] == "powerlaw":
+        from paper_2604_13433_b200.stencil import powerlaw_rows
+        A = powerlaw_rows(cfg["n"], cfg["seed"], r0, r1)
+    else:
+        A = stencil_rows(cfg["kind"], cfg["nx"], r0, r1)
     vals = A.values
     if cfg["scale"] == "rowsum":
         rows = np.repeat(np.arange(A.n_rows), A.row_lengths())
@@ -163,7 +197,7 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
     """Oracle port of packsell_spmv on `workers` host cores, disjoint slab samples."""
     import multiprocessing as mp
     ctx = mp.get_context("fork")
-    n = cfg["nx"] ** (2 if cfg["kind"] == "poisson2d" else 3)
+    n = cfg_rows(cfg)
     kl = stencil_k_left(cfg["kind"], cfg["nx"])
     rows_per_worker = max(cfg["sigma"], rows_per_worker // cfg["sigma"] * cfg["sigma"])
     workers = max(1, min(workers, n // rows_per_worker))
@@ -338,26 +372,27 @@ def run_ours(args, cfg):
         if world > 1:
             dist.barrier(device_ids=[local])
 
-    nx = cfg["nx"]
-    n = nx ** (2 if cfg["kind"] == "poisson2d" else 3)
+    n = cfg_rows(cfg)
     sig = cfg["sigma"]
-    nblk = -(-n // sig)
-    r0 = min(n, (nblk * rank // world) * sig)
-    r1 = min(n, (nblk * (rank + 1) // world) * sig)
+    r0, r1 = partition(cfg, world)[rank]
     fmt = P.parse_format(cfg["preset"])
 
     t_b0 = time.perf_counter()
-    S = P.stencil_device(cfg["kind"], nx, scale=cfg["scale"], row_begin=r0, row_end=r1)
+    S = make_slab(cfg, r0, r1)
     kl = int(allreduce(lower_bandwidth(S), dist.ReduceOp.MAX if world > 1 else None))
     torch.cuda.synchronize()
     t_b1 = time.perf_counter()
     M = P.build_packsell(S, cfg["c"], sig, fmt, cfg["mode"], _k_left_override=kl)
     torch.cuda.synchronize()
     t_b2 = time.perf_counter()
-    # stencil rows are ascending with ascending columns: the slab's x footprint
-    # runs from its first stored column to its last
-    cmin = int(S.col_idx[0].item()) if S.nnz else 0
-    cmax = int(S.col_idx[-1].item()) if S.nnz else -1
+    if world == 1:
+        touched = n
+    elif cfg["kind"] == "powerlaw":
+        touched = int(torch.unique(S.col_idx).numel())  # distinct x entries this slab gathers
+    else:
+        # stencil rows are ascending with ascending columns: the slab's x footprint
+        # runs from its first stored column to its last
+        touched = int(S.col_idx[-1].item()) - int(S.col_idx[0].item()) + 1 if S.nnz else 0
     nnz_local = S.nnz
     del S
     torch.cuda.empty_cache()
@@ -368,7 +403,6 @@ def run_ours(args, cfg):
     x = (torch.rand(n, generator=g, device=dev, dtype=torch.float32) * 2 - 1).to(xt)
     y = torch.empty(M.n_rows, dtype=xt, device=dev)
     xsz = x.element_size()
-    touched = n if world == 1 else (cmax - cmin + 1)
     bytes_local = M.spmv_bytes(xsz, xsz, with_perm=True, x_elems=touched)
     bytes_noperm = M.spmv_bytes(xsz, xsz, with_perm=False, x_elems=touched)
     st = torch.cuda.current_stream()
@@ -478,8 +512,9 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["workload"], "n": n, "nnz": int(nnz_all),
                        "n_stored_rank0": m_info[0], "counts_rank0": m_info[1], "k_left": kl,
                        "partition": "sigma-aligned row slabs, x replicated (no collective in the step)",
-                       "l2": "inputs larger than L2: packed words stream at 1.94 GB per SpMV (126 MB L2); "
-                             "x (33.5 MB f16) is L2-resident by design and counted once"},
+                       "l2": f"inputs larger than L2: {m_info[0] * 4 / 1e9:.2f} GB of packed words stream per "
+                             f"SpMV on rank 0 (126 MB L2); x ({n * np.dtype(cfg['xdt']).itemsize / 1e6:.1f} MB) "
+                             "is L2-resident by design and counted once"},
             "pct_hbm_peak": value / (peak * world),
             "gflops": gflops,
             "bytes_per_step": int(bytes_all),
@@ -514,6 +549,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--sigma", type=int, default=0, help="override the sorting window")
     ap.add_argument("--ref-rows", type=int, default=131072, help="rows per CPU worker (reference arm)")
     ap.add_argument("--cpu-rows", type=int, default=262144, help="rows of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -522,7 +558,12 @@ def main():
     ap.add_argument("--pcg-m-in", type=int, default=50)
     ap.add_argument("--pcg-cpu-nx", type=int, default=32)
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.sigma:
+        cfg["sigma"] = args.sigma
+        cfg["workload"] += f" [sigma overridden to {args.sigma}]"
+    if args.config == "c4" and not args.no_pcg:
+        args.no_pcg = True  # the PCG time-to-solution belongs to the stencil configs (config 5)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -183,6 +183,22 @@ def powerlaw(n: int = 2**23, seed: int = 2604) -> CsrMatrix:
     return powerlaw_rows(n, seed)
 
 
+def powerlaw_row_lengths(n: int = 2**23, seed: int = 2604) -> np.ndarray:
+    """Row lengths of the whole config-4 matrix (device count pass only) — partition weights."""
+    import ctypes
+    from . import _dev, _lib
+    lib = _lib.lib()
+    thr = _dev.upload(powerlaw_thresholds())
+    ws = _dev.workspace(lib.psell_gen_workspace_bytes(n))
+    row_ptr = _dev.empty(n + 1, np.int64)
+    nnz = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    rc = lib.psell_gen_powerlaw_plan(n, seed, _lib.ptr(thr), 0, n, _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr),
+                                     ctypes.byref(nnz), _lib.stream_handle(), err)
+    _lib.check(rc, err)
+    return np.diff(_dev.download(row_ptr, np.int64))
+
+
 def powerlaw_device(n: int = 2**23, seed: int = 2604, *, row_begin: int = 0, row_end: int = None):
     """Rows [row_begin, row_end) of the config-4 matrix generated in HBM (DeviceCsrMatrix)."""
     import ctypes
