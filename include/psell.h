@@ -278,6 +278,18 @@ PSELL_API int psell_gen_stencil_fill(int64_t d0, int64_t d1, int64_t d2, int32_t
                                      const int64_t* row_ptr, int32_t* col_idx, double* values,
                                      void* stream, psell_error* err);
 
+/* ---- SELL-C-sigma comparator (reference sell.py:49-204) ----
+ * Layout from psell_build_plan with a no-dummy format (w=64, d=31, fp32embed),
+ * then psell_sell_fill writes values (val_dtype f64/f32/f16, direct RNE) and
+ * int32 columns (padding: value 0, the row's last column).  psell_sell_spmv is
+ * bitwise sell_spmv (values cast to x dtype, numpy rounding order). */
+PSELL_API int psell_sell_fill(const psell_desc* desc, const int64_t* row_ptr, const int32_t* col_idx,
+                              const double* values, const void* plan_workspace, const int64_t* offset,
+                              int32_t val_dtype, void* val, int32_t* col, void* stream, psell_error* err);
+PSELL_API int psell_sell_spmv(const psell_desc* desc, const void* val, int32_t val_dtype, const int32_t* col,
+                              const int64_t* offset, const void* perm, const void* x, int32_t x_dtype,
+                              void* y, void* stream, psell_error* err);
+
 /* Config-4 power-law matrix (counter-based splitmix64 law in csrc/gen.cu), rows
  * [row_begin, row_end) of an n x n matrix; reproduced bit for bit on the host by
  * paper_2604_13433_b200.stencil.powerlaw_rows. */

@@ -74,6 +74,11 @@ static BuildWs carve(const psell_desc* d, void* base) {
   return w;
 }
 
+// storage-row -> original-row order the plan leaves in the workspace (SELL fill reuses it)
+const int32_t* build_ws_order(const psell_desc* d, const void* ws) {
+  return carve(d, const_cast<void*>(ws)).order;
+}
+
 // Eq. 4 base offset of global row g (packed.py:40-52).
 __device__ __forceinline__ long long base_of(long long g, long long se, long long k_left) {
   const long long blk = (g / se) * se;

@@ -218,4 +218,6 @@ namespace psell {
 // out[0] = 0, out[i+1] = in[0] + ... + in[i]   (build.cu); tmp >= ceil(n/4096)+1 longs
 int scan_i64(const long long* in, long long n, long long* tmp, long long* out, cudaStream_t st,
              psell_error* err);
+// storage-row -> original-row order stored in a psell_build_plan workspace (build.cu)
+const int32_t* build_ws_order(const psell_desc* d, const void* ws);
 }  // namespace psell

@@ -1,0 +1,178 @@
+// SELL-C-sigma comparator format on sm_100a: the FP64 / FP32 /
+// FP16 sliced-ELL baseline of the reference (sell.py:49-204), used by
+// make_backend("sell64" | "sell32" | "sell16") and the FP32 IO-CG comparator.
+//
+// The layout plan (widths from row lengths, stable descending sigma-block
+// sort, int64 offsets, perm) is the PackSELL plan with a format that can never
+// emit a dummy word (W = 64, D = 31), so it is shared with K1.  The fill writes
+// values converted to the value dtype (direct RNE) and int32 columns; padding
+// carries value 0 and the row's last column (0 for empty rows) (sell.py:161-172).
+// The SpMV reproduces sell_spmv's numpy rounding: values cast to x's dtype,
+// accumulator from 0, one rounding per product and per sum (sell.py:181-204).
+#include "psell_internal.cuh"
+
+namespace psell {
+
+template <typename V> __device__ __forceinline__ V from_f64(double v);
+template <> __device__ __forceinline__ double from_f64<double>(double v) { return v; }
+template <> __device__ __forceinline__ float from_f64<float>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ __half from_f64<__half>(double v) { return __double2half(v); }
+
+template <typename V>
+__global__ void __launch_bounds__(kBlock) sell_fill_kernel(const int64_t* __restrict__ row_ptr,
+                                                           const int32_t* __restrict__ col_idx,
+                                                           const double* __restrict__ values,
+                                                           const int32_t* __restrict__ order,
+                                                           const int64_t* __restrict__ offset, long long n,
+                                                           long long n_slices, int c, V* __restrict__ val,
+                                                           int32_t* __restrict__ col) {
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (s >= n_slices * c) return;
+  const long long k = s / c, lane = s - k * c;
+  const long long o = offset[k];
+  const long long width = (offset[k + 1] - o) / c;
+  long long q = 0;
+  int32_t last = 0;
+  if (s < n) {
+    const long long r = order ? (long long)order[s] : s;
+    const long long beg = row_ptr[r], end = row_ptr[r + 1];
+    for (long long j = beg; j < end; ++j, ++q) {
+      const long long pos = o + lane + q * c;
+      val[pos] = from_f64<V>(values[j]);
+      col[pos] = col_idx[j];
+    }
+    if (end > beg) last = col_idx[end - 1];
+  }
+  for (; q < width; ++q) {
+    const long long pos = o + lane + q * c;
+    val[pos] = from_f64<V>(0.0);
+    col[pos] = last;
+  }
+}
+
+// value (stored dtype VT) -> x dtype XT, numpy astype semantics (RNE)
+template <typename VT, typename XT> __device__ __forceinline__ XT vcast(VT v);
+template <> __device__ __forceinline__ double vcast<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ float vcast<double, float>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ __half vcast<double, __half>(double v) { return __double2half(v); }
+template <> __device__ __forceinline__ double vcast<float, double>(float v) { return (double)v; }
+template <> __device__ __forceinline__ float vcast<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ __half vcast<float, __half>(float v) { return __float2half_rn(v); }
+template <> __device__ __forceinline__ double vcast<__half, double>(__half v) { return (double)__half2float(v); }
+template <> __device__ __forceinline__ float vcast<__half, float>(__half v) { return __half2float(v); }
+template <> __device__ __forceinline__ __half vcast<__half, __half>(__half v) { return v; }
+
+template <typename T> struct RefOps;
+template <> struct RefOps<double> {
+  __device__ static double step(double a, double v, double x) { return __dadd_rn(a, __dmul_rn(v, x)); }
+  __device__ static double zero() { return 0.0; }
+};
+template <> struct RefOps<float> {
+  __device__ static float step(float a, float v, float x) { return __fadd_rn(a, __fmul_rn(v, x)); }
+  __device__ static float zero() { return 0.f; }
+};
+template <> struct RefOps<__half> {
+  __device__ static __half step(__half a, __half v, __half x) { return __hadd_rn(a, __hmul_rn(v, x)); }
+  __device__ static __half zero() { return __ushort_as_half(0); }
+};
+
+template <typename VT, typename XT>
+__global__ void __launch_bounds__(kBlock) sell_spmv_kernel(const VT* __restrict__ val,
+                                                           const int32_t* __restrict__ col,
+                                                           const int64_t* __restrict__ offset,
+                                                           const void* perm, int perm_bytes, int implicit,
+                                                           int sigma, long long n_rows, int c,
+                                                           const XT* __restrict__ x, XT* __restrict__ y) {
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (s >= n_rows) return;
+  const long long k = s / c, lane = s - k * c;
+  const long long o = offset[k];
+  const long long width = (offset[k + 1] - o) / c;
+  XT acc = RefOps<XT>::zero();
+  for (long long q = 0; q < width; ++q) {
+    const long long pos = o + lane + q * c;
+    acc = RefOps<XT>::step(acc, vcast<VT, XT>(val[pos]), x[col[pos]]);
+  }
+  long long out = s;
+  if (implicit) {
+    const long long p = perm_bytes == 1 ? (long long)static_cast<const uint8_t*>(perm)[s]
+                                        : (long long)static_cast<const uint16_t*>(perm)[s];
+    out = (s / sigma) * sigma + p;
+  }
+  y[out] = acc;
+}
+
+template <typename VT, typename XT>
+static void launch_sell(const psell_desc* d, const void* val, const int32_t* col, const int64_t* offset,
+                        const void* perm, const void* x, void* y, cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(d->n_rows, kBlock);
+  sell_spmv_kernel<VT, XT><<<grid, kBlock, 0, st>>>(
+      static_cast<const VT*>(val), col, offset, perm, d->sigma <= 256 ? 1 : 2, d->mode == PSELL_MODE_IMPLICIT,
+      d->sigma, d->n_rows, d->c, static_cast<const XT*>(x), static_cast<XT*>(y));
+}
+
+template <typename VT>
+static int dispatch_sell_x(const psell_desc* d, const void* val, const int32_t* col, const int64_t* offset,
+                           const void* perm, const void* x, int32_t xdt, void* y, cudaStream_t st) {
+  switch (xdt) {
+    case PSELL_DT_F64: launch_sell<VT, double>(d, val, col, offset, perm, x, y, st); return 0;
+    case PSELL_DT_F32: launch_sell<VT, float>(d, val, col, offset, perm, x, y, st); return 0;
+    case PSELL_DT_F16: launch_sell<VT, __half>(d, val, col, offset, perm, x, y, st); return 0;
+  }
+  return 1;
+}
+
+}  // namespace psell
+
+using namespace psell;
+
+extern "C" {
+
+PSELL_API int psell_sell_fill(const psell_desc* d, const int64_t* row_ptr, const int32_t* col_idx,
+                              const double* values, const void* workspace, const int64_t* offset,
+                              int32_t val_dtype, void* val, int32_t* col, void* stream, psell_error* err) {
+  if (!d || d->c < 1) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "bad descriptor");
+  const long long n = d->n_rows;
+  const long long ns = ceil_div(n, d->c);
+  if (ns == 0) return ok(err);
+  const int32_t* order = d->mode == PSELL_MODE_NONE ? nullptr : build_ws_order(d, workspace);
+  const unsigned grid = (unsigned)ceil_div(ns * d->c, kBlock);
+  cudaStream_t st = as_stream(stream);
+  switch (val_dtype) {
+    case PSELL_DT_F64:
+      sell_fill_kernel<double><<<grid, kBlock, 0, st>>>(row_ptr, col_idx, values, order, offset, n, ns, d->c,
+                                                        static_cast<double*>(val), col);
+      break;
+    case PSELL_DT_F32:
+      sell_fill_kernel<float><<<grid, kBlock, 0, st>>>(row_ptr, col_idx, values, order, offset, n, ns, d->c,
+                                                       static_cast<float*>(val), col);
+      break;
+    case PSELL_DT_F16:
+      sell_fill_kernel<__half><<<grid, kBlock, 0, st>>>(row_ptr, col_idx, values, order, offset, n, ns, d->c,
+                                                        static_cast<__half*>(val), col);
+      break;
+    default:
+      return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "bad value dtype");
+  }
+  PSELL_CHECK_LAUNCH(err, "psell_sell_fill");
+  return ok(err);
+}
+
+PSELL_API int psell_sell_spmv(const psell_desc* d, const void* val, int32_t val_dtype, const int32_t* col,
+                              const int64_t* offset, const void* perm, const void* x, int32_t x_dtype,
+                              void* y, void* stream, psell_error* err) {
+  if (!d || d->c < 1) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "bad descriptor");
+  if (d->n_rows <= 0) return ok(err);
+  cudaStream_t st = as_stream(stream);
+  int bad = 1;
+  switch (val_dtype) {
+    case PSELL_DT_F64: bad = dispatch_sell_x<double>(d, val, col, offset, perm, x, x_dtype, y, st); break;
+    case PSELL_DT_F32: bad = dispatch_sell_x<float>(d, val, col, offset, perm, x, x_dtype, y, st); break;
+    case PSELL_DT_F16: bad = dispatch_sell_x<__half>(d, val, col, offset, perm, x, x_dtype, y, st); break;
+  }
+  if (bad) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "bad dtype");
+  PSELL_CHECK_LAUNCH(err, "psell_sell_spmv");
+  return ok(err);
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+"""SELL-C-sigma comparator on the GPU vs the reference (sell.py:114-204) and the
+acceptance c08 relation: e8m14 IO-CG needs <= 1.25x the FP32-SELL inner iterations."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2604_13433_b200 as P
+from paper_2604_13433_b200 import solvers as S
+from conftest import GOLDEN, golden_x
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def test_sell_layout_and_spmv_bitwise():
+    z = np.load(os.path.join(GOLDEN, "sell_golden.npz"))
+    with open(os.path.join(GOLDEN, "sell_golden.json")) as f:
+        meta = json.load(f)
+    for i, m in enumerate(meta):
+        p = f"s{i}_"
+        A = P.CsrMatrix(m["n_rows"], m["n_cols"], z[p + "row_ptr"], z[p + "col_idx"], z[p + "values"])
+        M = P.build_sell(A, m["c"], m["sigma"], m["mode"], np.dtype(m["vdt"]))
+        assert np.array_equal(_bits(M.val), _bits(z[p + "val"])), i
+        assert np.array_equal(M.col, z[p + "col"]), i
+        assert np.array_equal(M.offset, z[p + "offset"]), i
+        assert M.n_padding == m["n_padding"], i
+        if m["has_perm"]:
+            assert np.array_equal(M.perm, z[p + "perm"]), i
+        else:
+            assert M.perm is None
+        for dt in (np.float16, np.float32, np.float64):
+            y = P.sell_spmv(M, golden_x(5000 + i, m["n_cols"], dt))
+            want = z[p + f"y_{np.dtype(dt).name}"]
+            assert y.dtype == want.dtype and np.array_equal(_bits(y), _bits(want)), (i, dt)
+
+
+def test_iocg_sell32_and_acceptance_ordering(golden_solver):
+    z, meta = golden_solver
+    A = P.sym_diag_scale(P.poisson3d(10))
+    b = z["b"]
+    cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="sell32", max_outer=200)
+    r = S.iocg(A, b, cfg)
+    ref = meta["iocg_sell32"]
+    assert r.converged and abs(r.outer_iters - ref["outer"]) <= 1
+    assert np.abs(r.x - z["iocg_sell32_x"]).max() / np.abs(z["iocg_sell32_x"]).max() < 1e-6
+    r14 = S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200))
+    assert r14.converged and r14.total_inner_iters <= 1.25 * r.total_inner_iters
+
+
+def test_make_backend_all_names():
+    A = P.sym_diag_scale(P.poisson3d(6))
+    x = np.random.default_rng(0).uniform(-1, 1, A.n_cols)
+    want = P.csr_spmv(A, x, np.float64)
+    for name in ("csr64", "sell64", "sell32", "sell16", "packsell-fp16", "packsell-e8m14", "packsell-fp32embed"):
+        be = S.make_backend(A, name)
+        y = be.apply(x)
+        assert y.dtype == np.float64 and np.abs(y - want).max() < 1e-2, name
