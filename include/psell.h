@@ -65,7 +65,8 @@ typedef enum psell_dtype { PSELL_DT_F16 = 0, PSELL_DT_F32 = 1, PSELL_DT_F64 = 2 
 /* psell_spmv flags */
 #define PSELL_SPMV_REF_ORDER 1 /* numpy rounding order: value cast to x dtype, product and sum rounded separately */
 #define PSELL_SPMV_TMA_STREAM 2 /* C=32 fast path: persistent TMA bulk-copy stream instead of the default
-                                  register-pipelined one-warp-per-slice kernel (A/B experiments) */
+                                  register-pipelined dual-slice kernel (A/B experiments) */
+#define PSELL_SPMV_NARROW 4     /* mean slice width <= 12 steps (e.g. 7-point rows): 12-step chunks */
 
 typedef struct psell_error {
   int32_t code;  /* psell_status */
@@ -171,7 +172,8 @@ PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc);
  * skip_flag != NULL and *skip_flag != 0 the kernel does nothing (breakdown). */
 PSELL_API int psell_spmv_dot(const psell_desc* desc, const void* pack, const int64_t* offset,
                    const void* perm, const float* x, float* y, const float* p_own,
-                   double* partials, const int32_t* skip_flag, void* stream, psell_error* err);
+                   double* partials, const int32_t* skip_flag, int32_t flags, void* stream,
+                   psell_error* err);
 
 /* ---- K5: PackSELL -> CSR decode (replaces packsell_to_csr, packed.py:274-303) ---- */
 PSELL_API size_t psell_to_csr_workspace_bytes(const psell_desc* desc);

@@ -30,7 +30,8 @@ struct SpmvArgs {
   const int32_t* skip;
   long long n_rows, n_cols, n_slices, row0, k_left;
   int c, se, sigma, mode, d, perm_bytes;
-  int variant;  // 0: register-pipelined warp-per-slice (default), 2: persistent TMA stream
+  int variant;  // 0: register-pipelined kernels (default), 2: persistent TMA stream
+  int narrow;   // mean slice width <= 12 steps (PSELL_SPMV_NARROW)
   int spw;      // slices per warp of the multi-slice kernel (1: warp-per-slice kernel)
   int codec;
   // long-slice segmentation (0 = off): slices wider than seg_len steps run as
@@ -147,13 +148,39 @@ __device__ __forceinline__ long long out_row(const SpmvArgs& a, long long s) {
   return blk + p;
 }
 
-template <bool DOT>
+template <bool DOT, int NT = kBlock>
 __device__ __forceinline__ void finish_dot(const SpmvArgs& a, double v) {
   if constexpr (DOT) {
-    __shared__ double sh[kBlock / 32];
-    const double t = block_sum<kBlock>(v, sh);
+    __shared__ double sh[NT / 32];
+    const double t = block_sum<NT>(v, sh);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
   }
+}
+
+constexpr int kWarpsPerCta = kBlock / 32;
+
+// dual-slice kernel switch (PSELL_DUAL=1 forces it on, =0 off; A/B)
+static bool dual_slices(long long n_slices) {
+  if (const char* e = getenv("PSELL_DUAL")) return atoi(e) != 0;
+  return n_slices >= 2;  // measured faster than one slice per warp on configs 2, 3, 5
+}
+
+// steps per chunk of the dual-slice kernel (PSELL_DUAL_U overrides: 8 | 12 | 16)
+static int dual_chunk(bool narrow) {
+  if (const char* e = getenv("PSELL_DUAL_U")) {
+    const int v = atoi(e);
+    if (v == 8 || v == 12 || v == 16) return v;
+  }
+  return narrow ? 12 : 8;  // 12 covers a whole 7-point slice in one chunk (sweep: +14 %)
+}
+
+// threads per CTA of the one-warp-per-slice kernel (PSELL_NT overrides, A/B)
+static int fast_nt() {
+  if (const char* e = getenv("PSELL_NT")) {
+    const int v = atoi(e);
+    if (v == 64 || v == 128 || v == 256) return v;
+  }
+  return 256;
 }
 
 // ---- fast path: C == 32, warp == slice
@@ -272,13 +299,13 @@ template <> struct FastPolicy<PSELL_FP16, float> { static constexpr bool kHave =
 template <> struct FastPolicy<PSELL_E8MY, float> { static constexpr bool kHave = true; };
 template <> struct FastPolicy<PSELL_E8MY, __half> { static constexpr bool kHave = true; };
 
-template <int CODEC, typename XT, bool DOT, int U>
-__global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) {
+template <int CODEC, typename XT, bool DOT, int U, int NT = kBlock>
+__global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_fast_kernel(const SpmvArgs a) {
   using S = FastStep<CODEC, XT>;
   if constexpr (DOT) {
     if (a.skip && *a.skip) return;
   }
-  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long s = (long long)blockIdx.x * NT + threadIdx.x;
   const long long k = s >> 5;
   const int lane = threadIdx.x & 31;
   double dotv = 0.0;
@@ -364,6 +391,77 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_fast_kernel(const SpmvArgs a) 
     }
   }
 done:
+  finish_dot<DOT, NT>(a, dotv);
+}
+
+// ---- dual-slice kernel (C == 32): a warp runs slices 2w and 2w+1 in lockstep
+// chunks, so the two per-slice latency chains (offset -> words -> x -> y)
+// overlap inside one warp.  Aimed at narrow slices (7-point rows: ~9 steps),
+// where one slice per warp leaves the chain exposed.
+template <int CODEC, typename XT, bool DOT, int U>
+__global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) {
+  using S = FastStep<CODEC, XT>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const long long wg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long kA = 2 * wg, kB = kA + 1;
+  double dotv = 0.0;
+  if (kA < a.n_slices) {
+    const bool hasB = kB < a.n_slices;
+    const long long oA = a.offset[kA], oB = a.offset[kA + 1];
+    const long long oE = hasB ? a.offset[kB + 1] : oB;
+    const int wA = (int)((oB - oA) >> 5), wB = (int)((oE - oB) >> 5);
+    const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + oA + lane;
+    const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + oB + lane;
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+    const uint32_t se = (uint32_t)a.se, kl = (uint32_t)a.k_left;
+    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    auto base2 = [&](long long k) -> uint32_t {
+      const uint32_t g = (uint32_t)a.row0 + (uint32_t)(k * 32) + lane;
+      const uint32_t blk = (g / se) * se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    uint32_t cA = base2(kA), cB = base2(kB);
+    float accA = 0.f, accB = 0.f;
+    const int wmax = wA > wB ? wA : wB;
+    for (int q = 0; q < wmax; q += U) {
+      uint32_t a8[U], b8[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a8[u] = (q + u < wA) ? __ldcs(pA + (q + u) * 32) : 0u;
+        b8[u] = (q + u < wB) ? __ldcs(pB + (q + u) * 32) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        S::run(a8[u], cA, x, accA, m_real, vmask);
+        S::run(b8[u], cB, x, accB, m_real, vmask);
+      }
+    }
+    const uint32_t sig = (uint32_t)a.sigma;
+    auto flush = [&](long long k, float acc) {
+      const uint32_t s = (uint32_t)(k * 32) + lane;
+      if ((long long)s < a.n_rows) {
+        uint32_t o = s;
+        if (a.mode == PSELL_MODE_IMPLICIT) {
+          const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
+                                                : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
+          o = (s / sig) * sig + pp;
+        }
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
+      }
+    };
+    flush(kA, accA);
+    if (hasB) flush(kB, accB);
+  }
   finish_dot<DOT>(a, dotv);
 }
 
@@ -943,7 +1041,19 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
     if constexpr (!REF && FastPolicy<CODEC, XT>::kHave) {
       if (a.variant != 2) {
         if (a.spw == 1) {
-          spmv_fast_kernel<CODEC, XT, DOT, 8><<<grid, kBlock, 0, st>>>(a);
+          const int nt = fast_nt();
+          const unsigned gnt = (unsigned)ceil_div(rows, nt);
+          const unsigned gd = (unsigned)ceil_div(ceil_div(a.n_slices, 2), kWarpsPerCta);
+          const int du = dual_chunk(a.narrow);
+          if (dual_slices(a.n_slices) && du == 12)
+            spmv_dual_kernel<CODEC, XT, DOT, 12><<<gd, kBlock, 0, st>>>(a);
+          else if (dual_slices(a.n_slices) && du == 16)
+            spmv_dual_kernel<CODEC, XT, DOT, 16><<<gd, kBlock, 0, st>>>(a);
+          else if (dual_slices(a.n_slices))
+            spmv_dual_kernel<CODEC, XT, DOT, 8><<<gd, kBlock, 0, st>>>(a);
+          else if (nt == 64) spmv_fast_kernel<CODEC, XT, DOT, 8, 64><<<gnt, 64, 0, st>>>(a);
+          else if (nt == 128) spmv_fast_kernel<CODEC, XT, DOT, 8, 128><<<gnt, 128, 0, st>>>(a);
+          else spmv_fast_kernel<CODEC, XT, DOT, 8, 256><<<gnt, 256, 0, st>>>(a);
         } else if (a.spw == 0) {
           const unsigned g = (unsigned)spmv_grid(a.n_slices, 32, true);
           spmv_persist_kernel<CODEC, XT, DOT, 8><<<g, kBlock, 0, st>>>(a);
@@ -1014,6 +1124,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.d = d->d;
   a.perm_bytes = d->sigma <= 256 ? 1 : 2;
   a.variant = 0;
+  a.narrow = 0;
   a.codec = d->codec;
   a.seg_len = 0;
   a.seg_slice = a.seg_q0 = a.long_slice = a.long_seg0 = nullptr;
@@ -1083,6 +1194,7 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
   cudaStream_t st = as_stream(stream);
   const bool ref = (flags & PSELL_SPMV_REF_ORDER) != 0;
   a.variant = (flags & PSELL_SPMV_TMA_STREAM) ? 2 : 0;
+  a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
   int bad = 1;
   switch (d->codec) {
     case PSELL_FP16: bad = dispatch_x<PSELL_FP16>(a, x_dtype, ref, st); break;
@@ -1173,6 +1285,8 @@ int64_t psell_spmv_dot_partials(const psell_desc* d) {
     const int spw = slices_per_warp(ns);
     if (d->codec != PSELL_FP32EMBED && spw > 1) return ceil_div(ceil_div(ns, spw), kWarps);
     if (d->codec != PSELL_FP32EMBED && spw == 0) return spmv_grid(ns, 32, true);
+    if (d->codec != PSELL_FP32EMBED && dual_slices(ns)) return ceil_div(ceil_div(ns, 2), kWarpsPerCta);
+    if (d->codec != PSELL_FP32EMBED) return ceil_div(ns * 32, fast_nt());
     return ceil_div(ns * 32, kBlock);
   }
   return ceil_div(d->n_rows, kBlock);
@@ -1180,9 +1294,10 @@ int64_t psell_spmv_dot_partials(const psell_desc* d) {
 
 int psell_spmv_dot(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
                    const float* x, float* y, const float* p_own, double* partials,
-                   const int32_t* skip_flag, void* stream, psell_error* err) {
+                   const int32_t* skip_flag, int32_t flags, void* stream, psell_error* err) {
   SpmvArgs a;
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
   a.x = x;
   a.y = y;
   a.p_own = p_own;

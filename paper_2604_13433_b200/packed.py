@@ -190,6 +190,13 @@ class PackSellMatrix:
         d.k_left, d.nnz = self.k_left, self.counts.nnz_real
         return d
 
+    def spmv_flags(self) -> int:
+        """Kernel-shape hint for psell_spmv / psell_spmv_dot: PSELL_SPMV_NARROW when the
+        mean slice width is <= 12 steps (7-point rows), so one 12-step chunk covers a slice."""
+        if self.n_slices == 0:
+            return 0
+        return 4 if self.n_stored <= 12 * self.c * self.n_slices else 0
+
     def spmv_bytes(self, x_itemsize: int, y_itemsize: Optional[int] = None, with_perm: bool = True,
                    x_elems: Optional[int] = None) -> int:
         """Algorithmic bytes of one SpMV: words + slice offsets + x once + y (+ perm)."""
@@ -336,7 +343,7 @@ def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool, pipe: int = 0):
             return y
     rc = lib.psell_spmv(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
                         _lib.ptr(xd), _dev.T_DT_CODE[xd.dtype], _lib.ptr(y),
-                        (_lib.SPMV_REF_ORDER if ref_order else 0) | (2 if pipe else 0),
+                        (_lib.SPMV_REF_ORDER if ref_order else 0) | (2 if pipe else 0) | M.spmv_flags(),
                         _lib.stream_handle(), err)
     _lib.check(rc, err, M.fmt)
     return y

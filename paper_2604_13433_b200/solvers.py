@@ -268,7 +268,7 @@ class _InnerPCG:
             _gather_full(self.comm, self.p, self.p_full)
             rc = lib.psell_spmv_dot(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
                                     self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
-                                    d.p(d.partials), d.p(d.flags), st, err)
+                                    d.p(d.partials), d.p(d.flags), M.spmv_flags(), st, err)
             L.check(rc, err, M.fmt)
             lib.psell_sum_partials(d.p(d.partials), self.npart, 1, d.p(d.loc, 1), d.p(d.flags), st)
             g, stride = d.gather()

@@ -24,7 +24,7 @@ err = L.PsellError()
 steps = {
     "spmv_dot": lambda: lib.psell_spmv_dot(inner.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
                                            inner.p_full.data_ptr(), inner.q.data_ptr(), inner.p.data_ptr(),
-                                           d.p(d.partials), d.p(d.flags), st, err),
+                                           d.p(d.partials), d.p(d.flags), M.spmv_flags(), st, err),
     "sum_partials(spmv)": lambda: lib.psell_sum_partials(d.p(d.partials), inner.npart, 1, d.p(d.loc, 1),
                                                          d.p(d.flags), st),
     "alpha": lambda: lib.psell_ipcg_alpha(d.p(d.loc, 1), 1, 8, d.p(d.scal), d.p(d.flags), st),
