@@ -296,7 +296,7 @@ def run_pcg(args, world, rank, comm, peak):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         if comm is not None:
-            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda" if comm.nccl else "cpu")
             comm.dist.all_reduce(tt, op=comm.dist.ReduceOp.MAX)
             dt = tt.item()
         return rep, dt
@@ -356,21 +356,32 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PSELL_SHARE_GPU=1 + PSELL_DIST_BACKEND=gloo: every rank on cuda:0 over gloo, to
+    # exercise the multi-rank bench path on a single GPU (the real run uses NCCL)
+    if os.environ.get("PSELL_SHARE_GPU"):
+        local = 0
+    backend = os.environ.get("PSELL_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def allreduce(v, op):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=op)
         return t.item()
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     n = cfg_rows(cfg)
     sig = cfg["sigma"]
@@ -495,6 +506,8 @@ def run_ours(args, cfg):
                          f"global k_left; oracle port of packsell_spmv, numpy single thread; "
                          f"{r['gflops']:.4f} GFLOP/s"}
 
+    # every collective runs on all ranks, before the rank-0-only report
+    bytes_noperm_all = allreduce(float(bytes_noperm), dist.ReduceOp.SUM if world > 1 else None)
     pcg = None
     m_info = (M.n_stored, list(M.counts))
     h2d_b, d2h_b = int(xh.numel() * xh.element_size()), int(yh.numel() * yh.element_size())
@@ -518,7 +531,7 @@ def run_ours(args, cfg):
             "pct_hbm_peak": value / (peak * world),
             "gflops": gflops,
             "bytes_per_step": int(bytes_all),
-            "bytes_per_step_without_perm": int(allreduce(float(bytes_noperm), dist.ReduceOp.SUM if world > 1 else None)),
+            "bytes_per_step_without_perm": int(bytes_noperm_all),
             "build_s": t_b2 - t_b1, "gen_s": t_b1 - t_b0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
