@@ -414,6 +414,8 @@ def run_ours(args, cfg):
     x = (torch.rand(n, generator=g, device=dev, dtype=torch.float32) * 2 - 1).to(xt)
     y = torch.empty(M.n_rows, dtype=xt, device=dev)
     xsz = x.element_size()
+    from paper_2604_13433_b200 import _dev, _lib
+    kernel_name = _lib.lib().psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
     bytes_local = M.spmv_bytes(xsz, xsz, with_perm=True, x_elems=touched)
     bytes_noperm = M.spmv_bytes(xsz, xsz, with_perm=False, x_elems=touched)
     st = torch.cuda.current_stream()
@@ -536,7 +538,7 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                          "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                         "kernel": "spmv_fast_kernel (register-pipelined, one warp per slice, one launch per step)"},
+                         "kernel": f"{kernel_name} (one launch per step; ncu per-launch DRAM bytes in traffic)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": h2d_b,

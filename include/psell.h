@@ -143,6 +143,10 @@ PSELL_API int psell_spmv(const psell_desc* desc, const void* pack, const int64_t
                const void* x, int32_t x_dtype, void* y, int32_t flags, void* stream,
                psell_error* err);
 
+/* Name of the kernel psell_spmv launches for this descriptor, x dtype and flags
+ * (the same dispatch, no launch): lets a benchmark report the kernel it timed. */
+PSELL_API const char* psell_spmv_kernel_name(const psell_desc* desc, int32_t x_dtype, int32_t flags);
+
 /* Long-slice segmentation for irregular (power-law) matrices.  Slices wider than
  * seg_len steps are cut into segments (seg_slice/seg_q0: the slice and first
  * step of each; long_slice/long_seg0: the long slices and their first segment,

@@ -55,6 +55,7 @@ _SIGS = {
     "psell_sort_workspace_bytes": (c_size_t, [c_int64, c_int32]),
     "psell_sort_order": (c_int32, [_P, c_int64, c_int32, _P, _P, c_size_t, _P, _E]),
     "psell_spmv": (c_int32, [_D, _P, _P, _P, _P, c_int32, _P, c_int32, _P, _E]),
+    "psell_spmv_kernel_name": (ctypes.c_char_p, [_D, c_int32, c_int32]),
     "psell_spmv_seg_checkpoints": (c_int32, [_D, _P, _P, c_int32, c_int64, _P, _P, c_int64, _P, _P, _P, _P, _E]),
     "psell_spmv_segmented": (c_int32, [_D, _P, _P, _P, _P, c_int32, _P, c_int32, c_int64, _P, _P, _P, _P,
                                        c_int64, _P, _P, _P, _E]),

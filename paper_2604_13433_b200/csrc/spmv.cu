@@ -1206,6 +1206,24 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
   return ok(err);
 }
 
+const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t flags) {
+  if (!d || d->n_rows <= 0) return "none";
+  const bool ref = (flags & PSELL_SPMV_REF_ORDER) != 0;
+  const bool fast = !ref && d->codec != PSELL_FP32EMBED && x_dtype != PSELL_DT_F64;
+  if (d->c != 32) return "spmv_generic_kernel";
+  if (!fast) return "spmv_c32_kernel";
+  if (flags & PSELL_SPMV_TMA_STREAM) return "spmv_stream_kernel";
+  const long long ns = ceil_div(d->n_rows, d->c);
+  const int spw = slices_per_warp(ns);
+  if (spw == 0) return "spmv_persist_kernel";
+  if (spw > 1) return "spmv_multi_kernel";
+  if (dual_slices(ns)) {
+    const int du = dual_chunk((flags & PSELL_SPMV_NARROW) != 0);
+    return du == 12 ? "spmv_dual_kernel<U=12>" : du == 16 ? "spmv_dual_kernel<U=16>" : "spmv_dual_kernel<U=8>";
+  }
+  return "spmv_fast_kernel";
+}
+
 int psell_spmv_seg_checkpoints(const psell_desc* d, const void* pack, const int64_t* offset,
                                int32_t seg_len, int64_t n_seg, const int32_t* seg_slice,
                                const int32_t* seg_q0, int64_t n_long, const int32_t* long_slice,
