@@ -306,6 +306,19 @@ PSELL_API int psell_gen_powerlaw_fill(int64_t n, uint64_t seed, const double* th
                                       const int64_t* row_ptr, int32_t* col_idx, double* values,
                                       void* stream, psell_error* err);
 
+/* ---- K6 metrics: backward error (replaces metrics.py:43-66 backward_error /
+ * inf_norm_matrix).  One pass over the f64 CSR A (unquantised source), x and
+ * y (any psell_dtype each, widened to f64).  Writes out[0] = max_i |y_i - (Ax)_i|
+ * ((Ax)_i row-sequential as csr_spmv, matrix.py:272-291), out[1] = ||A||_inf
+ * (max absolute row sum), out[2] = ||x||_inf; the host forms out[0] / (out[1] *
+ * out[2]) and raises the reference's ValueError when the denominator is 0.
+ * Order-independent maxima: bit-identical to the reference.  out is a device
+ * pointer to 3 doubles. */
+PSELL_API int psell_backward_error(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                                   const int32_t* col_idx, const double* values, const void* x,
+                                   int32_t x_dtype, const void* y, int32_t y_dtype, double* out,
+                                   void* stream, psell_error* err);
+
 #ifdef __cplusplus
 }
 #endif
