@@ -121,7 +121,7 @@ def test_bench_spmv_reports(rng):
     assert M.counts.n_dummy > 0
     x = np.ones(200, dtype=np.float32)
     rep = P.bench_spmv(M, x, reps=5, warmup=1, source=A)
-    assert rep.format_name == "packsell-e8m20" and rep.elapsed_per_call > 0
+    assert rep.format_name == "packsell-e8m21" and rep.elapsed_per_call > 0
     assert rep.gflops == pytest.approx(2 * A.nnz / rep.elapsed_per_call / 1e9)
     assert rep.y.dtype == np.float32 and rep.y.shape == (300,)
     assert rep.backward_error == P.backward_error(A, x, rep.y)
