@@ -43,7 +43,20 @@ struct SpmvArgs {
   float* seg_partial;         // [n_seg][32] partial sums
   const int32_t* long_slice;  // [n_long] slices run as segments
   const int32_t* long_seg0;   // [n_long + 1] first segment of each long slice
+  // n / se and n / sigma for n < 2^31 as (umulhi(n, m) + n) >> l (Granlund-Montgomery)
+  uint32_t se_m, se_l, sig_m, sig_l;
 };
+
+// (m, l) with n / d == (umulhi(n, m) + n) >> l for every n < 2^31 (d >= 1)
+static inline void magic_div(uint32_t d, uint32_t& m, uint32_t& l) {
+  l = 0;
+  while ((1ull << l) < d) ++l;
+  m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+}
+
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t l) {
+  return (__umulhi(n, m) + n) >> l;
+}
 
 template <int CODEC> struct WordOf { using T = uint32_t; };
 template <> struct WordOf<PSELL_FP32EMBED> { using T = uint64_t; };
@@ -172,6 +185,18 @@ static int dual_chunk(bool narrow) {
     if (v == 8 || v == 12 || v == 16) return v;
   }
   return narrow ? 12 : 8;  // 12 covers a whole 7-point slice in one chunk (sweep: +14 %)
+}
+
+// exact-tail pair kernel instead of the chunk-rounded dual kernel (PSELL_PAIR=0: dual, A/B)
+static bool pair_kernel() {
+  if (const char* e = getenv("PSELL_PAIR")) return atoi(e) != 0;
+  return true;
+}
+
+// pair kernel for wide slices too (PSELL_PAIR_WIDE=1, A/B; default: dual kernel)
+static bool pair_wide() {
+  if (const char* e = getenv("PSELL_PAIR_WIDE")) return atoi(e) != 0;
+  return false;
 }
 
 // threads per CTA of the one-warp-per-slice kernel (PSELL_NT overrides, A/B)
@@ -461,6 +486,126 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
     };
     flush(kA, accA);
     if (hasB) flush(kB, accB);
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
+// ---- pair kernel (C == 32): a warp runs slices 2w and 2w+1.  Full U-step
+// chunks run in lockstep with unpredicated loads; the tails (< U steps) load
+// with one predicate per word from a fixed base (immediate offsets).  Base offsets and output rows use multiply-high
+// division by sigma; the perm bytes are loaded before the word stream so
+// their latency hides under it.
+template <int CODEC, typename XT, bool DOT, int U, bool HOIST>
+__global__ void __launch_bounds__(kBlock, 6) spmv_pair_kernel(const SpmvArgs a) {
+    using S = FastStep<CODEC, XT>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const uint32_t wg = (uint32_t)((blockIdx.x * (unsigned)kBlock + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const uint32_t kA = 2u * wg, kB = kA + 1u;
+  const uint32_t ns = (uint32_t)a.n_slices;
+  double dotv = 0.0;
+  if (kA < ns) {
+    const bool hasB = kB < ns;
+    const uint32_t n_rows = (uint32_t)a.n_rows;
+    const uint32_t sA = kA * 32u + lane, sB = sA + 32u;
+    // output rows; with HOIST (narrow slices) the perm bytes load before the
+    // word stream so their latency hides under it (wide slices: at the end,
+    // where the registers are free)
+    const bool impl = a.mode == PSELL_MODE_IMPLICIT;
+    auto out_of = [&](uint32_t k, uint32_t s) -> uint32_t {
+      if (!impl) return s;
+      const uint32_t blk = fast_div(k * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma;
+      const uint32_t pp = s >= n_rows ? 0u
+                          : a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + s)
+                                              : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + s);
+      return blk + pp;
+    };
+    uint32_t oA = sA, oB = sB;
+    if constexpr (HOIST) {
+      oA = out_of(kA, sA);
+      oB = out_of(kB, sB);
+    }
+    const long long o0 = a.offset[kA], o1 = a.offset[kA + 1];
+    const long long o2 = hasB ? a.offset[kA + 2] : o1;
+    const int wA = (int)((o1 - o0) >> 5), wB = (int)((o2 - o1) >> 5);
+    const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + o0 + lane;
+    const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + o1 + lane;
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+    const uint32_t kl = (uint32_t)a.k_left;
+    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    auto base2 = [&](uint32_t k) -> uint32_t {
+      const uint32_t g = (uint32_t)a.row0 + k * 32u + lane;
+      const uint32_t blk = a.se == 1 ? g : fast_div(g, a.se_m, a.se_l) * (uint32_t)a.se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    uint32_t cA = base2(kA), cB = base2(kB);
+    float accA = 0.f, accB = 0.f;
+    uint32_t wa[U], wb[U];
+    const int both = (wA < wB ? wA : wB) / U;
+    int q = 0;
+    for (int c = 0; c < both; ++c, q += U) {  // lockstep full chunks
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        wa[u] = __ldcs(pA + (q + u) * 32);
+        wb[u] = __ldcs(pB + (q + u) * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        S::run(wa[u], cA, x, accA, m_real, vmask);
+        S::run(wb[u], cB, x, accB, m_real, vmask);
+      }
+    }
+    int qa = q, qb = q;
+    for (; qa + U <= wA; qa += U) {  // the longer slice's remaining full chunks
+#pragma unroll
+      for (int u = 0; u < U; ++u) wa[u] = __ldcs(pA + (qa + u) * 32);
+#pragma unroll
+      for (int u = 0; u < U; ++u) S::run(wa[u], cA, x, accA, m_real, vmask);
+    }
+    for (; qb + U <= wB; qb += U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) wb[u] = __ldcs(pB + (qb + u) * 32);
+#pragma unroll
+      for (int u = 0; u < U; ++u) S::run(wb[u], cB, x, accB, m_real, vmask);
+    }
+    // tails (< U steps): predicated loads from a fixed base, branch-free decode
+    // (zero words past the width only move nothing: delta 0, FMA predicated off),
+    // A and B interleaved so all gathers issue before the first FMA waits
+    const int ra = wA - qa, rb = wB - qb;
+    if (ra > 0 || rb > 0) {
+      const uint32_t* tA = pA + qa * 32;
+      const uint32_t* tB = pB + qb * 32;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        wa[u] = u < ra ? __ldcs(tA + u * 32) : 0u;
+        wb[u] = u < rb ? __ldcs(tB + u * 32) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        S::run(wa[u], cA, x, accA, m_real, vmask);
+        S::run(wb[u], cB, x, accB, m_real, vmask);
+      }
+    }
+    auto flush = [&](uint32_t s, uint32_t o, float acc) {
+      if (s < n_rows) {
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
+      }
+    };
+    if constexpr (!HOIST) {
+      oA = out_of(kA, sA);
+      oB = out_of(kB, sB);
+    }
+    flush(sA, oA, accA);
+    if (hasB) flush(sB, oB, accB);
   }
   finish_dot<DOT>(a, dotv);
 }
@@ -1045,7 +1190,11 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
           const unsigned gnt = (unsigned)ceil_div(rows, nt);
           const unsigned gd = (unsigned)ceil_div(ceil_div(a.n_slices, 2), kWarpsPerCta);
           const int du = dual_chunk(a.narrow);
-          if (dual_slices(a.n_slices) && du == 12)
+          if (dual_slices(a.n_slices) && a.narrow && pair_kernel()) {
+            spmv_pair_kernel<CODEC, XT, DOT, 12, true><<<gd, kBlock, 0, st>>>(a);
+          } else if (dual_slices(a.n_slices) && pair_wide()) {
+            spmv_pair_kernel<CODEC, XT, DOT, 8, false><<<gd, kBlock, 0, st>>>(a);
+          } else if (dual_slices(a.n_slices) && du == 12)
             spmv_dual_kernel<CODEC, XT, DOT, 12><<<gd, kBlock, 0, st>>>(a);
           else if (dual_slices(a.n_slices) && du == 16)
             spmv_dual_kernel<CODEC, XT, DOT, 16><<<gd, kBlock, 0, st>>>(a);
@@ -1131,6 +1280,8 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.seg_c2 = nullptr;
   a.seg_partial = nullptr;
   a.spw = d->c == 32 ? slices_per_warp(a.n_slices) : 1;
+  magic_div((uint32_t)(a.se > 0 ? a.se : 1), a.se_m, a.se_l);
+  magic_div((uint32_t)(a.sigma > 0 ? a.sigma : 1), a.sig_m, a.sig_l);
   return PSELL_OK;
 }
 
@@ -1217,6 +1368,8 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   const int spw = slices_per_warp(ns);
   if (spw == 0) return "spmv_persist_kernel";
   if (spw > 1) return "spmv_multi_kernel";
+  if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel()) return "spmv_pair_kernel<U=12>";
+  if (dual_slices(ns) && pair_wide()) return "spmv_pair_kernel<U=8>";
   if (dual_slices(ns)) {
     const int du = dual_chunk((flags & PSELL_SPMV_NARROW) != 0);
     return du == 12 ? "spmv_dual_kernel<U=12>" : du == 16 ? "spmv_dual_kernel<U=16>" : "spmv_dual_kernel<U=8>";
