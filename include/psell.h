@@ -167,8 +167,8 @@ PSELL_API int psell_spmv_segmented(const psell_desc* desc, const void* pack, con
                                    int64_t n_long, const int32_t* long_slice, const int32_t* long_seg0,
                                    void* stream, psell_error* err);
 
-/* Number of double partials psell_spmv_dot writes (one per CTA). */
-PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc);
+/* Number of double partials psell_spmv_dot writes (one per CTA) for these flags. */
+PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc, int32_t flags);
 
 /* SpMV fused with the PCG curvature dot: also writes partials[b] =
  * sum over the CTA's rows of (double)p_own[i] * (double)y[i] (solvers.py:294-295),

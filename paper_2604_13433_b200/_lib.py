@@ -59,7 +59,7 @@ _SIGS = {
     "psell_spmv_seg_checkpoints": (c_int32, [_D, _P, _P, c_int32, c_int64, _P, _P, c_int64, _P, _P, _P, _P, _E]),
     "psell_spmv_segmented": (c_int32, [_D, _P, _P, _P, _P, c_int32, _P, c_int32, c_int64, _P, _P, _P, _P,
                                        c_int64, _P, _P, _P, _E]),
-    "psell_spmv_dot_partials": (c_int64, [_D]),
+    "psell_spmv_dot_partials": (c_int64, [_D, c_int32]),
     "psell_spmv_dot": (c_int32, [_D, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P, _E]),
     "psell_to_csr_workspace_bytes": (c_size_t, [_D]),
     "psell_to_csr_plan": (c_int32, [_D, _P, _P, _P, _P, c_size_t, _P, POINTER(c_int64), _P, _E]),

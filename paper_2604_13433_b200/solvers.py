@@ -248,7 +248,7 @@ class _InnerPCG:
             self.p = self.p_full[self.row0:self.row0 + self.n]
         lib = _lib.lib()
         self.desc = M.desc()
-        self.npart = lib.psell_spmv_dot_partials(self.desc)
+        self.npart = lib.psell_spmv_dot_partials(self.desc, M.spmv_flags())
         self.d = _Dev(max(self.npart, _lib.RED_BLOCKS), comm)
         self.graph = None
         self.graph_in = None

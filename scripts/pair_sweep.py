@@ -46,7 +46,7 @@ for name, kind, scale, pre, dt in cases:
         outs[pair] = y.clone()
         line = f"{name:20s} PAIR={pair} {kname:24s} {ms * 1e3:8.1f} us {nb / ms / 1e6:8.1f} GB/s"
         if dt == torch.float32:
-            npart = lib.psell_spmv_dot_partials(M.desc())
+            npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
             part = torch.zeros(max(npart, 1), dtype=torch.float64, device="cuda")
             err = _lib.PsellError()
             st = _lib.stream_handle()

@@ -108,7 +108,7 @@ def test_workspace_sizing_is_host_only():
     ws = l.psell_build_workspace_bytes(d)
     assert 3 * 4 * (1 << 24) <= ws < 64 * (1 << 24)
     # persistent TMA grid: SMs x CTAs/SM (148 x 6 when no device is visible)
-    assert 1 <= l.psell_spmv_dot_partials(d) <= (1 << 24) // 256
+    assert 1 <= l.psell_spmv_dot_partials(d, 0) <= (1 << 24) // 256
 
 
 def test_no_cpu_fallback_without_gpu():
