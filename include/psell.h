@@ -239,6 +239,26 @@ PSELL_API int psell_ipcg_alpha(const double* parts, int32_t n_parts, int32_t str
 PSELL_API int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
                       const float* inv_diag, const double* scal, const int32_t* iflags,
                       double* partials, double* local_out, void* stream);
+/* Single-GPU fused variants of the inner-PCG step (one launch each instead of
+ * kernel + partial sum + scalar kernel).  `ticket` is a device array of
+ * 1 + ceil(P / 256) unsigned ints (P = partials of the launch: psell_spmv_dot_partials
+ * or PSELL_RED_BLOCKS), zero before the first call and left zero by every call;
+ * `partials` holds P + ceil(P / 256) doubles.  The last CTAs of the launch sum the
+ * partials in a fixed two-level order (deterministic) and perform the scalar step.  psell_spmv_dot_alpha = psell_spmv_dot + psell_sum_partials +
+ * psell_ipcg_alpha (solvers.py:294-299); psell_ipcg_update_beta =
+ * psell_ipcg_update + psell_ipcg_beta (solvers.py:300-306). */
+PSELL_API int psell_spmv_dot_alpha(const psell_desc* desc, const void* pack, const int64_t* offset,
+                                   const void* perm, const float* x, float* y, const float* p_own,
+                                   double* partials, double* scal, int32_t* iflags, unsigned* ticket,
+                                   int32_t flags, void* stream, psell_error* err);
+PSELL_API int psell_ipcg_update_beta(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
+                                     const float* inv_diag, double* scal, int32_t* iflags, double* partials,
+                                     unsigned* ticket, void* stream);
+/* With x == NULL, psell_ipcg_update(_beta) only does r -= alpha q, z = P(r), r.z;
+ * psell_ipcg_direction_x then applies x += alpha p_old and p = z + beta p_old in
+ * one pass (same f32 ops, 4 fewer bytes per row per iteration). */
+PSELL_API int psell_ipcg_direction_x(int64_t n, float* p, const float* z, float* x, const double* scal,
+                                     const int32_t* iflags, void* stream);
 PSELL_API int psell_ipcg_beta(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                     void* stream);
 PSELL_API int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal,

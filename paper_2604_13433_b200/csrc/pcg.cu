@@ -105,14 +105,61 @@ __device__ __forceinline__ void upd1(float a, float& xv, float& rv, float& zv, f
   zv = inv ? __fmul_rn(rv, inv[i]) : rv;
 }
 
+// r -= a q; z = P(r) only (the x += a p half moves into the direction kernel)
+__device__ __forceinline__ void upd1_r(float a, float& rv, float& zv, float qv, const float* inv, long long i) {
+  rv = __fsub_rn(rv, __fmul_rn(a, qv));
+  zv = inv ? __fmul_rn(rv, inv[i]) : rv;
+}
+
+// Fused tail of one inner iteration, x half of the update deferred here:
+// x += alpha p_old; p = z + beta p_old (solvers.py:301, 307).  Same separately
+// rounded f32 ops as ipcg_update + ipcg_direction, one pass over p instead of two.
+__global__ void __launch_bounds__(kBlock) ipcg_direction_x_kernel(long long n, float* __restrict__ p,
+                                                                  const float* __restrict__ z,
+                                                                  float* __restrict__ x,
+                                                                  const double* __restrict__ scal,
+                                                                  const int32_t* __restrict__ iflags) {
+  if (iflags[0]) return;
+  const float al = __double2float_rn(scal[2]);
+  const float b = __double2float_rn(scal[3]);
+  const long long gt = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gs = (long long)gridDim.x * kBlock;
+  long long done = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(z) |
+                     reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  if (vec) {
+    const long long n4 = n >> 2;
+    for (long long i4 = gt; i4 < n4; i4 += gs) {
+      float4 pv = reinterpret_cast<float4*>(p)[i4];
+      float4 xv = reinterpret_cast<float4*>(x)[i4];
+      const float4 zv = reinterpret_cast<const float4*>(z)[i4];
+      xv.x = __fadd_rn(xv.x, __fmul_rn(al, pv.x));
+      xv.y = __fadd_rn(xv.y, __fmul_rn(al, pv.y));
+      xv.z = __fadd_rn(xv.z, __fmul_rn(al, pv.z));
+      xv.w = __fadd_rn(xv.w, __fmul_rn(al, pv.w));
+      pv.x = __fadd_rn(zv.x, __fmul_rn(b, pv.x));
+      pv.y = __fadd_rn(zv.y, __fmul_rn(b, pv.y));
+      pv.z = __fadd_rn(zv.z, __fmul_rn(b, pv.z));
+      pv.w = __fadd_rn(zv.w, __fmul_rn(b, pv.w));
+      reinterpret_cast<float4*>(x)[i4] = xv;
+      reinterpret_cast<float4*>(p)[i4] = pv;
+    }
+    done = n4 * 4;
+  }
+  for (long long i = done + gt; i < n; i += gs) {
+    const float pv = p[i];
+    x[i] = __fadd_rn(x[i], __fmul_rn(al, pv));
+    p[i] = __fadd_rn(z[i], __fmul_rn(b, pv));
+  }
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float* __restrict__ x, float* r,
                                                              float* z, const float* __restrict__ p,
                                                              const float* __restrict__ q,
                                                              const float* __restrict__ inv,
-                                                             const double* __restrict__ scal,
-                                                             const int32_t* __restrict__ iflags,
-                                                             double* __restrict__ parts) {
+                                                             double* scal, int32_t* iflags,
+                                                             double* __restrict__ parts, unsigned* ticket) {
   if (iflags[0]) return;
   __shared__ double sh[kBlock / 32];
   const float a = __double2float_rn(scal[2]);
@@ -123,17 +170,24 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
   if (VEC) {
     const long long n4 = n >> 2;
     for (long long i4 = gt; i4 < n4; i4 += gs) {
-      float4 xv = reinterpret_cast<float4*>(x)[i4];
       float4 rv = reinterpret_cast<float4*>(r)[i4];
-      const float4 pv = reinterpret_cast<const float4*>(p)[i4];
       const float4 qv = reinterpret_cast<const float4*>(q)[i4];
       float4 zv;
       const long long i = i4 * 4;
-      upd1(a, xv.x, rv.x, zv.x, pv.x, qv.x, inv, i);
-      upd1(a, xv.y, rv.y, zv.y, pv.y, qv.y, inv, i + 1);
-      upd1(a, xv.z, rv.z, zv.z, pv.z, qv.z, inv, i + 2);
-      upd1(a, xv.w, rv.w, zv.w, pv.w, qv.w, inv, i + 3);
-      reinterpret_cast<float4*>(x)[i4] = xv;
+      if (x) {
+        float4 xv = reinterpret_cast<float4*>(x)[i4];
+        const float4 pv = reinterpret_cast<const float4*>(p)[i4];
+        upd1(a, xv.x, rv.x, zv.x, pv.x, qv.x, inv, i);
+        upd1(a, xv.y, rv.y, zv.y, pv.y, qv.y, inv, i + 1);
+        upd1(a, xv.z, rv.z, zv.z, pv.z, qv.z, inv, i + 2);
+        upd1(a, xv.w, rv.w, zv.w, pv.w, qv.w, inv, i + 3);
+        reinterpret_cast<float4*>(x)[i4] = xv;
+      } else {
+        upd1_r(a, rv.x, zv.x, qv.x, inv, i);
+        upd1_r(a, rv.y, zv.y, qv.y, inv, i + 1);
+        upd1_r(a, rv.z, zv.z, qv.z, inv, i + 2);
+        upd1_r(a, rv.w, zv.w, qv.w, inv, i + 3);
+      }
       reinterpret_cast<float4*>(r)[i4] = rv;
       if (inv) reinterpret_cast<float4*>(z)[i4] = zv;
       v += (double)rv.x * (double)zv.x;
@@ -144,15 +198,23 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
     done = n4 * 4;
   }
   for (long long i = done + gt; i < n; i += gs) {
-    float xv = x[i], rv = r[i], zv;
-    upd1(a, xv, rv, zv, p[i], q[i], inv, i);
-    x[i] = xv;
+    float rv = r[i], zv;
+    if (x) {
+      float xv = x[i];
+      upd1(a, xv, rv, zv, p[i], q[i], inv, i);
+      x[i] = xv;
+    } else {
+      upd1_r(a, rv, zv, q[i], inv, i);
+    }
     r[i] = rv;
     if (inv) z[i] = zv;
     v += (double)rv * (double)zv;
   }
   v = block_sum<kBlock>(v, sh);
   if (threadIdx.x == 0) parts[blockIdx.x] = v;
+  double rz_new;  // fused beta (psell_ipcg_update_beta): the last CTA finishes the iteration's scalars
+  if (ticket && last_cta_sum<kBlock>(parts, ticket, rz_new, sh) && threadIdx.x == 0)
+    ipcg_beta_step(rz_new, scal, iflags);
 }
 
 // solvers.py:304-306
@@ -391,9 +453,23 @@ int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, c
   cudaStream_t st = as_stream(stream);
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(z) |
                      reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
-  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials);
-  else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials);
+  double* sc = const_cast<double*>(scal);
+  int32_t* fl = const_cast<int32_t*>(iflags);
+  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, sc, fl, partials, nullptr);
+  else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, sc, fl, partials, nullptr);
   finalize(partials, kRB, 1, local_out, iflags, st);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_update_beta(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
+                           const float* inv_diag, double* scal, int32_t* iflags, double* partials,
+                           unsigned* ticket, void* stream) {
+  if (!ticket) return 1;
+  cudaStream_t st = as_stream(stream);
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(z) |
+                     reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
+  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket);
+  else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket);
   return LAUNCH_OK();
 }
 
@@ -405,6 +481,12 @@ int psell_ipcg_beta(const double* parts, int32_t n_parts, int32_t stride, double
 int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal,
                          const int32_t* iflags, void* stream) {
   ipcg_direction_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, scal, iflags);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_direction_x(int64_t n, float* p, const float* z, float* x, const double* scal,
+                           const int32_t* iflags, void* stream) {
+  ipcg_direction_x_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, x, scal, iflags);
   return LAUNCH_OK();
 }
 

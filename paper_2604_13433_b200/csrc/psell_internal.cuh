@@ -212,6 +212,64 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* NT/32 */) {
   return t;
 }
 
+// Fixed-order grid reduction epilogue ("last CTA reduces"), two levels so no
+// thread ever walks a long chain of dependent loads.  Thread 0 of every CTA
+// has stored parts[blockIdx.x].  CTAs form groups of NT; the last CTA of a
+// group to arrive (ticket tickets[1 + g]) sums the group's partials (one load
+// per thread, fixed CTA tree) into parts[gridDim.x + g]; the last group to
+// finish (ticket tickets[0]) sums the group partials the same way.  Every sum
+// has a fixed association, so the total is deterministic run to run.  Returns
+// true in that final CTA (total valid in thread 0) and re-arms its tickets.
+// Needs parts[gridDim.x + ceil(gridDim.x / NT)] and tickets[1 + ceil(gridDim.x / NT)],
+// all tickets zero before the first launch.
+template <int NT>
+__device__ __forceinline__ bool last_cta_sum(double* parts, unsigned* tickets, double& total,
+                                             double* sh /* NT/32 */) {
+  __shared__ unsigned s_last;
+  const unsigned n_grp = (gridDim.x + NT - 1) / NT;
+  const unsigned g = blockIdx.x / NT;
+  const unsigned g_size = min((unsigned)NT, gridDim.x - g * NT);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(tickets + 1 + g, 1u) == g_size - 1;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  double v = threadIdx.x < g_size ? __ldcg(parts + g * NT + threadIdx.x) : 0.0;
+  v = block_sum<NT>(v, sh);
+  if (threadIdx.x == 0) {
+    parts[gridDim.x + g] = v;
+    tickets[1 + g] = 0u;
+    __threadfence();
+    s_last = atomicAdd(tickets, 1u) == n_grp - 1;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  double w = 0.0;
+  for (unsigned i = threadIdx.x; i < n_grp; i += NT) w += __ldcg(parts + gridDim.x + i);
+  total = block_sum<NT>(w, sh);
+  if (threadIdx.x == 0) tickets[0] = 0u;
+  return true;
+}
+
+// inner-PCG scalar steps shared by the fused epilogues (solvers.py:295-299, 304-306)
+// scal: [0]=rz [1]=pq [2]=alpha [3]=beta [4]=rz_new ; iflags: [0]=breakdown [1]=done
+__device__ __forceinline__ void ipcg_alpha_step(double pq, double* scal, int32_t* iflags) {
+  scal[1] = pq;
+  if (pq <= 0.0 || !isfinite(pq) || scal[0] == 0.0) {
+    iflags[0] = 1;
+    return;
+  }
+  scal[2] = scal[0] / pq;
+}
+
+__device__ __forceinline__ void ipcg_beta_step(double rz_new, double* scal, int32_t* iflags) {
+  scal[4] = rz_new;
+  scal[3] = rz_new / scal[0];
+  scal[0] = rz_new;
+  iflags[1] += 1;
+}
+
 }  // namespace psell
 
 namespace psell {

@@ -28,6 +28,10 @@ struct SpmvArgs {
   const float* p_own;
   double* partials;
   const int32_t* skip;
+  // fused alpha epilogue (psell_spmv_dot_alpha): last CTA sums the partials
+  unsigned* ticket;
+  double* scal;
+  int32_t* iflags;
   long long n_rows, n_cols, n_slices, row0, k_left;
   int c, se, sigma, mode, d, perm_bytes;
   int variant;  // 0: register-pipelined kernels (default), 2: persistent TMA stream
@@ -167,6 +171,9 @@ __device__ __forceinline__ void finish_dot(const SpmvArgs& a, double v) {
     __shared__ double sh[NT / 32];
     const double t = block_sum<NT>(v, sh);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
+    double pq;
+    if (a.ticket && last_cta_sum<NT>(a.partials, a.ticket, pq, sh) && threadIdx.x == 0)
+      ipcg_alpha_step(pq, a.scal, a.iflags);
   }
 }
 
@@ -202,6 +209,23 @@ static int pair_nt(bool dot) {
     if (v == 64 || v == 128 || v == 256) return v;
   }
   return dot ? 256 : 128;
+}
+
+// persistent grid-stride pair kernel: one resident wave of 6 CTAs per SM walks the
+// slice pairs (PSELL_PAIR_PERSIST = CTAs per SM, 0 = one CTA per 8 pairs; A/B).
+// 7-point 256^3: 164 vs 170 us plain, 169 vs 183 us with the fused dot, whose
+// partials (and fixed-order last-CTA sum) shrink to one per resident CTA.
+// Returns its grid (0 = not used).
+static int sm_count();
+static unsigned pair_persist_grid(long long n_slices, bool dot) {
+  int per_sm = 6;
+  if (const char* e = getenv("PSELL_PAIR_PERSIST")) per_sm = atoi(e);
+  (void)dot;
+  if (per_sm <= 0) return 0;
+  if (per_sm > 6) per_sm = 6;
+  const long long full = ceil_div(ceil_div(n_slices, 2), kWarpsPerCta);
+  const long long cap = (long long)sm_count() * per_sm;
+  return (unsigned)(full < cap ? full : cap);
 }
 
 // pair kernel for wide slices too (PSELL_PAIR_WIDE=1, A/B; default: dual kernel)
@@ -506,18 +530,19 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
 // with one predicate per word from a fixed base (immediate offsets).  Base offsets and output rows use multiply-high
 // division by sigma; the perm bytes are loaded before the word stream so
 // their latency hides under it.
-template <int CODEC, typename XT, bool DOT, int U, bool HOIST, int NT = kBlock>
+template <int CODEC, typename XT, bool DOT, int U, bool HOIST, int NT = kBlock, bool PERSIST = false>
 __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const SpmvArgs a) {
     using S = FastStep<CODEC, XT>;
   if constexpr (DOT) {
     if (a.skip && *a.skip) return;
   }
-  const uint32_t wg = (uint32_t)((blockIdx.x * (unsigned)NT + threadIdx.x) >> 5);
+  const uint32_t wg0 = (uint32_t)((blockIdx.x * (unsigned)NT + threadIdx.x) >> 5);
+  const uint32_t wstride = gridDim.x * (unsigned)(NT / 32);  // PERSIST: grid-stride over slice pairs
   const int lane = threadIdx.x & 31;
-  const uint32_t kA = 2u * wg, kB = kA + 1u;
   const uint32_t ns = (uint32_t)a.n_slices;
   double dotv = 0.0;
-  if (kA < ns) {
+  for (uint32_t wg = wg0; 2u * wg < ns; wg += wstride) {
+    const uint32_t kA = 2u * wg, kB = kA + 1u;
     const bool hasB = kB < ns;
     const uint32_t n_rows = (uint32_t)a.n_rows;
     const uint32_t sA = kA * 32u + lane, sB = sA + 32u;
@@ -617,6 +642,7 @@ __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const Sp
     }
     flush(sA, oA, accA);
     if (hasB) flush(sB, oB, accB);
+    if (!PERSIST) break;
   }
   finish_dot<DOT, NT>(a, dotv);
 }
@@ -1204,7 +1230,9 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
           if (dual_slices(a.n_slices) && a.narrow && pair_kernel()) {
             const int pn = pair_nt(DOT);
             const unsigned gp = (unsigned)ceil_div(ceil_div(a.n_slices, 2), pn / 32);
-            if (pn == 64) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 64><<<gp, 64, 0, st>>>(a);
+            const unsigned gpp = pair_persist_grid(a.n_slices, DOT);
+            if (gpp) spmv_pair_kernel<CODEC, XT, DOT, 12, true, kBlock, true><<<gpp, kBlock, 0, st>>>(a);
+            else if (pn == 64) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 64><<<gp, 64, 0, st>>>(a);
             else if (pn == 128) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 128><<<gp, 128, 0, st>>>(a);
             else spmv_pair_kernel<CODEC, XT, DOT, 12, true><<<gd, kBlock, 0, st>>>(a);
           } else if (dual_slices(a.n_slices) && pair_wide()) {
@@ -1276,6 +1304,9 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.p_own = nullptr;
   a.partials = nullptr;
   a.skip = nullptr;
+  a.ticket = nullptr;
+  a.scal = nullptr;
+  a.iflags = nullptr;
   a.n_rows = d->n_rows;
   a.n_cols = d->n_cols;
   a.n_slices = ceil_div(d->n_rows, d->c);
@@ -1383,7 +1414,8 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   const int spw = slices_per_warp(ns);
   if (spw == 0) return "spmv_persist_kernel";
   if (spw > 1) return "spmv_multi_kernel";
-  if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel()) return "spmv_pair_kernel<U=12>";
+  if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel())
+    return pair_persist_grid(ns, false) ? "spmv_pair_kernel<U=12, persistent>" : "spmv_pair_kernel<U=12>";
   if (dual_slices(ns) && pair_wide()) return "spmv_pair_kernel<U=8>";
   if (dual_slices(ns)) {
     const int du = dual_chunk((flags & PSELL_SPMV_NARROW) != 0);
@@ -1471,8 +1503,10 @@ int64_t psell_spmv_dot_partials(const psell_desc* d, int32_t flags) {
     const int spw = slices_per_warp(ns);
     if (d->codec != PSELL_FP32EMBED && spw > 1) return ceil_div(ceil_div(ns, spw), kWarps);
     if (d->codec != PSELL_FP32EMBED && spw == 0) return spmv_grid(ns, 32, true);
-    if (d->codec != PSELL_FP32EMBED && dual_slices(ns) && pair_kernel() && (flags & PSELL_SPMV_NARROW))
+    if (d->codec != PSELL_FP32EMBED && dual_slices(ns) && pair_kernel() && (flags & PSELL_SPMV_NARROW)) {
+      if (const unsigned g = pair_persist_grid(ns, true)) return g;
       return ceil_div(ceil_div(ns, 2), pair_nt(true) / 32);
+    }
     if (d->codec != PSELL_FP32EMBED && dual_slices(ns)) return ceil_div(ceil_div(ns, 2), kWarpsPerCta);
     if (d->codec != PSELL_FP32EMBED) return ceil_div(ns * 32, fast_nt());
     return ceil_div(ns * 32, kBlock);
@@ -1502,6 +1536,32 @@ int psell_spmv_dot(const psell_desc* d, const void* pack, const int64_t* offset,
     case PSELL_FP32EMBED: launch_spmv<PSELL_FP32EMBED, float, false, true>(a, st); break;
   }
   PSELL_CHECK_LAUNCH(err, "psell_spmv_dot");
+  return ok(err);
+}
+
+int psell_spmv_dot_alpha(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
+                         const float* x, float* y, const float* p_own, double* partials, double* scal,
+                         int32_t* iflags, unsigned* ticket, int32_t flags, void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  if (!ticket || !scal || !iflags) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null scalar state");
+  a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
+  a.x = x;
+  a.y = y;
+  a.p_own = p_own;
+  a.partials = partials;
+  a.skip = iflags;
+  a.ticket = ticket;
+  a.scal = scal;
+  a.iflags = iflags;
+  cudaStream_t st = as_stream(stream);
+  if (a.n_rows == 0) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "empty operator");
+  switch (d->codec) {
+    case PSELL_FP16: launch_spmv<PSELL_FP16, float, false, true>(a, st); break;
+    case PSELL_E8MY: launch_spmv<PSELL_E8MY, float, false, true>(a, st); break;
+    case PSELL_FP32EMBED: launch_spmv<PSELL_FP32EMBED, float, false, true>(a, st); break;
+  }
+  PSELL_CHECK_LAUNCH(err, "psell_spmv_dot_alpha");
   return ok(err);
 }
 

@@ -173,11 +173,15 @@ class _Dev:
         self.L = _lib
         self.comm = comm
         self.G = 1 if comm is None else comm.world
-        self.partials = torch.zeros(max(int(n_partials), 2 * _lib.RED_BLOCKS), dtype=torch.float64, device="cuda")
+        np_ = max(int(n_partials), 2 * _lib.RED_BLOCKS)
+        self.partials = torch.zeros(np_ + -(-np_ // 32) + 8, dtype=torch.float64, device="cuda")
         self.loc = torch.zeros(8, dtype=torch.float64, device="cuda")
         self.glob = torch.zeros(self.G * 8, dtype=torch.float64, device="cuda")
         self.scal = torch.zeros(32, dtype=torch.float64, device="cuda")
         self.flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+        # last-CTA tickets of the fused epilogues: [0, T) SpMV + alpha, [T, 2T) update + beta
+        self.tstride = 1 + -(-np_ // 32)  # groups of >= 32 CTAs
+        self.ticket = torch.zeros(2 * self.tstride, dtype=torch.int32, device="cuda")
 
     def st(self):
         return self.L.stream_handle()
@@ -253,6 +257,16 @@ class _InnerPCG:
         self.graph = None
         self.graph_in = None
         self.use_graph = use_graph and G == 1
+        self._io = None
+
+    def buffers(self):
+        """Persistent f64 (r, z) the outer loop can hand to solve(): the captured graph
+        is bound to them, so repeated solves replay without re-capture."""
+        if self._io is None:
+            f64 = self.torch.float64
+            self._io = (self.torch.zeros(self.n, dtype=f64, device="cuda"),
+                        self.torch.zeros(self.n, dtype=f64, device="cuda"))
+        return self._io
 
     def _sequence(self, r64, z64):
         d, L, lib = self.d, self.d.L, self.d.lib
@@ -264,6 +278,23 @@ class _InnerPCG:
                              self.p.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
         g, stride = d.gather()
         lib.psell_ipcg_set_rz(d.p(g, 0), d.G, stride, d.p(d.scal), d.p(d.flags), st)
+        if d.G == 1:
+            # one GPU: 3 launches per iteration -- SpMV + p.q + alpha, r/z update + r.z + beta,
+            # x += alpha p with p = z + beta p
+            # (the scalar steps run in the last CTA of the preceding kernel, fixed-order sums)
+            for _ in range(self.m_in):
+                rc = lib.psell_spmv_dot_alpha(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
+                                              self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
+                                              d.p(d.partials), d.p(d.scal), d.p(d.flags), d.p(d.ticket, 0),
+                                              M.spmv_flags(), st, err)
+                L.check(rc, err, M.fmt)
+                lib.psell_ipcg_update_beta(self.n, None, self.r.data_ptr(), self.z.data_ptr(),
+                                           self.p.data_ptr(), self.q.data_ptr(), inv, d.p(d.scal), d.p(d.flags),
+                                           d.p(d.partials), d.p(d.ticket, d.tstride), st)
+                lib.psell_ipcg_direction_x(self.n, self.p.data_ptr(), self.z.data_ptr(), self.x.data_ptr(),
+                                           d.p(d.scal), d.p(d.flags), st)
+            lib.psell_ipcg_end(self.n, self.x.data_ptr(), z64.data_ptr(), st)
+            return
         for _ in range(self.m_in):
             _gather_full(self.comm, self.p, self.p_full)
             rc = lib.psell_spmv_dot(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
@@ -395,7 +426,8 @@ class _Outer:
         self.row0 = getattr(src, "row0", 0)
         b = np.asarray(b, dtype=np.float64)
         self.n = len(b)
-        self.b = torch.as_tensor(b).cuda()
+        from . import _dev
+        self.b = _dev.upload_pinned(b)
         self.d = _Dev(_lib.RED_BLOCKS, comm)
         self.lib = self.d.lib
         f64 = torch.float64
@@ -440,6 +472,11 @@ class _Outer:
             msg = f"true residual {report.final_true_relres:.3e} exceeds 10x tolerance"
             report.reason = f"{report.reason}; {msg}" if report.reason else msg
         return report
+
+
+def _dev_mod():
+    from . import _dev
+    return _dev
 
 
 def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
@@ -502,7 +539,7 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
     torch.cuda.synchronize()
     report = SolveReport(converged, it, 0, history, 0.0, time.perf_counter() - t0, reason)
     report = o.audit(report, x, bnorm, cfg.tol)
-    report.x = x.cpu().numpy()
+    report.x = _dev_mod().download_pinned(x)
     return report
 
 
@@ -528,9 +565,13 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
     inv = None
     if _inner is None and inner_preconditioner is None and cfg.preconditioner == "jacobi":
         inv = _jacobi_inv(backend, np.float64)
-    r = o.b.clone()
+    if _inner is not None and hasattr(_inner, "buffers"):
+        r, z = _inner.buffers()  # the inner solver's graph is bound to these
+        r.copy_(o.b)
+    else:
+        r, z = o.b.clone(), o.vec()
     history = [d.norm(r) / bnorm]
-    z, p, q, r_prev = o.vec(), o.vec(), o.vec(), o.vec()
+    p, q, r_prev = o.vec(), o.vec(), o.vec()
     converged, reason, it, first = False, None, 0, True
     inner_total = 0
     while it < cfg.max_outer:
@@ -578,7 +619,7 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
     torch.cuda.synchronize()
     report = SolveReport(converged, it, inner_total, history, 0.0, time.perf_counter() - t0, reason)
     report = o.audit(report, x, bnorm, cfg.tol)
-    report.x = x.cpu().numpy()
+    report.x = _dev_mod().download_pinned(x)
     return report
 
 
@@ -602,7 +643,13 @@ def iocg(A, b, cfg: SolveConfig = None, *, backend: SpmvBackend = None, comm=Non
     dtype = _PRECISIONS[cfg.inner_precision]
     inv = _jacobi_inv(backend, dtype) if cfg.preconditioner == "jacobi" else None
     if dtype == np.float32 and backend.is_packsell:
-        inner = _InnerPCG(backend, cfg.m_in, inv, comm=comm, use_graph=use_graph)
+        # one inner solver (vectors + captured CUDA graph) per operator and setting,
+        # reused by every solve on this backend
+        key = (cfg.m_in, cfg.preconditioner, id(comm), use_graph)
+        cache = backend.__dict__.setdefault("_inner_cache", {})
+        inner = cache.get(key)
+        if inner is None:
+            inner = cache[key] = _InnerPCG(backend, cfg.m_in, inv, comm=comm, use_graph=use_graph)
     else:
         if comm is not None and comm.world > 1:
             raise NotImplementedError("distributed iocg needs a PackSELL inner backend in real32")
