@@ -325,7 +325,9 @@ def run_pcg(args, world, rank, comm, peak):
                      "roofline_s": agg(p64_bytes) / (peak * world * 1e9)},
         "speedup_iocg_vs_fp64_pcg": t_64 / t_io,
         "build_s": t_build,
-        "collectives": "none" if world == 1 else "NCCL all-gather of p (f32 inner, f64 outer) + all-gather of FP64 dot partials",
+        "collectives": "none" if world == 1 else (
+            "NCCL point-to-point halo exchange of p (f32 inner, f64 outer; K7 pack/unpack, "
+            "dist.Halo) + all-gather of the FP64 per-rank dot sums (rank-ordered)"),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O

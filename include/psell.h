@@ -339,6 +339,15 @@ PSELL_API int psell_backward_error(int64_t n_rows, int64_t n_cols, const int64_t
                                    int32_t x_dtype, const void* y, int32_t y_dtype, double* out,
                                    void* stream, psell_error* err);
 
+/* ---- K7 halo exchange: dst[i] = src[idx[i]] (pack the entries
+ * a peer rank needs from the local slab) and dst[idx[i]] = src[i] (scatter
+ * received entries to their global positions); elem_bytes 4 or 8.  Index
+ * lists come from dist.Halo (built once per operator). */
+PSELL_API int psell_halo_pack(int64_t n, const void* src, const int32_t* idx, void* dst, int32_t elem_bytes,
+                              void* stream);
+PSELL_API int psell_halo_unpack(int64_t n, const void* src, const int64_t* idx, void* dst, int32_t elem_bytes,
+                                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

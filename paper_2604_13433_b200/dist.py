@@ -12,7 +12,10 @@ needs no collective (x replicated).  The PCG needs exactly two, over NCCL
 * all-gather of the per-rank FP64 local dot sums, summed in rank order on the
   device (deterministic regardless of the collective's reduction tree).
 
-`Comm` wraps a process group (NCCL on GPUs, gloo in the CPU tests).
+`Comm` wraps a process group (NCCL on GPUs, gloo in the CPU tests).  `Halo`
+ replaces the direction all-gather by a neighbour exchange
+of just the columns a rank's rows read: for banded operators (the stencils)
+that is two thin boundary layers instead of the whole vector.
 """
 
 from __future__ import annotations
@@ -68,6 +71,104 @@ class Comm:
         self.dist.barrier(group=self.group)
 
 
+class Halo:
+    """Point-to-point halo plan of one row-partitioned operator (built once, collectively).
+
+    `needed` are the sorted unique global columns this rank's rows read
+    (the CSR slab's col_idx).  Columns outside the own slab [row0, row1) are
+    requested from their owners; `exchange(full, local)` then packs what each
+    peer needs from `local` (K7 pack), moves it with NCCL send/recv over
+    NVLink, and scatters the received entries into `full` (K7 unpack) — the
+    entries of `full` the SpMV reads are then exactly those of the all-gathered
+    vector.  When the halo covers more than `max_frac` of the remote part of
+    the vector (irregular matrices) the plan sets `use_allgather` and the
+    solvers keep the all-gather.
+    """
+
+    def __init__(self, comm: "Comm", row0: int, row1: int, needed, max_frac: float = 0.5):
+        self.comm = comm
+        self.row0, self.row1 = int(row0), int(row1)
+        needed = np.unique(np.asarray(needed, dtype=np.int64))
+        slabs = [None] * comm.world
+        comm.dist.all_gather_object(slabs, (self.row0, self.row1), group=comm.group)
+        self.slabs = [tuple(map(int, s)) for s in slabs]
+        ends = np.array([b for _, b in self.slabs], dtype=np.int64)
+        remote = needed[(needed < self.row0) | (needed >= self.row1)]
+        owner = np.searchsorted(ends, remote, side="right")
+        self.recv_lists = [remote[owner == s] for s in range(comm.world)]
+        wanted = [None] * comm.world  # wanted[s][r]: columns rank s needs from rank r
+        comm.dist.all_gather_object(wanted, self.recv_lists, group=comm.group)
+        self.send_lists = [np.asarray(wanted[s][comm.rank], dtype=np.int64) for s in range(comm.world)]
+        self.recv_counts = [len(v) for v in self.recv_lists]
+        self.send_counts = [len(v) for v in self.send_lists]
+        n_glob = max(b for _, b in self.slabs)
+        n_remote = n_glob - (self.row1 - self.row0)
+        tot = [0] * comm.world
+        comm.dist.all_gather_object(tot, int(sum(self.recv_counts)), group=comm.group)
+        self.use_allgather = max(tot) > max_frac * max(n_remote, 1)
+        self.send_idx = np.concatenate(self.send_lists + [np.zeros(0, np.int64)]) - self.row0
+        self.recv_idx = np.concatenate(self.recv_lists + [np.zeros(0, np.int64)])
+        self._dev = None
+
+    @property
+    def volume(self) -> int:
+        """Entries this rank receives per exchange (the all-gather would deliver n_glob - n_own)."""
+        return int(sum(self.recv_counts))
+
+    def _device_plan(self):
+        if self._dev is None:
+            import torch
+            self._dev = (torch.as_tensor(self.send_idx.astype(np.int32)).cuda(),
+                         torch.as_tensor(self.recv_idx).cuda(), {})
+        return self._dev
+
+    def p2p(self, send, recv):
+        """Move send[slice for peer s] to peer s and fill recv[slice from peer s] (stream-ordered on NCCL)."""
+        dist, grp = self.comm.dist, self.comm.group
+        staged = send.is_cuda and not self.comm.nccl  # gloo moves host tensors
+        s_buf = send.cpu() if staged else send
+        r_buf = recv.cpu() if staged else recv
+        ops, so, ro = [], 0, 0
+        for peer in range(self.comm.world):
+            ns, nr = self.send_counts[peer], self.recv_counts[peer]
+            if nr:
+                ops.append(dist.P2POp(dist.irecv, r_buf[ro:ro + nr], peer, grp))
+            if ns:
+                ops.append(dist.P2POp(dist.isend, s_buf[so:so + ns], peer, grp))
+            so += ns
+            ro += nr
+        if ops:
+            if self.comm.nccl:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+            else:
+                reqs = [op.op(op.tensor, op.peer, op.group) for op in ops]
+                for req in reqs:
+                    req.wait()
+        if staged:
+            recv.copy_(r_buf)
+
+    def exchange(self, full, local):
+        """full[recv_idx] <- the owners' entries; `local` is this rank's slab (any 4/8-byte dtype)."""
+        import torch
+        from . import _lib
+        lib = _lib.lib()
+        send_idx, recv_idx, bufs = self._device_plan()
+        key = full.dtype
+        if key not in bufs:
+            bufs[key] = (torch.empty(len(self.send_idx), dtype=full.dtype, device=full.device),
+                         torch.empty(len(self.recv_idx), dtype=full.dtype, device=full.device))
+        send, recv = bufs[key]
+        st = _lib.stream_handle()
+        es = full.element_size()
+        if lib.psell_halo_pack(len(self.send_idx), local.data_ptr(), send_idx.data_ptr(), send.data_ptr(), es, st):
+            raise _lib.LibpsellError("psell_halo_pack failed")
+        self.p2p(send, recv)
+        if lib.psell_halo_unpack(len(self.recv_idx), recv.data_ptr(), recv_idx.data_ptr(), full.data_ptr(), es, st):
+            raise _lib.LibpsellError("psell_halo_unpack failed")
+        return full
+
+
 def equal_row_slabs(n: int, world: int, sigma: int) -> List[Tuple[int, int]]:
     """sigma-aligned contiguous row slabs, as equal as the sigma granularity allows.
 
@@ -120,4 +221,4 @@ def rank_order_sum(parts: np.ndarray) -> float:
     return s
 
 
-__all__ = ["Comm", "equal_row_slabs", "check_equal", "word_balanced_slabs", "rank_order_sum"]
+__all__ = ["Comm", "Halo", "equal_row_slabs", "check_equal", "word_balanced_slabs", "rank_order_sum"]

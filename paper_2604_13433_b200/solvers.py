@@ -209,12 +209,32 @@ class _Dev:
         return float(np.sqrt(float(self.scal[slot].item())))
 
 
-def _gather_full(comm, local, full):
-    """full <- concatenation of every rank's equal slab (in place when local aliases full)."""
+def _gather_full(comm, local, full, halo=None):
+    """Entries of `full` the slab's rows read <- their owners' values.
+
+    With a halo plan (dist.Halo): point-to-point exchange of the
+    boundary columns only; otherwise the in-place all-gather of equal slabs."""
     if comm is None or comm.world == 1:
         return local
+    if halo is not None and not halo.use_allgather:
+        return halo.exchange(full, local)
     comm.all_gather_vec(full, local)
     return full
+
+
+def _halo_for(comm, src):
+    """The operator's halo plan (cached on its CSR slab); None on one GPU or with PSELL_HALO=0."""
+    import os
+    if comm is None or comm.world == 1 or os.environ.get("PSELL_HALO", "1") == "0":
+        return None
+    D = src.to_device()
+    cache = D.__dict__.setdefault("_halo", {})
+    if id(comm) not in cache:
+        import torch
+        from .dist import Halo
+        needed = torch.unique(D.col_idx).cpu().numpy() if D.nnz else np.zeros(0, np.int64)
+        cache[id(comm)] = Halo(comm, D.row0, D.row0 + D.n_rows, needed)
+    return cache[id(comm)]
 
 
 # ----------------------------------------------------------------------------
@@ -234,6 +254,7 @@ class _InnerPCG:
         M = backend.matrix
         if not isinstance(M, PackSellMatrix):
             raise TypeError("_InnerPCG drives a PackSELL backend")
+        self.halo = _halo_for(comm, backend.source)
         self.M = M
         self.n = M.n_rows
         self.row0 = M.row0
@@ -296,7 +317,7 @@ class _InnerPCG:
             lib.psell_ipcg_end(self.n, self.x.data_ptr(), z64.data_ptr(), st)
             return
         for _ in range(self.m_in):
-            _gather_full(self.comm, self.p, self.p_full)
+            _gather_full(self.comm, self.p, self.p_full, self.halo)
             rc = lib.psell_spmv_dot(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
                                     self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
                                     d.p(d.partials), d.p(d.flags), M.spmv_flags(), st, err)
@@ -424,6 +445,7 @@ class _Outer:
         self.G = 1 if comm is None else comm.world
         src = backend.matrix if not backend.is_packsell else backend.source
         self.row0 = getattr(src, "row0", 0)
+        self.halo = _halo_for(comm, src)
         b = np.asarray(b, dtype=np.float64)
         self.n = len(b)
         from . import _dev
@@ -446,7 +468,7 @@ class _Outer:
             out.copy_(self.backend.apply(v))
             return out
         self.slab_of_full().copy_(v)
-        _gather_full(self.comm, self.slab_of_full(), self.full)
+        _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
         out.copy_(self.backend.apply(self.full))
         return out
 
@@ -462,7 +484,7 @@ class _Outer:
             ax.copy_(csr_spmv(src, x, np.float64))
         else:
             self.slab_of_full().copy_(x)
-            _gather_full(self.comm, self.slab_of_full(), self.full)
+            _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
             ax.copy_(csr_spmv(src, self.full, np.float64))
         self.lib.psell_resid(self.n, self.b.data_ptr(), ax.data_ptr(), d.p(d.partials), d.p(d.loc, 6), d.st())
         d.reduce(6, 1, 14)

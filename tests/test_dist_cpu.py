@@ -100,3 +100,51 @@ def test_stencil_rows_match_full():
     S = stencil.stencil_rows("poisson3d", 7, 50, 200)
     assert np.array_equal(S.col_idx, A.col_idx[A.row_ptr[50]:A.row_ptr[200]])
     assert np.array_equal(S.row_ptr, A.row_ptr[50:201] - A.row_ptr[50])
+
+
+def _halo_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = D.Comm()
+        nx = 8
+        n = nx ** 3
+        slabs = D.equal_row_slabs(n, world, 32)
+        r0, r1 = slabs[rank]
+        A = stencil.poisson3d(nx)
+        cols = A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]]
+        h = D.Halo(comm, r0, r1, cols)
+        # the exchange on host tensors (the device path runs K7 pack/unpack around the same p2p)
+        full_ref = torch.arange(n, dtype=torch.float64) * 0.5 + 1.0
+        full = torch.zeros(n, dtype=torch.float64)
+        full[r0:r1] = full_ref[r0:r1]
+        send = full[r0:r1][torch.as_tensor(h.send_idx)]
+        recv = torch.zeros(h.volume, dtype=torch.float64)
+        h.p2p(send, recv)
+        full[torch.as_tensor(h.recv_idx)] = recv
+        need = np.unique(cols.astype(np.int64))
+        ok = bool(torch.equal(full[torch.as_tensor(need)], full_ref[torch.as_tensor(need)]))
+        # an irregular operator (every row reads everything) falls back to the all-gather
+        g = D.Halo(comm, r0, r1, np.arange(n))
+        q.put((rank, ok, h.volume, h.use_allgather, g.use_allgather, list(h.recv_counts), list(h.send_counts)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_halo_exchange():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for rank, ok, vol, h_ag, g_ag, rc, sc in res:
+        assert ok
+        assert vol == 8 * 8  # one boundary plane of the 7-point stencil from the neighbour slab
+        assert not h_ag and g_ag
+    # what rank 0 receives from rank 1 is what rank 1 sends to rank 0, and vice versa
+    assert res[0][5][1] == res[1][6][0] and res[1][5][0] == res[0][6][1]

@@ -1,7 +1,8 @@
 """Distributed PCG path with real ranks on one GPU (gloo transport through host memory;
-the NCCL run differs only in the transport).  Rank slabs + NCCL-style all-gathers
-must reproduce the single-GPU solve: same convergence, outer iterations within 1,
-x within 1e-6 relative (only the association of the FP64 dot sums differs)."""
+the NCCL run differs only in the transport).  Rank slabs + halo exchange (or the
+all-gather) must reproduce the single-GPU solve: same convergence, outer
+iterations within 1, x within 1e-6 relative (only the association of the FP64 dot
+sums differs); halo and all-gather solves are bitwise identical."""
 
 import os
 import socket
@@ -40,8 +41,14 @@ def _rank(rank, world, port, nx, q):
         rep = S.iocg(A, b[r0:r1], cfg, comm=comm)
         pc = S.pcg(P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1), b[r0:r1],
                    S.SolveConfig(tol=1e-9, max_outer=2000), comm=comm)
+        halo = S._halo_for(comm, A)
+        # the same solve with the full all-gather: the SpMVs read identical values -> identical x
+        os.environ["PSELL_HALO"] = "0"
+        A2 = P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1)
+        rep_ag = S.iocg(A2, b[r0:r1], cfg, comm=comm)
         q.put((rank, r0, r1, rep.converged, rep.outer_iters, rep.total_inner_iters, rep.final_true_relres,
-               rep.x, pc.converged, pc.outer_iters, pc.x))
+               rep.x, pc.converged, pc.outer_iters, pc.x,
+               None if halo is None else (halo.volume, halo.use_allgather), rep_ag.x))
     except Exception as e:  # noqa: BLE001
         q.put((rank, repr(e)))
         raise
@@ -73,7 +80,9 @@ def test_distributed_iocg_matches_single_gpu(world):
     assert all(len(r) > 2 for r in res), res
     x = np.zeros(n)
     xp = np.zeros(n)
-    for (rank, r0, r1, conv, outer, inner, relres, xs, pconv, pouter, pxs) in res:
+    for (rank, r0, r1, conv, outer, inner, relres, xs, pconv, pouter, pxs, halo, xs_ag) in res:
+        assert halo is not None and halo == (nx * nx, False)  # one boundary plane, point-to-point
+        assert np.array_equal(xs, xs_ag)
         assert conv and abs(outer - ref.outer_iters) <= 1
         assert inner == cfg.m_in * outer
         assert relres < 1e-9
