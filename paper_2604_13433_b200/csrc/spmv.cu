@@ -472,7 +472,10 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
     const bool hasB = kB < a.n_slices;
     const long long oA = a.offset[kA], oB = a.offset[kA + 1];
     const long long oE = hasB ? a.offset[kB + 1] : oB;
-    const int wA = (int)((oB - oA) >> 5), wB = (int)((oE - oB) >> 5);
+    // long slices (power-law rows) belong to the segment kernels when segmentation is on
+    const bool skipA = a.seg_len > 0 && (int)((oB - oA) >> 5) > a.seg_len;
+    const bool skipB = a.seg_len > 0 && (int)((oE - oB) >> 5) > a.seg_len;
+    const int wA = skipA ? 0 : (int)((oB - oA) >> 5), wB = skipB ? 0 : (int)((oE - oB) >> 5);
     const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + oA + lane;
     const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + oB + lane;
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
@@ -519,8 +522,8 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
         if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
       }
     };
-    flush(kA, accA);
-    if (hasB) flush(kB, accB);
+    if (!skipA) flush(kA, accA);
+    if (hasB && !skipB) flush(kB, accB);
   }
   finish_dot<DOT>(a, dotv);
 }
@@ -565,7 +568,9 @@ __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const Sp
     }
     const long long o0 = a.offset[kA], o1 = a.offset[kA + 1];
     const long long o2 = hasB ? a.offset[kA + 2] : o1;
-    const int wA = (int)((o1 - o0) >> 5), wB = (int)((o2 - o1) >> 5);
+    const bool skipA = a.seg_len > 0 && (int)((o1 - o0) >> 5) > a.seg_len;  // segment kernels own it
+    const bool skipB = a.seg_len > 0 && (int)((o2 - o1) >> 5) > a.seg_len;
+    const int wA = skipA ? 0 : (int)((o1 - o0) >> 5), wB = skipB ? 0 : (int)((o2 - o1) >> 5);
     const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + o0 + lane;
     const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + o1 + lane;
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
@@ -640,8 +645,8 @@ __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const Sp
       oA = out_of(kA, sA);
       oB = out_of(kB, sB);
     }
-    flush(sA, oA, accA);
-    if (hasB) flush(sB, oB, accB);
+    if (!skipA) flush(sA, oA, accA);
+    if (hasB && !skipB) flush(sB, oB, accB);
     if (!PERSIST) break;
   }
   finish_dot<DOT, NT>(a, dotv);
