@@ -41,6 +41,10 @@ struct SpmvArgs {
   // long-slice segmentation (0 = off): slices wider than seg_len steps run as
   // segments (see spmv_seg_kernel)
   int seg_len;
+  // bulk L2 prefetch of the slice pair's words at warp start (dual kernel: 27-point
+  // 359 -> 325 us).  PSELL_L2PF=0 disables, =2 also prefetches the next pair in
+  // the persistent pair kernel (measured slower: 166 -> 187 us on 7-point).
+  int l2pf;
   const int32_t* seg_slice;   // [n_seg] slice of each segment
   const int32_t* seg_q0;      // [n_seg] first step of each segment
   uint32_t* seg_c2;           // [n_seg][32] cursor checkpoints (2 * column)
@@ -60,6 +64,14 @@ static inline void magic_div(uint32_t d, uint32_t& m, uint32_t& l) {
 
 __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t l) {
   return (__umulhi(n, m) + n) >> l;
+}
+
+// One TMA-engine L2 prefetch of a contiguous byte range (16-B aligned, multiple
+// of 16 B): the slice pair's whole word stream is requested from HBM up front,
+// without holding registers, so the chunked register loads that follow hit L2.
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+               : "memory");
 }
 
 template <int CODEC> struct WordOf { using T = uint32_t; };
@@ -478,6 +490,11 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
     const int wA = skipA ? 0 : (int)((oB - oA) >> 5), wB = skipB ? 0 : (int)((oE - oB) >> 5);
     const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + oA + lane;
     const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + oB + lane;
+    if (a.l2pf && lane == 0 && oE > oA) {
+      const uint64_t bytes = (uint64_t)(oE - oA) * 4u;
+      l2_prefetch_bulk(static_cast<const uint32_t*>(a.pack) + oA, (uint32_t)(bytes < (1u << 20) ? bytes : (1u << 20)),
+                       policy_evict_first());
+    }
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
     const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
     const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
@@ -573,6 +590,18 @@ __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const Sp
     const int wA = skipA ? 0 : (int)((o1 - o0) >> 5), wB = skipB ? 0 : (int)((o2 - o1) >> 5);
     const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + o0 + lane;
     const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + o1 + lane;
+    if (PERSIST && a.l2pf >= 2 && lane == 0) {  // next pair of the walk (A/B only: measured slower)
+      const uint32_t kn = kA + 2u * wstride;
+      if (kn < ns) {
+        const long long n0 = a.offset[kn];
+        const long long n2 = a.offset[kn + 2u < ns ? kn + 2u : ns];
+        if (n2 > n0) {
+          const uint64_t bytes = (uint64_t)(n2 - n0) * 4u;
+          l2_prefetch_bulk(static_cast<const uint32_t*>(a.pack) + n0,
+                           (uint32_t)(bytes < (1u << 20) ? bytes : (1u << 20)), policy_evict_first());
+        }
+      }
+    }
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
     const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
     const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
@@ -1333,6 +1362,8 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.spw = d->c == 32 ? slices_per_warp(a.n_slices) : 1;
   magic_div((uint32_t)(a.se > 0 ? a.se : 1), a.se_m, a.se_l);
   magic_div((uint32_t)(a.sigma > 0 ? a.sigma : 1), a.sig_m, a.sig_l);
+  a.l2pf = 1;
+  if (const char* e = getenv("PSELL_L2PF")) a.l2pf = atoi(e);
   return PSELL_OK;
 }
 
