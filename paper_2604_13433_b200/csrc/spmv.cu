@@ -590,6 +590,11 @@ __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const Sp
     const int wA = skipA ? 0 : (int)((o1 - o0) >> 5), wB = skipB ? 0 : (int)((o2 - o1) >> 5);
     const uint32_t* pA = static_cast<const uint32_t*>(a.pack) + o0 + lane;
     const uint32_t* pB = static_cast<const uint32_t*>(a.pack) + o1 + lane;
+    if (!PERSIST && a.l2pf && lane == 0 && o2 > o0) {  // this pair's words, one TMA request
+      const uint64_t bytes = (uint64_t)(o2 - o0) * 4u;
+      l2_prefetch_bulk(static_cast<const uint32_t*>(a.pack) + o0, (uint32_t)(bytes < (1u << 20) ? bytes : (1u << 20)),
+                       policy_evict_first());
+    }
     if (PERSIST && a.l2pf >= 2 && lane == 0) {  // next pair of the walk (A/B only: measured slower)
       const uint32_t kn = kA + 2u * wstride;
       if (kn < ns) {

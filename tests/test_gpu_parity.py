@@ -288,3 +288,34 @@ def test_spmv_stream_equals_per_call(rng):
     ys = P.packsell_spmv_stream(M, [x.numpy() for x in xs], ref_order=True)
     for x, y in zip(xs, ys):
         assert np.array_equal(_bits(y.numpy()), _bits(P.packsell_spmv(M, x.numpy(), ref_order=True)))
+
+
+@pytest.mark.parametrize("sigma,nnz_per_row", [(96, 7), (160, 7), (224, 27), (32 * 1023, 5), (96, 27)])
+@pytest.mark.parametrize("mode", ["implicit", "explicit", "none"])
+def test_production_kernels_non_pow2_sigma(rng, sigma, nnz_per_row, mode):
+    """Dual / pair / persistent-pair kernels with sigma not a power of two (multiply-high division of
+    base offsets and output rows): FMA SpMV within the bound of the REF_ORDER result, which is bitwise
+    the oracle's; build bit-exact."""
+    n = 4096 + 96 * 7
+    rows = np.repeat(np.arange(n), nnz_per_row)
+    cols = np.clip(rows + rng.integers(-600, 600, rows.size), 0, n - 1)
+    order = np.lexsort((cols, rows))
+    r, c = rows[order], cols[order]
+    keep = np.ones(r.size, bool)
+    keep[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+    r, c = r[keep], c[keep]
+    v = rng.uniform(0.01, 1, r.size) * rng.choice([-1.0, 1.0], r.size)
+    rp = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n))]).astype(np.int64)
+    A = P.CsrMatrix(n, n, rp, c.astype(np.int32), v)
+    for pre, dt in (("fp16", np.float16), ("e8m14", np.float32)):
+        M = P.build_packsell(A, 32, sigma, P.parse_format(pre), mode)
+        OM = O.build(rp, c.astype(np.int32), v, n, 32, sigma, O.preset(pre), mode)
+        assert np.array_equal(M.pack, OM.pack) and np.array_equal(M.offset, OM.offset)
+        x = rng.uniform(-1, 1, n).astype(dt)
+        yr = P.packsell_spmv(M, x.astype(np.float32), ref_order=True)
+        assert np.array_equal(_bits(yr), _bits(O.spmv(OM, x.astype(np.float32))))
+        yf = P.packsell_spmv(M, x).astype(np.float64)
+        lmax = int(np.max(np.diff(M.offset) // 32))
+        anorm = np.bincount(np.repeat(np.arange(n), np.diff(rp)), np.abs(P.quantize(P.parse_format(pre), v))).max()
+        err = np.abs(yf - yr.astype(np.float64)).max() / (anorm * np.abs(x.astype(np.float64)).max())
+        assert err <= 2 * lmax * 2.0 ** -24 + (2.0 ** -11 if dt == np.float16 else 0.0), (pre, err)

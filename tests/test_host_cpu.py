@@ -117,3 +117,18 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         P.encode_values(P.PackFormat(), [1.0])
+
+
+def test_multiply_high_division_identity():
+    """Host mirror of magic_div / fast_div (csrc/spmv.cu): n / d == (umulhi(n, m) + n) >> l for n < 2^31."""
+    rng = np.random.default_rng(5)
+    for d in list(range(1, 300)) + [32 * k for k in range(1, 2048, 7)] + [65535, 65536]:
+        l = 0
+        while (1 << l) < d:
+            l += 1
+        m = ((1 << 32) * ((1 << l) - d)) // d + 1
+        assert m < (1 << 32)
+        ns = np.concatenate([np.arange(0, 4096), rng.integers(0, 2 ** 31, 2000),
+                             [2 ** 31 - 1, 2 ** 31 - 2, d - 1, d, d + 1, 2 ** 31 - 1 - (2 ** 31 - 1) % d]])
+        for n in ns.tolist():
+            assert (((n * m) >> 32) + n) >> l == n // d, (d, n)
