@@ -13,7 +13,8 @@ import os
 from ctypes import POINTER, c_char, c_double, c_int32, c_int64, c_size_t, c_uint8, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsell.so")
+# PSELL_LIB selects an alternative in-tree build for A/B runs (csrc/Makefile `alt` target)
+LIB_PATH = os.path.join(_HERE, os.environ.get("PSELL_LIB", "libpsell.so"))
 
 PSELL_OK, PSELL_EVALUE, PSELL_ECODEC, PSELL_ECUDA, PSELL_EARG = 0, 1, 2, 3, 4
 KIND_NONE, KIND_FIRST_GAP, KIND_GAP_RANGE, KIND_NONFINITE, KIND_OVERFLOW, KIND_PARAM, KIND_CUDA = range(7)

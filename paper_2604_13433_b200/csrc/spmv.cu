@@ -315,6 +315,32 @@ __device__ __forceinline__ const char* xbyte(const XT* x, uint32_t c2) {
   return reinterpret_cast<const char*>(x) + (size_t)c2 * (sizeof(XT) / 2);
 }
 
+// PSELL_GATHER_REAL_ONLY (build-time A/B, `make alt EXTRA=-DPSELL_GATHER_REAL_ONLY=1`):
+// predicate the x gather on the flag too, so dummy and padding words issue no
+// load.  Measured: power-law (config 4) 397 -> 367 us, but the stencils lose
+// 10-15 % (the predicated asm loads schedule worse), so it is off by default.
+#ifndef PSELL_GATHER_REAL_ONLY
+#define PSELL_GATHER_REAL_ONLY 0
+#endif
+__device__ __forceinline__ unsigned short gather_u16(const void* p, uint32_t f) {
+  unsigned short v;
+  if (PSELL_GATHER_REAL_ONLY)
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n mov.b16 %0, 0;\n @p ld.global.nc.u16 %0, [%2];\n}"
+                 : "=h"(v) : "r"(f), "l"(p));
+  else
+    v = __ldg(reinterpret_cast<const unsigned short*>(p));
+  return v;
+}
+__device__ __forceinline__ float gather_f32(const void* p, uint32_t f) {
+  float v;
+  if (PSELL_GATHER_REAL_ONLY)
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n mov.b32 %0, 0;\n @p ld.global.nc.f32 %0, [%2];\n}"
+                 : "=f"(v) : "r"(f), "l"(p));
+  else
+    v = __ldg(reinterpret_cast<const float*>(p));
+  return v;
+}
+
 template <int CODEC, typename XT> struct FastStep;
 
 template <> struct FastStep<PSELL_FP16, __half> {
@@ -322,7 +348,7 @@ template <> struct FastStep<PSELL_FP16, __half> {
   __device__ static void run(uint32_t w, uint32_t& c2, const __half* x, float& acc, uint32_t, uint32_t) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? 0xFFFEu : 0xFFFFFFFEu);
-    const unsigned short xb = __ldg(reinterpret_cast<const unsigned short*>(xbyte(x, c2)));
+    const unsigned short xb = gather_u16(xbyte(x, c2), f);
     asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
         " @p fma.rn.f32.f16 %0, hi, %3, %0;\n}" : "+f"(acc) : "r"(f), "r"(w), "h"(xb));
   }
@@ -332,7 +358,7 @@ template <> struct FastStep<PSELL_FP16, float> {
   __device__ static void run(uint32_t w, uint32_t& c2, const float* x, float& acc, uint32_t, uint32_t) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? 0xFFFEu : 0xFFFFFFFEu);
-    const float xv = __ldg(reinterpret_cast<const float*>(xbyte(x, c2)));
+    const float xv = gather_f32(xbyte(x, c2), f);
     asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n .reg .f32 v;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
         " cvt.f32.f16 v, hi;\n @p fma.rn.f32 %0, v, %3, %0;\n}" : "+f"(acc) : "r"(f), "r"(w), "f"(xv));
   }
@@ -344,7 +370,7 @@ template <> struct FastStep<PSELL_E8MY, float> {
                              uint32_t vmask) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? m_real : 0xFFFFFFFEu);
-    const float xv = __ldg(reinterpret_cast<const float*>(xbyte(x, c2)));
+    const float xv = gather_f32(xbyte(x, c2), f);
     const float v = __uint_as_float(w & vmask);
     asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
         : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
@@ -356,7 +382,7 @@ template <> struct FastStep<PSELL_E8MY, __half> {
                              uint32_t vmask) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? m_real : 0xFFFFFFFEu);
-    const float xv = __half2float(__ldg(reinterpret_cast<const __half*>(xbyte(x, c2))));
+    const float xv = __half2float(__ushort_as_half(gather_u16(xbyte(x, c2), f)));
     const float v = __uint_as_float(w & vmask);
     asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
         : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
