@@ -502,6 +502,19 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     ms_e2e = allreduce((time.perf_counter() - w0) / k_e2e * 1e3, dist.ReduceOp.MAX if world > 1 else None)
     e2e_value = bytes_all / (ms_e2e * 1e-3) / 1e9
+    # the e2e bound: pinned H2D of x and D2H of y on two copy engines, no compute
+    s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
+    xd_b, yd_b = torch.empty_like(x), torch.empty_like(y)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for _ in range(k_e2e):
+        with torch.cuda.stream(s_a):
+            xd_b.copy_(xh, non_blocking=True)
+        with torch.cuda.stream(s_b):
+            yh.copy_(yd_b, non_blocking=True)
+    torch.cuda.synchronize()
+    ms_pcie = (time.perf_counter() - w0) / k_e2e * 1e3
+    del xd_b, yd_b
 
     peak, peak_kind = measured_peak()
     achieved = bytes_local / (ms_local * 1e-3) / 1e9
@@ -553,6 +566,8 @@ def run_ours(args, cfg):
                     "d2h_bytes_per_step": d2h_b,
                     "api": "paper_2604_13433_b200.packsell_spmv_stream(M, [x_pinned]*K, [y_pinned]*K) "
                            "(copy-in / compute / copy-out streams overlapped across steps)",
+                    "pcie_bound": {"ms_per_step": ms_pcie, "frac": ms_pcie / ms_e2e,
+                                   "what": "x H2D || y D2H from / to pinned host memory alone (no SpMV)"},
                     "sync_per_call": {"value": bytes_all / (ms_sync * 1e-3) / 1e9, "ms_per_step": ms_sync,
                                       "api": "packsell_spmv(M, x_pinned_cpu, out=y_pinned_cpu), one blocking call per step"}},
             "gpu_launches": args.steps * launches_per_step,
