@@ -36,7 +36,6 @@ struct SpmvArgs {
   int c, se, sigma, mode, d, perm_bytes;
   int variant;  // 0: register-pipelined kernels (default), 2: persistent TMA stream
   int narrow;   // mean slice width <= 12 steps (PSELL_SPMV_NARROW)
-  int spw;      // slices per warp of the multi-slice kernel (1: warp-per-slice kernel)
   int codec;
   // long-slice segmentation (0 = off): slices wider than seg_len steps run as
   // segments (see spmv_seg_kernel)
@@ -197,11 +196,11 @@ static bool dual_slices(long long n_slices) {
   return n_slices >= 2;  // measured faster than one slice per warp on configs 2, 3, 5
 }
 
-// steps per chunk of the dual-slice kernel (PSELL_DUAL_U overrides: 8 | 12 | 16)
+// steps per chunk of the dual-slice kernel (PSELL_DUAL_U overrides: 8 | 12)
 static int dual_chunk(bool narrow) {
   if (const char* e = getenv("PSELL_DUAL_U")) {
     const int v = atoi(e);
-    if (v == 8 || v == 12 || v == 16) return v;
+    if (v == 8 || v == 12) return v;
   }
   return narrow ? 12 : 8;  // 12 covers a whole 7-point slice in one chunk (sweep: +14 %)
 }
@@ -818,223 +817,6 @@ __global__ void __launch_bounds__(kBlock) seg_combine_kernel(const SpmvArgs a, l
   }
 }
 
-// ---- multi-slice register pipeline (C == 32): warp w owns the S consecutive
-// slices [w*S, (w+1)*S) — one contiguous range of 128-byte steps in `pack` —
-// and streams it in U-step chunks, double buffered in registers, straight
-// across slice boundaries (detected per step: flush y, reset the cursor).
-// Consecutive warps own consecutive ranges, so resident warps still sweep a
-// dense window of `pack`.  S amortises the per-slice prologue and pipeline
-// fill over narrow slices (7-point rows: ~9 steps per slice).
-template <int CODEC, typename XT, bool DOT, int U>
-__global__ void __launch_bounds__(kBlock, 6) spmv_multi_kernel(const SpmvArgs a) {
-  using S = FastStep<CODEC, XT>;
-  if constexpr (DOT) {
-    if (a.skip && *a.skip) return;
-  }
-  const int lane = threadIdx.x & 31;
-  const long long wg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const long long k0 = wg * a.spw;
-  double dotv = 0.0;
-  if (k0 < a.n_slices) {
-    // 32-bit state: steps and slices of one warp's range, rows < 2^31
-    const int nk = (int)(min(k0 + (long long)a.spw, a.n_slices) - k0);
-    const int64_t* off = a.offset + k0;
-    const long long T0 = off[0];
-    const int nsteps = (int)((off[nk] - T0) >> 5);
-    const uint32_t* p = static_cast<const uint32_t*>(a.pack) + T0 + lane;
-    const XT* __restrict__ x = static_cast<const XT*>(a.x);
-    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
-    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
-    const uint32_t se = (uint32_t)a.se, sig = (uint32_t)a.sigma, kl = (uint32_t)a.k_left;
-    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
-    const uint32_t s0 = (uint32_t)(k0 * 32) + lane;  // storage row of slice k0
-    const uint32_t n_rows = (uint32_t)a.n_rows;
-    auto base2 = [&](int kk) -> uint32_t {
-      const uint32_t g = (uint32_t)a.row0 + s0 + 32u * kk;
-      const uint32_t blk = (g / se) * se;
-      const uint32_t d = blk > kl ? blk - kl : 0u;
-      return 2u * (d < cmax ? d : cmax);
-    };
-    auto flush = [&](int kk, float acc) {
-      const uint32_t s = s0 + 32u * kk;
-      if (s < n_rows) {
-        uint32_t o = s;
-        if (a.mode == PSELL_MODE_IMPLICIT) {
-          const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
-                                                : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
-          o = (s / sig) * sig + pp;
-        }
-        XT yv;
-        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
-        else yv = acc;
-        static_cast<XT*>(a.y)[o] = yv;
-        if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
-      }
-    };
-    auto end_of = [&](int kk) -> int { return (int)((off[kk + 1] - T0) >> 5); };
-    int kk = 0;
-    int bnd = end_of(0);
-    while (bnd == 0 && kk + 1 < nk) {  // leading zero-width slices
-      flush(kk, 0.f);
-      bnd = end_of(++kk);
-    }
-    uint32_t c2 = base2(kk);
-    float acc = 0.f;
-    auto advance = [&](int g) {
-      flush(kk, acc);
-      bnd = end_of(++kk);
-      while (bnd == g && kk + 1 < nk) {
-        flush(kk, 0.f);
-        bnd = end_of(++kk);
-      }
-      c2 = base2(kk);
-      acc = 0.f;
-    };
-    uint32_t cur[U], nxt[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = (u < nsteps) ? __ldcs(p + u * 32) : 0u;
-    for (int g0 = 0; g0 < nsteps; g0 += U) {
-      const int gn = g0 + U;
-      if (gn + U <= nsteps) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) nxt[u] = __ldcs(p + (gn + u) * 32);
-      } else {
-#pragma unroll
-        for (int u = 0; u < U; ++u) nxt[u] = (gn + u < nsteps) ? __ldcs(p + (gn + u) * 32) : 0u;
-      }
-      if (g0 + U <= nsteps) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (g0 + u == bnd) advance(g0 + u);
-          S::run(cur[u], c2, x, acc, m_real, vmask);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (g0 + u < nsteps) {
-            if (g0 + u == bnd) advance(g0 + u);
-            S::run(cur[u], c2, x, acc, m_real, vmask);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-    }
-    flush(kk, acc);
-    for (++kk; kk < nk; ++kk) flush(kk, 0.f);
-  }
-  finish_dot<DOT>(a, dotv);
-}
-
-// ---- persistent strided register pipeline (C == 32).  Warp w of W walks
-// slices w, w+W, w+2W, ... so the resident warps always sweep one dense
-// window of `pack` (DRAM locality, like the one-warp-per-slice launch), but
-// the per-slice dependency chain offset -> pack -> x is broken: the next
-// slice's offsets are loaded a whole slice ahead and its first chunk is
-// issued while the current slice's last chunk is being processed.
-template <int CODEC, typename XT, bool DOT, int U>
-__global__ void __launch_bounds__(kBlock, 6) spmv_persist_kernel(const SpmvArgs a) {
-  using S = FastStep<CODEC, XT>;
-  if constexpr (DOT) {
-    if (a.skip && *a.skip) return;
-  }
-  const int lane = threadIdx.x & 31;
-  const long long W = (long long)gridDim.x * (kBlock / 32);
-  long long k = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const long long n = a.n_slices;
-  const int64_t* off = a.offset;
-  const uint32_t* pack = static_cast<const uint32_t*>(a.pack) + lane;
-  const XT* __restrict__ x = static_cast<const XT*>(a.x);
-  const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
-  const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
-  const uint32_t se = (uint32_t)a.se, sig = (uint32_t)a.sigma, kl = (uint32_t)a.k_left;
-  const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
-  const uint32_t n_rows = (uint32_t)a.n_rows;
-  double dotv = 0.0;
-  if (k < n) {
-    auto base2 = [&](long long kk) -> uint32_t {
-      const uint32_t g = (uint32_t)a.row0 + (uint32_t)(kk * 32) + lane;
-      const uint32_t blk = (g / se) * se;
-      const uint32_t d = blk > kl ? blk - kl : 0u;
-      return 2u * (d < cmax ? d : cmax);
-    };
-    long long o = off[k];
-    int width = (int)((off[k + 1] - o) >> 5);
-    long long kn = k + W, on = 0;
-    int wn = 0;
-    if (kn < n) {
-      on = off[kn];
-      wn = (int)((off[kn + 1] - on) >> 5);
-    }
-    uint32_t cur[U], nxt[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = (u < width) ? __ldcs(pack + o + u * 32) : 0u;
-    uint32_t c2 = base2(k);
-    float acc = 0.f;
-    int q = 0;
-    while (true) {
-      const bool same = q + U < width;
-      if (same) {
-        const uint32_t* pn = pack + o + (long long)(q + U) * 32;
-        if (q + 2 * U <= width) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) nxt[u] = __ldcs(pn + u * 32);
-        } else {
-          const int r = width - q - U;
-#pragma unroll
-          for (int u = 0; u < U; ++u) nxt[u] = (u < r) ? __ldcs(pn + u * 32) : 0u;
-        }
-      } else {
-        const uint32_t* pn = pack + on;
-#pragma unroll
-        for (int u = 0; u < U; ++u) nxt[u] = (u < wn) ? __ldcs(pn + u * 32) : 0u;
-      }
-      if (q + U <= width) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) S::run(cur[u], c2, x, acc, m_real, vmask);
-      } else {
-        const int r = width - q;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (u < r) S::run(cur[u], c2, x, acc, m_real, vmask);
-      }
-      if (same) {
-        q += U;
-      } else {
-        const uint32_t s = (uint32_t)(k * 32) + lane;
-        if (s < n_rows) {
-          uint32_t oo = s;
-          if (a.mode == PSELL_MODE_IMPLICIT) {
-            const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
-                                                  : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
-            oo = (s / sig) * sig + pp;
-          }
-          XT yv;
-          if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
-          else yv = acc;
-          static_cast<XT*>(a.y)[oo] = yv;
-          if constexpr (DOT) dotv += (double)a.p_own[oo] * (double)to_f<XT>(yv);
-        }
-        if (kn >= n) break;
-        k = kn;
-        o = on;
-        width = wn;
-        q = 0;
-        c2 = base2(k);
-        acc = 0.f;
-        kn = k + W;
-        if (kn < n) {
-          on = off[kn];
-          wn = (int)((off[kn + 1] - on) >> 5);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-    }
-  }
-  finish_dot<DOT>(a, dotv);
-}
-
 // ---- TMA-staged production path (C == 32): per-warp cp.async.bulk ring
 //
 // Each warp owns one slice.  Its words stream global -> shared memory through
@@ -1220,21 +1002,6 @@ static int sm_count() {
   return n;
 }
 
-// Work decomposition of the C = 32 production kernel (a pure function of the
-// slice count, so the fused-dot partial count is known on the host):
-//   1   one warp per slice (spmv_fast_kernel)
-//   0   persistent strided warps (spmv_persist_kernel)
-//   >1  that many consecutive slices per warp (spmv_multi_kernel)
-// PSELL_SPW overrides it for A/B sweeps (scripts/spw_sweep.py).
-static int slices_per_warp(long long n_slices) {
-  if (const char* e = getenv("PSELL_SPW")) {
-    const int v = atoi(e);
-    if (v >= 0 && v <= 64) return v;
-  }
-  (void)n_slices;
-  return 1;
-}
-
 // grid of the C = 32 launch: persistent for the TMA ring, one warp per slice otherwise
 static long long spmv_grid(long long n_slices, int c, bool tma) {
   if (c != 32) return 0;
@@ -1287,7 +1054,7 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
     constexpr int U = sizeof(typename WordOf<CODEC>::T) == 4 ? 8 : 4;
     if constexpr (!REF && FastPolicy<CODEC, XT>::kHave) {
       if (a.variant != 2) {
-        if (a.spw == 1) {
+        {
           const int nt = fast_nt();
           const unsigned gnt = (unsigned)ceil_div(rows, nt);
           const unsigned gd = (unsigned)ceil_div(ceil_div(a.n_slices, 2), kWarpsPerCta);
@@ -1304,19 +1071,11 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
             spmv_pair_kernel<CODEC, XT, DOT, 8, false><<<gd, kBlock, 0, st>>>(a);
           } else if (dual_slices(a.n_slices) && du == 12)
             spmv_dual_kernel<CODEC, XT, DOT, 12><<<gd, kBlock, 0, st>>>(a);
-          else if (dual_slices(a.n_slices) && du == 16)
-            spmv_dual_kernel<CODEC, XT, DOT, 16><<<gd, kBlock, 0, st>>>(a);
           else if (dual_slices(a.n_slices))
             spmv_dual_kernel<CODEC, XT, DOT, 8><<<gd, kBlock, 0, st>>>(a);
           else if (nt == 64) spmv_fast_kernel<CODEC, XT, DOT, 8, 64><<<gnt, 64, 0, st>>>(a);
           else if (nt == 128) spmv_fast_kernel<CODEC, XT, DOT, 8, 128><<<gnt, 128, 0, st>>>(a);
           else spmv_fast_kernel<CODEC, XT, DOT, 8, 256><<<gnt, 256, 0, st>>>(a);
-        } else if (a.spw == 0) {
-          const unsigned g = (unsigned)spmv_grid(a.n_slices, 32, true);
-          spmv_persist_kernel<CODEC, XT, DOT, 8><<<g, kBlock, 0, st>>>(a);
-        } else {
-          const unsigned g = (unsigned)ceil_div(ceil_div(a.n_slices, a.spw), kWarps);
-          spmv_multi_kernel<CODEC, XT, DOT, 8><<<g, kBlock, 0, st>>>(a);
         }
       } else {
         static bool carveout = false;  // idempotent attribute, benign race
@@ -1390,7 +1149,6 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.seg_slice = a.seg_q0 = a.long_slice = a.long_seg0 = nullptr;
   a.seg_c2 = nullptr;
   a.seg_partial = nullptr;
-  a.spw = d->c == 32 ? slices_per_warp(a.n_slices) : 1;
   magic_div((uint32_t)(a.se > 0 ? a.se : 1), a.se_m, a.se_l);
   magic_div((uint32_t)(a.sigma > 0 ? a.sigma : 1), a.sig_m, a.sig_l);
   a.l2pf = 1;
@@ -1478,15 +1236,12 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   if (!fast) return "spmv_c32_kernel";
   if (flags & PSELL_SPMV_TMA_STREAM) return "spmv_stream_kernel";
   const long long ns = ceil_div(d->n_rows, d->c);
-  const int spw = slices_per_warp(ns);
-  if (spw == 0) return "spmv_persist_kernel";
-  if (spw > 1) return "spmv_multi_kernel";
   if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel())
     return pair_persist_grid(ns, false) ? "spmv_pair_kernel<U=12, persistent>" : "spmv_pair_kernel<U=12>";
   if (dual_slices(ns) && pair_wide()) return "spmv_pair_kernel<U=8>";
   if (dual_slices(ns)) {
     const int du = dual_chunk((flags & PSELL_SPMV_NARROW) != 0);
-    return du == 12 ? "spmv_dual_kernel<U=12>" : du == 16 ? "spmv_dual_kernel<U=16>" : "spmv_dual_kernel<U=8>";
+    return du == 12 ? "spmv_dual_kernel<U=12>" : "spmv_dual_kernel<U=8>";
   }
   return "spmv_fast_kernel";
 }
@@ -1540,7 +1295,6 @@ int psell_spmv_segmented(const psell_desc* d, const void* pack, const int64_t* o
                    "segmented SpMV: C = 32, fp16/e8my codec, f16/f32 x only");
   a.x = x;
   a.y = y;
-  a.spw = 1;
   a.seg_len = seg_len;
   a.seg_slice = seg_slice;
   a.seg_q0 = seg_q0;
@@ -1565,11 +1319,8 @@ int64_t psell_spmv_dot_partials(const psell_desc* d, int32_t flags) {
   if (!d || d->n_rows <= 0 || d->c < 1) return 1;
   const long long ns = ceil_div(d->n_rows, d->c);
   if (d->c == 32) {
-    // must match launch_spmv<.., DOT=true>: fp16/e8my take the multi-slice kernel when
-    // slices_per_warp > 1; fp32embed (and spw == 1) one warp per slice
-    const int spw = slices_per_warp(ns);
-    if (d->codec != PSELL_FP32EMBED && spw > 1) return ceil_div(ceil_div(ns, spw), kWarps);
-    if (d->codec != PSELL_FP32EMBED && spw == 0) return spmv_grid(ns, 32, true);
+    // must match launch_spmv<.., DOT=true>: fp16/e8my take the (persistent) pair kernel for
+    // narrow slices, the dual kernel otherwise; fp32embed one warp per slice (REF-style kernel)
     if (d->codec != PSELL_FP32EMBED && dual_slices(ns) && pair_kernel() && (flags & PSELL_SPMV_NARROW)) {
       if (const unsigned g = pair_persist_grid(ns, true)) return g;
       return ceil_div(ceil_div(ns, 2), pair_nt(true) / 32);

@@ -6,7 +6,7 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2604_13433_b200 as P  # noqa: E402
-from spw_sweep import bench  # noqa: E402
+from pair_sweep import timed as bench  # noqa: E402
 
 for name, kind, scale, pre, dt in [("c2 27pt fp16 f16x", "stencil27", None, "fp16", torch.float16),
                                    ("c3 27pt e8m10 f32x", "stencil27", "rowsum", "e8m10", torch.float32),
