@@ -620,18 +620,6 @@ __global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const Sp
       l2_prefetch_bulk(static_cast<const uint32_t*>(a.pack) + o0, (uint32_t)(bytes < (1u << 20) ? bytes : (1u << 20)),
                        policy_evict_first());
     }
-    if (PERSIST && a.l2pf >= 2 && lane == 0) {  // next pair of the walk (A/B only: measured slower)
-      const uint32_t kn = kA + 2u * wstride;
-      if (kn < ns) {
-        const long long n0 = a.offset[kn];
-        const long long n2 = a.offset[kn + 2u < ns ? kn + 2u : ns];
-        if (n2 > n0) {
-          const uint64_t bytes = (uint64_t)(n2 - n0) * 4u;
-          l2_prefetch_bulk(static_cast<const uint32_t*>(a.pack) + n0,
-                           (uint32_t)(bytes < (1u << 20) ? bytes : (1u << 20)), policy_evict_first());
-        }
-      }
-    }
     const XT* __restrict__ x = static_cast<const XT*>(a.x);
     const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
     const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
