@@ -259,6 +259,9 @@ PSELL_API int psell_ipcg_update_beta(int64_t n, float* x, float* r, float* z, co
  * one pass (same f32 ops, 4 fewer bytes per row per iteration). */
 PSELL_API int psell_ipcg_direction_x(int64_t n, float* p, const float* z, float* x, const double* scal,
                                      const int32_t* iflags, void* stream);
+/* f64 inner PCG direction (real64 inner precision): p = z + coef[0] p, skipped after a breakdown. */
+PSELL_API int psell_xpby_checked(int64_t n, double* p, const double* z, const double* coef, const int32_t* iflags,
+                                 void* stream);
 PSELL_API int psell_ipcg_beta(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                     void* stream);
 PSELL_API int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal,

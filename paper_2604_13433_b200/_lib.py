@@ -90,6 +90,7 @@ _SIGS = {
     "psell_pq_pr": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P]),
     "psell_axpy2": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psell_xpby": (c_int32, [c_int64, _P, _P, _P, _P]),
+    "psell_xpby_checked": (c_int32, [c_int64, _P, _P, _P, _P, _P]),
     "psell_resid": (c_int32, [c_int64, _P, _P, _P, _P, _P]),
     "psell_precond_dot": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P]),
     "psell_scalar_div": (c_int32, [_P, _P, c_int32, c_int32, _P, _P, c_int32, _P]),

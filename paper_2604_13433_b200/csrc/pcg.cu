@@ -525,6 +525,23 @@ int psell_xpby(int64_t n, double* p, const double* z, const double* coef, void* 
   return LAUNCH_OK();
 }
 
+// p = z + b p unless the inner-PCG breakdown flag is set (f64 inner, solvers.py:307)
+__global__ void __launch_bounds__(kBlock) xpby_checked_kernel(long long n, double* __restrict__ p,
+                                                              const double* __restrict__ z,
+                                                              const double* __restrict__ coef,
+                                                              const int32_t* __restrict__ iflags) {
+  if (iflags[0]) return;
+  const double b = coef[0];
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock)
+    p[i] = __dadd_rn(z[i], __dmul_rn(b, p[i]));
+}
+
+int psell_xpby_checked(int64_t n, double* p, const double* z, const double* coef, const int32_t* iflags,
+                       void* stream) {
+  xpby_checked_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, coef, iflags);
+  return LAUNCH_OK();
+}
+
 int psell_resid(int64_t n, const double* b, const double* ax, double* partials, double* out1,
                 void* stream) {
   cudaStream_t st = as_stream(stream);

@@ -361,51 +361,74 @@ class _InnerPCG:
 
 
 class _GenericInner:
-    """Inner PCG for non-PackSELL backends or f64 inner precision (one GPU; device vectors)."""
+    """Inner PCG (solvers.py:278-308) on any device backend: the SELL-C-sigma / CSR
+    comparators in f32 (the FP32 IO-CG of config 5) and every backend in f64
+    (inner_precision="real64").  One GPU.  The same K3 scalar kernels as _InnerPCG
+    (breakdown flags, alpha / beta on the device); f32 vectors use the f32 update /
+    direction kernels, f64 vectors the outer loop's f64 kernels; the operator is
+    backend.apply on device vectors, p.q a fixed-grid FP64 dot."""
 
     def __init__(self, backend, m_in, dtype, inv):
         import torch
         from . import _dev, _lib
         self.torch = torch
         self.backend = backend
-        self.m_in = m_in
+        self.m_in = int(m_in)
         self.tdt = _dev.torch_dtype(dtype)
+        self.f32 = self.tdt == torch.float32
         self.dt_code = _dev.T_DT_CODE[self.tdt]
         self.inv = inv
         self.d = _Dev(_lib.RED_BLOCKS)
+        self.n = None
 
-    def _dot(self, a, b) -> float:
-        d = self.d
-        d.lib.psell_dot(a.data_ptr(), b.data_ptr(), self.dt_code, a.numel(), d.p(d.partials), d.p(d.loc, 0), d.st())
-        return float(d.loc[0].item())
+    def _alloc(self, n):
+        if self.n != n:
+            t = self.torch
+            self.n = n
+            self.x, self.r, self.p = (t.zeros(n, dtype=self.tdt, device="cuda") for _ in range(3))
+            self.z = t.zeros(n, dtype=self.tdt, device="cuda") if self.inv is not None else self.r
 
     def solve(self, r64, z64) -> int:
-        torch = self.torch
-        rhs = r64.to(self.tdt)
-        x = torch.zeros_like(rhs)
-        r = rhs.clone()
-        P = (lambda v: v) if self.inv is None else (lambda v: v * self.inv)
-        z = P(r)
-        p = z.clone()
-        rz = self._dot(r, z)
-        done = 0
+        d, lib, L = self.d, self.d.lib, self.d.L
+        n = int(r64.numel())
+        self._alloc(n)
+        st = d.st()
+        inv = None if self.inv is None else self.inv.data_ptr()
+        x, r, z, p = self.x, self.r, self.z, self.p
+        if self.f32:
+            lib.psell_ipcg_begin(n, r64.data_ptr(), x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), inv,
+                                 d.p(d.partials), d.p(d.loc, 0), st)
+        else:
+            x.zero_()
+            r.copy_(r64)
+            lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
+            lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
+        lib.psell_ipcg_set_rz(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), st)
         for _ in range(self.m_in):
             q = self.backend.apply(p)
-            pq = self._dot(p, q)
-            if pq <= 0.0 or not np.isfinite(pq) or rz == 0.0:
-                log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate", done, pq)
-                break
-            a = torch.tensor(rz / pq, dtype=self.tdt, device="cuda")
-            x.add_(a * p)
-            r.sub_(a * q)
-            done += 1
-            z = P(r)
-            rzn = self._dot(r, z)
-            beta = torch.tensor(rzn / rz, dtype=self.tdt, device="cuda")
-            rz = rzn
-            p = z + beta * p
-        z64.copy_(x.to(torch.float64))
-        return done
+            lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
+            lib.psell_ipcg_alpha(d.p(d.loc, 1), 1, 8, d.p(d.scal), d.p(d.flags), st)
+            if self.f32:
+                lib.psell_ipcg_update(n, x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), q.data_ptr(), inv,
+                                      d.p(d.scal), d.p(d.flags), d.p(d.partials), d.p(d.loc, 2), st)
+            else:
+                lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 2),
+                                d.p(d.flags), d.p(d.partials), d.p(d.loc, 3), st)
+                lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 2), st)
+            lib.psell_ipcg_beta(d.p(d.loc, 2), 1, 8, d.p(d.scal), d.p(d.flags), st)
+            if self.f32:
+                lib.psell_ipcg_direction(n, p.data_ptr(), z.data_ptr(), d.p(d.scal), d.p(d.flags), st)
+            else:
+                lib.psell_xpby_checked(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 3), d.p(d.flags), st)
+        if self.f32:
+            lib.psell_ipcg_end(n, x.data_ptr(), z64.data_ptr(), st)
+        else:
+            z64.copy_(x)
+        flags = d.flags[:2].cpu().numpy()
+        if int(flags[0]):
+            log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate",
+                        int(flags[1]), float(d.scal[1].item()))
+        return int(flags[1])
 
 
 # ----------------------------------------------------------------------------

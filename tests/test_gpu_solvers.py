@@ -125,3 +125,35 @@ def test_jacobi_preconditioner():
     ri = S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14",
                                     preconditioner="jacobi"))
     assert ri.converged
+
+
+def test_iocg_sell32_inner_matches_reference(golden_solver):
+    """The FP32 IO-CG comparator (SELL-C-sigma f32 inner) on the device kernels."""
+    z, meta = golden_solver
+    A, b = _problem()
+    m = meta["iocg_sell32"]
+    r = S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=m["m_in"], a_backend="sell32", max_outer=200))
+    assert r.converged == m["converged"] and abs(r.outer_iters - m["outer"]) <= 1
+    assert r.total_inner_iters == m["m_in"] * r.outer_iters
+    assert _close(r.x, z["iocg_sell32_x"])
+
+
+@pytest.mark.parametrize("backend", ["packsell-e8m14", "sell64", "csr64"])
+def test_iocg_real64_inner_vs_oracle(backend):
+    """inner_precision="real64": f64 inner PCG kernels vs the oracle's f64 IO-CG."""
+    import oracle as O
+    A, b = _problem(8, 3)
+    cfg = S.SolveConfig(solver="iocg", tol=1e-10, m_in=10, a_backend=backend, inner_precision="real64",
+                        max_outer=200)
+    r = S.iocg(A, b, cfg)
+    if backend.startswith("packsell"):
+        OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, 256, O.preset("e8m14"), "implicit")
+        inner_apply = lambda v: O.spmv(OM, v)  # noqa: E731
+    else:
+        inner_apply = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64)  # noqa: E731
+    ro = O.iocg(lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64), inner_apply, b,
+                1e-10, 200, 10, np.float64)
+    assert r.converged and ro["converged"]
+    assert abs(r.outer_iters - ro["outer_iters"]) <= 1
+    assert r.total_inner_iters == 10 * r.outer_iters
+    assert _close(r.x, ro["x"], 1e-8)
