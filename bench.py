@@ -305,6 +305,14 @@ def run_pcg(args, world, rank, comm, peak):
                                max_outer=1), backend=be, comm=comm)  # warm-up (graph capture)
     rep, t_io = timed(lambda: S.iocg(A, b, cfg, backend=be, comm=comm))
     rep64, t_64 = timed(lambda: S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=5000), comm=comm))
+    rep32 = t_32 = None
+    if world == 1:  # FP32 IO-CG comparator: SELL-C-sigma f32 inner operator, same protocol
+        be32 = S.make_backend(A, "sell32")
+        cfg32 = S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="sell32", max_outer=400)
+        S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="sell32", max_outer=1),
+               backend=be32)
+        rep32, t_32 = timed(lambda: S.iocg(A, b, cfg32, backend=be32))
+        del be32
     touched = n if world == 1 else (r1 - r0) + 2 * nx * nx
     ib, ob = pcg_bytes(be.matrix, r1 - r0, A.nnz, touched)
     io_bytes = rep.total_inner_iters * ib + (rep.outer_iters + 1) * ob
@@ -323,7 +331,12 @@ def run_pcg(args, world, rank, comm, peak):
         "fp64_pcg": {"solve_s": t_64, "iters": rep64.outer_iters, "converged": rep64.converged,
                      "true_relres": rep64.final_true_relres,
                      "roofline_s": agg(p64_bytes) / (peak * world * 1e9)},
+        "fp32_sell_iocg": None if rep32 is None else {
+            "inner": "SELL-C-sigma (C=32, sigma=256) f32 values + int32 columns, f32 vectors, m_in=%d" % args.pcg_m_in,
+            "solve_s": t_32, "outer_iters": rep32.outer_iters, "inner_iters": rep32.total_inner_iters,
+            "converged": rep32.converged, "true_relres": rep32.final_true_relres},
         "speedup_iocg_vs_fp64_pcg": t_64 / t_io,
+        "speedup_iocg_vs_fp32_sell_iocg": None if t_32 is None else t_32 / t_io,
         "build_s": t_build,
         "collectives": "none" if world == 1 else (
             "NCCL point-to-point halo exchange of p (f32 inner, f64 outer; K7 pack/unpack, "
