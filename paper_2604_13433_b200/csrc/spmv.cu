@@ -984,6 +984,217 @@ __global__ void __launch_bounds__(kBlock, kTmaCtasPerSm) spmv_stream_kernel(cons
   finish_dot<DOT>(a, dotv);
 }
 
+// ---- tile-TMA kernel (C == 32, narrow slices): producer/consumer over a smem ring
+//
+// A persistent CTA = 8 consumer warps + 1 producer warp.  Tiles of 16
+// consecutive slices are dealt round-robin over the CTAs (so the tiles in
+// flight across the chip form one dense window of `pack`, keeping DRAM pages
+// open).  The producer's elected lane streams each tile's words — one
+// contiguous byte range, since slices are stored back to back — into a 4-stage
+// shared-memory ring with ONE cp.async.bulk per tile (mbarrier complete_tx),
+// up to 4 tiles ahead; consumer warps take two slices each, read the words
+// with conflict-free LDS (step q of a slice is 32 consecutive words), and run
+// the usual decode / gather / FMA.  HBM latency is off the consumers' critical
+// path; they only wait on the L2-resident x gathers.  A tile wider than a
+// stage (12 steps per slice on average) is flagged and read straight from HBM.
+constexpr int kTileSlices = 16;
+constexpr int kTileStages = 4;
+constexpr int kTileStageWords = kTileSlices * 12 * 32;  // 24 KB
+constexpr int kTileConsumers = 8;
+constexpr int kTileThreads = (kTileConsumers + 1) * 32;
+constexpr int kTileCtasPerSm = 2;
+constexpr size_t kTileSmemBytes = (size_t)kTileStages * kTileStageWords * 4;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// both slices of a warp interleaved step by step (24 gathers in flight per 12-step chunk)
+template <int CODEC, typename XT, bool SMEM>
+__device__ __forceinline__ void tile_pair(const uint32_t* pA, int wA, const uint32_t* pB, int wB, uint32_t cA,
+                                          uint32_t cB, const XT* x, uint32_t m_real, uint32_t vmask, float& accA,
+                                          float& accB) {
+  using S = FastStep<CODEC, XT>;
+  constexpr int U = 12;
+  accA = 0.f;
+  accB = 0.f;
+  const int wm = wA > wB ? wA : wB;
+  for (int q = 0; q < wm; q += U) {
+    uint32_t ua[U], ub[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (SMEM) {
+        ua[u] = (q + u < wA) ? pA[(q + u) * 32] : 0u;
+        ub[u] = (q + u < wB) ? pB[(q + u) * 32] : 0u;
+      } else {
+        ua[u] = (q + u < wA) ? __ldcs(pA + (q + u) * 32) : 0u;
+        ub[u] = (q + u < wB) ? __ldcs(pB + (q + u) * 32) : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      S::run(ua[u], cA, x, accA, m_real, vmask);
+      S::run(ub[u], cB, x, accB, m_real, vmask);
+    }
+  }
+}
+
+template <int CODEC, typename XT, bool DOT>
+__global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm) spmv_tile_kernel(const SpmvArgs a) {
+  extern __shared__ __align__(128) uint32_t tsm[];  // [kTileStages][kTileStageWords]
+  __shared__ __align__(8) uint64_t full[kTileStages];
+  __shared__ __align__(8) uint64_t empty[kTileStages];
+  __shared__ long long tbase[kTileStages];
+  __shared__ int tdirect[kTileStages];
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ns = (uint32_t)a.n_slices;
+  const uint32_t n_tiles = (ns + kTileSlices - 1) / kTileSlices;
+  const uint32_t* pack = static_cast<const uint32_t*>(a.pack);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < kTileStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTileConsumers);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  double dotv = 0.0;
+  if (warp == kTileConsumers) {  // producer warp
+    // the word ranges of the CTA's next 32 tiles are loaded warp-wide at once
+    // (lane j: tile j of the batch), so the issuing lane never waits on an
+    // offset load between two bulk copies
+    const uint64_t pol = policy_evict_first();
+    int i = 0;
+    for (uint32_t tb = blockIdx.x; tb < n_tiles; tb += 32u * gridDim.x) {
+      const uint32_t tj = tb + (uint32_t)lane * gridDim.x;
+      long long bj = 0, ej = 0;
+      if (tj < n_tiles) {
+        bj = a.offset[tj * kTileSlices];
+        ej = a.offset[min((tj + 1) * (uint32_t)kTileSlices, ns)];
+      }
+      const int nb = (int)min(32u, (n_tiles - tb + gridDim.x - 1) / gridDim.x);
+      for (int j = 0; j < nb; ++j, ++i) {
+        const long long w0 = __shfl_sync(0xffffffffu, bj, j);
+        const long long words = __shfl_sync(0xffffffffu, ej, j) - w0;
+        if (lane == 0) {
+          const int st = i % kTileStages;
+          if (i >= kTileStages) mbar_wait(&empty[st], (uint32_t)((i / kTileStages) - 1) & 1u);
+          tbase[st] = w0;
+          if (words <= kTileStageWords) {
+            tdirect[st] = 0;
+            const uint32_t bytes = (uint32_t)words * 4u;
+            mbar_expect_tx(&full[st], bytes);
+            if (bytes) bulk_g2s(tsm + st * kTileStageWords, pack + w0, bytes, &full[st], pol);
+          } else {
+            tdirect[st] = 1;
+            mbar_arrive(&full[st]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else {  // consumers: slices 2w, 2w+1 of each tile
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+    const uint32_t kl = (uint32_t)a.k_left, n_rows = (uint32_t)a.n_rows;
+    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    const bool impl = a.mode == PSELL_MODE_IMPLICIT;
+    int i = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int st = i % kTileStages;
+      const uint32_t kA = t * kTileSlices + 2u * warp, kB = kA + 1u;
+      const bool hasA = kA < ns, hasB = kB < ns;
+      // independent of the stage: offsets, perm bytes, base offsets (latency overlaps the wait)
+      long long o0 = 0, o1 = 0, o2 = 0;
+      uint32_t oA = 0, oB = 0;
+      if (hasA) {
+        o0 = a.offset[kA];
+        o1 = a.offset[kA + 1];
+        o2 = hasB ? a.offset[kA + 2] : o1;
+        const uint32_t sA = kA * 32u + lane, sB = sA + 32u;
+        oA = sA;
+        oB = sB;
+        if (impl) {
+          const uint32_t blkA = fast_div(kA * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma;
+          const uint32_t blkB = fast_div(kB * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma;
+          if (a.perm_bytes == 1) {
+            const uint8_t* pm = static_cast<const uint8_t*>(a.perm);
+            oA = blkA + (sA < n_rows ? (uint32_t)__ldg(pm + sA) : 0u);
+            oB = blkB + (sB < n_rows ? (uint32_t)__ldg(pm + sB) : 0u);
+          } else {
+            const uint16_t* pm = static_cast<const uint16_t*>(a.perm);
+            oA = blkA + (sA < n_rows ? (uint32_t)__ldg(pm + sA) : 0u);
+            oB = blkB + (sB < n_rows ? (uint32_t)__ldg(pm + sB) : 0u);
+          }
+        }
+      }
+      auto base2 = [&](uint32_t k) -> uint32_t {
+        const uint32_t g = (uint32_t)a.row0 + k * 32u + lane;
+        const uint32_t blk = a.se == 1 ? g : fast_div(g, a.se_m, a.se_l) * (uint32_t)a.se;
+        const uint32_t d = blk > kl ? blk - kl : 0u;
+        return 2u * (d < cmax ? d : cmax);
+      };
+      mbar_wait(&full[st], (uint32_t)(i / kTileStages) & 1u);
+      if (hasA) {
+        const int wA = (int)((o1 - o0) >> 5), wB = (int)((o2 - o1) >> 5);
+        float accA, accB;
+        if (!tdirect[st]) {
+          const uint32_t* sp = tsm + st * kTileStageWords + (uint32_t)(o0 - tbase[st]) + lane;
+          tile_pair<CODEC, XT, true>(sp, wA, sp + (uint32_t)(o1 - o0), wB, base2(kA), base2(kB), x, m_real, vmask,
+                                     accA, accB);
+        } else {
+          tile_pair<CODEC, XT, false>(pack + o0 + lane, wA, pack + o1 + lane, wB, base2(kA), base2(kB), x, m_real,
+                                      vmask, accA, accB);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // words consumed: the producer may refill
+        auto flush = [&](uint32_t s, uint32_t o, float acc) {
+          if (s < n_rows) {
+            XT yv;
+            if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+            else yv = acc;
+            static_cast<XT*>(a.y)[o] = yv;
+            if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
+          }
+        };
+        flush(kA * 32u + lane, oA, accA);
+        if (hasB) flush(kB * 32u + lane, oB, accB);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+    }
+  }
+  finish_dot<DOT, kTileThreads>(a, dotv);
+}
+
+static int sm_count();
+
+template <int CODEC, typename XT, bool DOT>
+static void launch_tile(const SpmvArgs& a, cudaStream_t st) {
+  static bool attr = false;  // idempotent attribute, benign race
+  if (!attr) {
+    cudaFuncSetAttribute(spmv_tile_kernel<CODEC, XT, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kTileSmemBytes);
+    attr = true;
+  }
+  const long long n_tiles = ceil_div(a.n_slices, kTileSlices);
+  const long long cap = (long long)sm_count() * kTileCtasPerSm;
+  const unsigned g = (unsigned)(n_tiles < cap ? n_tiles : cap);
+  spmv_tile_kernel<CODEC, XT, DOT><<<g, kTileThreads, kTileSmemBytes, st>>>(a);
+}
+
+// tile-TMA kernel for narrow slices instead of the persistent pair kernel (PSELL_TILE=1, A/B)
+static bool tile_kernel() {
+  if (const char* e = getenv("PSELL_TILE")) return atoi(e) != 0;
+  return false;
+}
+
 static int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -1047,7 +1258,9 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
           const unsigned gnt = (unsigned)ceil_div(rows, nt);
           const unsigned gd = (unsigned)ceil_div(ceil_div(a.n_slices, 2), kWarpsPerCta);
           const int du = dual_chunk(a.narrow);
-          if (dual_slices(a.n_slices) && a.narrow && pair_kernel()) {
+          if (a.narrow && tile_kernel()) {
+            launch_tile<CODEC, XT, DOT>(a, st);
+          } else if (dual_slices(a.n_slices) && a.narrow && pair_kernel()) {
             const int pn = pair_nt(DOT);
             const unsigned gp = (unsigned)ceil_div(ceil_div(a.n_slices, 2), pn / 32);
             const unsigned gpp = pair_persist_grid(a.n_slices, DOT);
@@ -1224,6 +1437,7 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   if (!fast) return "spmv_c32_kernel";
   if (flags & PSELL_SPMV_TMA_STREAM) return "spmv_stream_kernel";
   const long long ns = ceil_div(d->n_rows, d->c);
+  if ((flags & PSELL_SPMV_NARROW) && tile_kernel()) return "spmv_tile_kernel (TMA ring)";
   if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel())
     return pair_persist_grid(ns, false) ? "spmv_pair_kernel<U=12, persistent>" : "spmv_pair_kernel<U=12>";
   if (dual_slices(ns) && pair_wide()) return "spmv_pair_kernel<U=8>";
@@ -1309,6 +1523,11 @@ int64_t psell_spmv_dot_partials(const psell_desc* d, int32_t flags) {
   if (d->c == 32) {
     // must match launch_spmv<.., DOT=true>: fp16/e8my take the (persistent) pair kernel for
     // narrow slices, the dual kernel otherwise; fp32embed one warp per slice (REF-style kernel)
+    if (d->codec != PSELL_FP32EMBED && tile_kernel() && (flags & PSELL_SPMV_NARROW)) {
+      const long long n_tiles = ceil_div(ns, kTileSlices);
+      const long long cap = (long long)sm_count() * kTileCtasPerSm;
+      return n_tiles < cap ? n_tiles : cap;
+    }
     if (d->codec != PSELL_FP32EMBED && dual_slices(ns) && pair_kernel() && (flags & PSELL_SPMV_NARROW)) {
       if (const unsigned g = pair_persist_grid(ns, true)) return g;
       return ceil_div(ceil_div(ns, 2), pair_nt(true) / 32);

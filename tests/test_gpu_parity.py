@@ -319,3 +319,31 @@ def test_production_kernels_non_pow2_sigma(rng, sigma, nnz_per_row, mode):
         anorm = np.bincount(np.repeat(np.arange(n), np.diff(rp)), np.abs(P.quantize(P.parse_format(pre), v))).max()
         err = np.abs(yf - yr.astype(np.float64)).max() / (anorm * np.abs(x.astype(np.float64)).max())
         assert err <= 2 * lmax * 2.0 ** -24 + (2.0 ** -11 if dt == np.float16 else 0.0), (pre, err)
+
+
+@pytest.mark.parametrize("kind,nx", [("poisson3d", 24), ("poisson2d", 200)])
+def test_tile_tma_kernel_equals_pair_kernel(monkeypatch, kind, nx):
+    """A/B kernel (PSELL_TILE=1: TMA producer/consumer ring) gives the production kernel's bits,
+    plain and with the fused p.q."""
+    from paper_2604_13433_b200 import _lib
+    S = P.stencil_device(kind, nx, scale="sym")
+    M = P.build_packsell(S, 32, 256, P.parse_format("e8m14"), "implicit")
+    assert M.spmv_flags() & 4  # narrow slices
+    import torch
+    x = torch.rand(M.n_cols, device="cuda") * 2 - 1
+    lib = _lib.lib()
+    res = {}
+    for tile in ("0", "1"):
+        monkeypatch.setenv("PSELL_TILE", tile)
+        y = P.packsell_spmv(M, x)
+        npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
+        part = torch.zeros(npart, dtype=torch.float64, device="cuda")
+        q = torch.empty_like(x)
+        err = _lib.PsellError()
+        rc = lib.psell_spmv_dot(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                                x.data_ptr(), q.data_ptr(), x.data_ptr(), part.data_ptr(), None, M.spmv_flags(),
+                                _lib.stream_handle(), err)
+        _lib.check(rc, err)
+        res[tile] = (y.clone(), q.clone(), float(part.sum()))
+    assert torch.equal(res["0"][0], res["1"][0]) and torch.equal(res["0"][1], res["1"][1])
+    assert res["0"][2] == pytest.approx(res["1"][2], rel=1e-12)
