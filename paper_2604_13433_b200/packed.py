@@ -17,7 +17,7 @@ from typing import NamedTuple, Optional
 import numpy as np
 
 from . import codec
-from .matrix import CsrMatrix, DeviceCsrMatrix
+from .matrix import CsrMatrix
 from .sell import _check_layout_params, perm_dtype
 
 MODES = ("none", "explicit", "implicit")

@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .matrix import CooMatrix, CsrMatrix, to_csr
+from .matrix import CsrMatrix
 
 
 def _grid_stencil(dims, box: bool, diag: float, row_begin: int = 0, row_end: int = None) -> CsrMatrix:
