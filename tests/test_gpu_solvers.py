@@ -157,3 +157,23 @@ def test_iocg_real64_inner_vs_oracle(backend):
     assert abs(r.outer_iters - ro["outer_iters"]) <= 1
     assert r.total_inner_iters == 10 * r.outer_iters
     assert _close(r.x, ro["x"], 1e-8)
+
+
+def test_iocg_and_pcg_64cubed_vs_reference():
+    """Config-5 protocol at 64^3 (e8m14 inner, m_in 50) against the real reference's solve."""
+    import json
+    import os
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "solver64_golden.npz"))
+    with open(os.path.join(GOLDEN, "solver64_golden.json")) as f:
+        meta = json.load(f)
+    A = P.sym_diag_scale(P.poisson3d(64))
+    b, _ = S.make_rhs_and_x0(A.n_rows, 42)
+    r = S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=50, a_backend="packsell-e8m14", max_outer=400))
+    m = meta["iocg"]
+    assert r.converged == m["converged"] and abs(r.outer_iters - m["outer"]) <= 1
+    assert r.total_inner_iters == 50 * r.outer_iters and r.final_true_relres < 1e-9
+    assert _close(r.x, z["iocg_x"])
+    p = S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=2000))
+    assert p.converged and abs(p.outer_iters - meta["pcg"]["outer"]) <= 1
+    assert _close(p.x, z["pcg_x"], 1e-9)
