@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round evidence in one gpurun call: GPU tests, smoke, bench lines for every config, the
+# reference arm, ncu launch lists and --set full captures of the production SpMV kernels.
+mkdir -p gpurun_out/ev
+cd "$(dirname "$0")/.."
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,power.limit --format=csv > gpurun_out/ev/gpu.txt 2>&1
+timeout -s KILL 900 python -m pytest tests -m gpu -q > gpurun_out/ev/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ev/pytest_gpu.log
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/ev/smoke.log
+timeout -s KILL 900 python bench.py > gpurun_out/ev/bench_c2.log 2>&1
+for c in c1 c3 c4; do timeout -s KILL 600 python bench.py --config $c --no-pcg > gpurun_out/ev/bench_$c.log 2>&1; done
+timeout -s KILL 600 python bench.py --impl reference > gpurun_out/ev/bench_reference.log 2>&1
+for c in c2 c3 c4; do
+  timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
+      --log-file gpurun_out/ev/launches_$c.csv python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-pcg > /dev/null 2>&1
+done
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_dual -s 3 -c 1 -o gpurun_out/ev/prof_c2 \
+    python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline --no-pcg > /dev/null 2>&1
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_dual -s 3 -c 1 -o gpurun_out/ev/prof_c4 \
+    python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline --no-pcg > /dev/null 2>&1
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_pair -s 3 -c 1 -o gpurun_out/ev/prof_c5 \
+    python scripts/prof_c5_spmv.py > /dev/null 2>&1
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv \
+    --log-file gpurun_out/ev/launches_pcg_iter.csv python scripts/pcg_iter.py 64 > /dev/null 2>&1
+tail -2 gpurun_out/ev/pytest_gpu.log; tail -1 gpurun_out/ev/smoke.log
