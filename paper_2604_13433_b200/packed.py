@@ -440,7 +440,13 @@ def packsell_spmv_stream(M: PackSellMatrix, xs, outs=None, *, ref_order: bool = 
 
 def packsell_to_csr(M: PackSellMatrix) -> CsrMatrix:
     """Decode every delta chain back to the quantised CSR, logical row order (packed.py:274-303)."""
+    return _to_csr_device(M).to_host()
+
+
+def _to_csr_device(M: PackSellMatrix):
+    """K5 decode into an HBM-resident CSR (DeviceCsrMatrix; row0 = M.row0)."""
     from . import _dev, _lib
+    from .matrix import DeviceCsrMatrix
     lib = _lib.lib()
     d = M.desc()
     ws = _dev.workspace(lib.psell_to_csr_workspace_bytes(d))
@@ -456,8 +462,7 @@ def packsell_to_csr(M: PackSellMatrix) -> CsrMatrix:
     rc = lib.psell_to_csr_fill(d, _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
                                _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(val), st, err)
     _lib.check(rc, err, M.fmt)
-    return CsrMatrix(M.n_rows, M.n_cols, _dev.download(row_ptr, np.int64),
-                     _dev.download(col, np.int32), _dev.download(val, np.float64))
+    return DeviceCsrMatrix(M.n_rows, M.n_cols, row_ptr, col, val, row0=M.row0)
 
 
 def footprint_bits(M: PackSellMatrix) -> FootprintReport:
