@@ -61,7 +61,7 @@ def _staging():
     return _stage
 
 
-def upload_pinned(a: np.ndarray, device=None) -> torch.Tensor:
+def upload_pinned(a: np.ndarray, device=None, out: torch.Tensor = None) -> torch.Tensor:
     """Host array -> device through a reused double-buffered page-locked stage.
 
     Large solver vectors (134 MB at 256^3) would otherwise go through the
@@ -71,7 +71,8 @@ def upload_pinned(a: np.ndarray, device=None) -> torch.Tensor:
     s = _SIGNED.get(a.dtype)
     if s is not None:
         a = a.view(s)
-    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=device or DEVICE)
+    if out is None:
+        out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=device or DEVICE)
     src = a.reshape(-1).view(np.uint8)
     dst = out.view(-1).view(torch.uint8)
     buf, ev = _staging()
