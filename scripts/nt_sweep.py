@@ -1,4 +1,4 @@
-"""A/B threads-per-CTA (PSELL_NT) of the one-warp-per-slice SpMV on configs 2/3/5."""
+"""A/B threads-per-CTA (PSELL_NT) of the one-warp-per-slice SpMV (PSELL_DUAL=0) on configs 2/3/5."""
 import os
 import sys
 
@@ -18,10 +18,12 @@ for name, kind, scale, pre, dt in [("c2 27pt fp16 f16x", "stencil27", None, "fp1
     x = (torch.rand(M.n_cols, device="cuda") * 2 - 1).to(dt)
     y = torch.empty(M.n_rows, dtype=dt, device="cuda")
     nb = M.spmv_bytes(x.element_size())
+    os.environ["PSELL_DUAL"] = "0"
     for nt in (256, 128, 64):
         os.environ["PSELL_NT"] = str(nt)
-        ms = bench(M, x, y)
+        ms = bench(lambda: P.packsell_spmv(M, x, out=y))
         print(f"{name:22s} NT={nt:3d} {ms * 1e3:8.1f} us {nb / ms / 1e6:8.1f} GB/s", flush=True)
     os.environ.pop("PSELL_NT")
+    os.environ.pop("PSELL_DUAL")
     del M
     torch.cuda.empty_cache()
