@@ -50,3 +50,12 @@ def row_sort_order(counts, sigma: int) -> np.ndarray:
                               _lib.stream_handle(), err)
     _lib.check(rc, err)
     return _dev.download(order, np.int32).astype(np.int64)
+
+
+def __getattr__(name):
+    """`sell.SellMatrix / build_sell / sell_spmv` as in the reference module (sell.py:49-204);
+    they live in sellfmt (device containers), loaded lazily to keep this module import-light."""
+    if name in ("SellMatrix", "build_sell", "sell_spmv"):
+        from . import sellfmt
+        return getattr(sellfmt, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
