@@ -204,3 +204,29 @@ def test_cli_footprint_and_solve(capsys, tmp_path, poisson_file):
     assert lines[0] == "iteration,relative_residual" and len(lines) == len(rep["residual_history"]) + 1
     code, o, e = _run(capsys, "solve", poisson_file, "--max-outer", "2")
     assert code == 1 and json.loads(o)["converged"] is False and "did not converge" in e
+
+
+def test_integration_ctypes_stub_runs():
+    """The reference-side ctypes binding shown in INTEGRATION.md §3 works as written."""
+    import os
+    import re
+    import types
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    sec = text[text.index("## 3. The C ABI directly"):]
+    code = re.search(r"```python\n(.*?)```", sec, re.S).group(1)
+    code = code.replace('ctypes.CDLL("paper_2604_13433_b200/libpsell.so")',
+                        'ctypes.CDLL(os.path.join(ROOT, "paper_2604_13433_b200", "libpsell.so"))')
+    ns = {"os": os, "ROOT": root}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    rng = np.random.default_rng(3)
+    from conftest import random_csr_arrays
+    rp, ci, v = random_csr_arrays(rng, 300, 280, 0.05)
+    A = P.CsrMatrix(300, 280, rp, ci, v)
+    M = P.build_packsell(A, 32, 256, P.parse_format("e8m14"), "implicit")
+    ref_like = types.SimpleNamespace(fmt=M.fmt, c=M.c, sigma=M.sigma, mode=M.mode, n_rows=M.n_rows,
+                                     n_cols=M.n_cols, k_left=M.k_left, counts=M.counts, pack=M.pack,
+                                     offset=M.offset, perm=M.perm)
+    x = rng.uniform(-1, 1, 280).astype(np.float32)
+    y = ns["packsell_spmv_b200"](ref_like, x)
+    assert np.array_equal(y, P.packsell_spmv(M, x))
