@@ -602,7 +602,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--sigma", type=int, default=0, help="override the sorting window")
     ap.add_argument("--ref-rows", type=int, default=131072, help="rows per CPU worker (reference arm)")
-    ap.add_argument("--cpu-rows", type=int, default=262144, help="rows of the cpu_baseline sample")
+    ap.add_argument("--cpu-rows", type=int, default=1048576, help="rows of the cpu_baseline sample (~10 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pcg", action="store_true", help="skip the config-5 PCG time-to-solution")
     ap.add_argument("--pcg-nx", type=int, default=256)
