@@ -5,7 +5,7 @@
  * (pure Python/numpy, /root/reference/pkg/src/packsell).  The reference has
  * no FFI of its own; each entry point below replaces the numpy body of the
  * reference function named beside it, and the Python mirror
- * (paper_2604_13433_b200/*.py) binds them with ctypes exactly where the
+ * (the modules of paper_2604_13433_b200/) binds them with ctypes exactly where the
  * reference calls numpy.  See INTEGRATION.md for the bindings.
  *
  * Conventions

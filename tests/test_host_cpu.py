@@ -162,3 +162,19 @@ def test_public_api_covers_reference():
     from paper_2604_13433_b200 import cli, container, metrics, sell
     assert callable(cli.main) and callable(container.read_psell) and callable(metrics.bench_spmv)
     assert sell.build_sell is P.build_sell
+
+
+@pytest.mark.parametrize("lang,std", [("c", "c99"), ("c++", "c++17")])
+def test_header_is_plain_c_abi(lang, std, tmp_path):
+    """include/psell.h compiles warning-free as C99 and C++17 (the boundary is a C ABI)."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc" if lang == "c" else "g++")
+    if cc is None:
+        pytest.skip("no host compiler")
+    src = tmp_path / ("t.c" if lang == "c" else "t.cc")
+    src.write_text('#include "psell.h"\nint main(void) { psell_desc d; psell_error e; (void)d; (void)e; '
+                   'return psell_abi_version() == PSELL_ABI_VERSION ? 0 : 1; }\n')
+    r = subprocess.run([cc, "-std=" + std, "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
+                        "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
