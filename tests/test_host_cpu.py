@@ -178,3 +178,41 @@ def test_header_is_plain_c_abi(lang, std, tmp_path):
     r = subprocess.run([cc, "-std=" + std, "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
                         "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_plain_c_program_links_and_calls_the_abi(tmp_path):
+    """A C program (no Python) links libpsell.so and calls its host-only entry points."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc")
+    if cc is None:
+        pytest.skip("no host compiler")
+    src = tmp_path / "abi.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "psell.h"
+int main(void) {
+  psell_desc d = {32, 15, PSELL_FP16, 32, 256, PSELL_MODE_IMPLICIT, 1 << 20, 1 << 20, 0, -1, 27000000};
+  size_t ws = psell_build_workspace_bytes(&d);
+  printf("%s %zu\n", psell_version(), ws);
+  return (psell_abi_version() == PSELL_ABI_VERSION && ws > 0) ? 0 : 1;
+}
+''')
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    exe = tmp_path / "abi"
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-I", os.path.join(ROOT, "include"), str(src), "-L", libdir,
+                        "-lpsell", "-Wl,-rpath," + libdir, "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    env = dict(os.environ)
+    import torch  # noqa: F401  (makes the bundled libcudart discoverable like the Python path does)
+    cudart = [p for p in os.environ.get("LD_LIBRARY_PATH", "").split(":") if p]
+    try:
+        import nvidia.cuda_runtime as ncr
+        cudart.append(os.path.join(os.path.dirname(ncr.__file__), "lib"))
+    except ImportError:
+        pass
+    cudart.append("/usr/local/cuda/lib64")
+    env["LD_LIBRARY_PATH"] = ":".join(cudart)
+    run = subprocess.run([str(exe)], capture_output=True, text=True, env=env)
+    assert run.returncode == 0, run.stderr
+    assert "sm_100a" in run.stdout
