@@ -443,6 +443,22 @@ def packsell_to_csr(M: PackSellMatrix) -> CsrMatrix:
     return _to_csr_device(M).to_host()
 
 
+def _decoded_row_lengths(M: PackSellMatrix) -> np.ndarray:
+    """Real entries per logical row (the decode's row pointer, packed.py:274-303) on the host."""
+    from . import _dev, _lib
+    lib = _lib.lib()
+    d = M.desc()
+    ws = _dev.workspace(lib.psell_to_csr_workspace_bytes(d))
+    row_ptr = _dev.empty(M.n_rows + 1, np.int64)
+    nnz = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    rc = lib.psell_to_csr_plan(d, _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                               _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr), ctypes.byref(nnz),
+                               _lib.stream_handle(), err)
+    _lib.check(rc, err, M.fmt)
+    return np.diff(_dev.download_pinned(row_ptr))
+
+
 def _to_csr_device(M: PackSellMatrix):
     """K5 decode into an HBM-resident CSR (DeviceCsrMatrix; row0 = M.row0)."""
     from . import _dev, _lib
@@ -475,10 +491,9 @@ def footprint_bits(M: PackSellMatrix) -> FootprintReport:
     value_bits = 16 if M.fmt.codec == codec.FP16 else 32
     perm_bits = 0 if M.perm is None else M.perm.dtype.itemsize * 8 * len(M.perm)
     pack_bits = M.fmt.w * M.n_stored + 64 * (M.n_slices + 1) + perm_bits
-    A = packsell_to_csr(M)
+    lens = _decoded_row_lengths(M)  # K5 count pass only: no column / value decode or download
     sell_mode = "none" if M.mode == "explicit" else M.mode
-    lens = A.row_lengths()
-    n = A.n_rows
+    n = M.n_rows
     if sell_mode == "none":
         ordered = lens
     else:

@@ -230,3 +230,17 @@ def test_integration_ctypes_stub_runs():
     x = rng.uniform(-1, 1, 280).astype(np.float32)
     y = ns["packsell_spmv_b200"](ref_like, x)
     assert np.array_equal(y, P.packsell_spmv(M, x))
+
+
+def test_footprint_bits_vs_reference():
+    """footprint_bits (packed.py:306-327) equals the reference on 15 fixtures (all modes, C, sigma, codecs)."""
+    z = np.load(os.path.join(GOLDEN, "footprint_golden.npz"))
+    with open(os.path.join(GOLDEN, "footprint_golden.json")) as f:
+        meta = json.load(f)
+    for i, m in enumerate(meta):
+        p = f"f{i}_"
+        A = P.CsrMatrix(m["n_rows"], m["n_cols"], z[p + "row_ptr"], z[p + "col_idx"], z[p + "values"])
+        M = P.build_packsell(A, m["c"], m["sigma"], P.parse_format(m["preset"]), m["mode"])
+        fp = P.footprint_bits(M)
+        assert (fp.pack_bits, fp.sell_equiv_bits) == (m["pack_bits"], m["sell_equiv_bits"]), i
+        assert fp.ratio == m["ratio"], i
