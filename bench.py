@@ -515,6 +515,17 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     ms_e2e = allreduce((time.perf_counter() - w0) / k_e2e * 1e3, dist.ReduceOp.MAX if world > 1 else None)
     e2e_value = bytes_all / (ms_e2e * 1e-3) / 1e9
+    # the literal drop-in call: numpy x in, numpy y out (packed.py:242 signature), one call per step
+    x_np = xh.numpy().copy()
+    for _ in range(2):
+        P.packsell_spmv(M, x_np)
+    barrier()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for _ in range(k_e2e):
+        P.packsell_spmv(M, x_np)
+    ms_np = allreduce((time.perf_counter() - w0) / k_e2e * 1e3, dist.ReduceOp.MAX if world > 1 else None)
+    del x_np
     # the e2e bound: pinned H2D of x and D2H of y on two copy engines, no compute
     s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
     xd_b, yd_b = torch.empty_like(x), torch.empty_like(y)
@@ -581,6 +592,9 @@ def run_ours(args, cfg):
                            "(copy-in / compute / copy-out streams overlapped across steps)",
                     "pcie_bound": {"ms_per_step": ms_pcie, "frac": ms_pcie / ms_e2e,
                                    "what": "x H2D || y D2H from / to pinned host memory alone (no SpMV)"},
+                    "numpy_per_call": {"value": bytes_all / (ms_np * 1e-3) / 1e9, "ms_per_step": ms_np,
+                                       "api": "y = packsell_spmv(M, x_numpy) (the reference signature; "
+                                              "pageable H2D, D2H into cached page-locked memory)"},
                     "sync_per_call": {"value": bytes_all / (ms_sync * 1e-3) / 1e9, "ms_per_step": ms_sync,
                                       "api": "packsell_spmv(M, x_pinned_cpu, out=y_pinned_cpu), one blocking call per step"}},
             "gpu_launches": args.steps * launches_per_step,

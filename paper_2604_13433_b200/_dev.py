@@ -34,8 +34,13 @@ def torch_dtype(np_dtype) -> torch.dtype:
     return _NP2T[np.dtype(np_dtype)]
 
 
+_PINNED_MIN = 4 << 20  # results from 4 MiB up land in page-locked memory
+
+
 def upload(a: np.ndarray, device=None) -> torch.Tensor:
-    """Copy a host array to the device (unsigned types as same-width signed)."""
+    """Copy a host array to the device (unsigned types as same-width signed).
+    (Pageable H2D measured faster than staging through pinned memory: 1.8 vs 2.7 ms
+    for 33.5 MB, the driver pipelines its own bounce buffer.)"""
     a = np.ascontiguousarray(a)
     s = _SIGNED.get(a.dtype)
     if s is not None:
@@ -44,8 +49,19 @@ def upload(a: np.ndarray, device=None) -> torch.Tensor:
 
 
 def download(t: torch.Tensor, np_dtype) -> np.ndarray:
-    """Device tensor -> host array re-viewed as np_dtype (same item size)."""
-    h = t.detach().cpu().numpy()
+    """Device tensor -> host array re-viewed as np_dtype (same item size).
+
+    Large results are copied into a page-locked tensor from torch's caching host
+    allocator and returned as a numpy view of it: full-PCIe D2H with no host
+    bounce (33.5 MB: 0.6 ms vs 15.5 ms pageable; the pinned block returns to the
+    cache when the array is released)."""
+    t = t.detach()
+    if t.is_cuda and t.numel() * t.element_size() >= _PINNED_MIN:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        h = h.numpy()
+    else:
+        h = t.cpu().numpy()
     return h.view(np.dtype(np_dtype)) if h.dtype != np.dtype(np_dtype) else h
 
 
