@@ -472,7 +472,7 @@ class _Outer:
         b = np.asarray(b, dtype=np.float64)
         self.n = len(b)
         from . import _dev
-        self.b = _dev.upload_pinned(b)
+        self.b = _dev.upload(b)
         self.d = _Dev(_lib.RED_BLOCKS, comm)
         self.lib = self.d.lib
         f64 = torch.float64
