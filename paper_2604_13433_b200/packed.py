@@ -361,22 +361,35 @@ def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None, _p
     import torch
     from . import _dev
     if _is_tensor(x):
+        if x.dim() != 1:
+            raise ValueError(f"x must be one-dimensional, got shape {tuple(x.shape)}")
         if len(x) != M.n_cols:
             raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
         if x.dtype not in _dev.T_DT_CODE:
             raise TypeError(f"unsupported x dtype {x.dtype}")
+        if out is not None and (not _is_tensor(out) or out.dim() != 1 or out.numel() != M.n_rows
+                                or out.dtype != x.dtype or not out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous {x.dtype} tensor of {M.n_rows} entries")
         if x.is_cuda:
+            if x.device != M.d_pack.device:
+                raise ValueError(f"x is on {x.device}, the matrix on {M.d_pack.device}")
+            if out is not None and out.device != x.device:
+                raise ValueError(f"out must be on {x.device}")
             y = out if out is not None else torch.empty(M.n_rows, dtype=x.dtype, device=x.device)
-            return _spmv_device(M, x, y, ref_order, _pipe)
-        xd = x.to(_dev.DEVICE, non_blocking=True)
-        yd = torch.empty(M.n_rows, dtype=x.dtype, device=_dev.DEVICE)
+            return _spmv_device(M, x.contiguous(), y, ref_order, _pipe)
+        xd = x.to(M.d_pack.device, non_blocking=True).contiguous()
+        yd = torch.empty(M.n_rows, dtype=x.dtype, device=M.d_pack.device)
         _spmv_device(M, xd, yd, ref_order, _pipe)
         if out is None:
             out = torch.empty(M.n_rows, dtype=x.dtype, pin_memory=True)
+        elif out.is_cuda:
+            raise ValueError("out must be a host tensor for a host x")
         out.copy_(yd, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return out
     x = np.asarray(x)
+    if x.ndim != 1:
+        raise ValueError(f"x must be one-dimensional, got shape {x.shape}")
     if len(x) != M.n_cols:
         raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
     if x.dtype not in _dev.DT_CODE:

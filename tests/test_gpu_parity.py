@@ -347,3 +347,25 @@ def test_tile_tma_kernel_equals_pair_kernel(monkeypatch, kind, nx):
         res[tile] = (y.clone(), q.clone(), float(part.sum()))
     assert torch.equal(res["0"][0], res["1"][0]) and torch.equal(res["0"][1], res["1"][1])
     assert res["0"][2] == pytest.approx(res["1"][2], rel=1e-12)
+
+
+def test_spmv_argument_validation(rng):
+    """Bad x / out shapes, dtypes and devices raise instead of reading or writing out of bounds."""
+    import torch
+    rp, ci, v = random_csr_arrays(rng, 100, 90, 0.1)
+    M = P.build_packsell(P.CsrMatrix(100, 90, rp, ci, v), 32, 256, P.parse_format("fp16"), "implicit")
+    x = torch.rand(90, device="cuda")
+    with pytest.raises(ValueError):
+        P.packsell_spmv(M, torch.rand(91, device="cuda"))
+    with pytest.raises(ValueError):
+        P.packsell_spmv(M, torch.rand(90, 2, device="cuda"))
+    with pytest.raises(ValueError):
+        P.packsell_spmv(M, x, out=torch.empty(99, device="cuda"))
+    with pytest.raises(ValueError):
+        P.packsell_spmv(M, x, out=torch.empty(100, dtype=torch.float16, device="cuda"))
+    with pytest.raises(ValueError):
+        P.packsell_spmv(M, np.ones((90, 2), np.float32))
+    with pytest.raises(TypeError):
+        P.packsell_spmv(M, x.to(torch.int32))
+    xs = torch.rand(180, device="cuda")[::2]  # strided view: made contiguous, same result
+    assert torch.equal(P.packsell_spmv(M, xs), P.packsell_spmv(M, xs.contiguous()))
