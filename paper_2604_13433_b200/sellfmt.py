@@ -115,8 +115,8 @@ def sell_spmv(M: SellMatrix, x):
     if len(x) != M.n_cols:
         raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
     if on_dev:
-        xd = x
-        wd = _dev.T2NP[x.dtype]
+        xd = x.contiguous()
+        wd = _dev.T2NP.get(x.dtype)
     else:
         x = np.asarray(x)
         wd = x.dtype
