@@ -314,25 +314,26 @@ __device__ __forceinline__ const char* xbyte(const XT* x, uint32_t c2) {
   return reinterpret_cast<const char*>(x) + (size_t)c2 * (sizeof(XT) / 2);
 }
 
-// PSELL_GATHER_REAL_ONLY (build-time A/B, `make alt EXTRA=-DPSELL_GATHER_REAL_ONLY=1`):
-// predicate the x gather on the flag too, so dummy and padding words issue no
-// load.  Measured: power-law (config 4) 397 -> 367 us, but the stencils lose
-// 10-15 % (the predicated asm loads schedule worse), so it is off by default.
-#ifndef PSELL_GATHER_REAL_ONLY
-#define PSELL_GATHER_REAL_ONLY 0
-#endif
+// Gathers predicated on the flag (GR = true): dummy and padding words issue no
+// x load, they only move the cursor.  Used for irregular (segmented power-law)
+// matrices, whose dummy gathers land on scattered L2 sectors: config 4
+// 397 -> 367 us.  The stencils keep GR = false (their dummy gathers fall where
+// the next real gather goes anyway, and the predicated asm loads schedule worse
+// there: -10-15 %).
+template <bool GR>
 __device__ __forceinline__ unsigned short gather_u16(const void* p, uint32_t f) {
   unsigned short v;
-  if (PSELL_GATHER_REAL_ONLY)
+  if (GR)
     asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n mov.b16 %0, 0;\n @p ld.global.nc.u16 %0, [%2];\n}"
                  : "=h"(v) : "r"(f), "l"(p));
   else
     v = __ldg(reinterpret_cast<const unsigned short*>(p));
   return v;
 }
+template <bool GR>
 __device__ __forceinline__ float gather_f32(const void* p, uint32_t f) {
   float v;
-  if (PSELL_GATHER_REAL_ONLY)
+  if (GR)
     asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n mov.b32 %0, 0;\n @p ld.global.nc.f32 %0, [%2];\n}"
                  : "=f"(v) : "r"(f), "l"(p));
   else
@@ -340,48 +341,48 @@ __device__ __forceinline__ float gather_f32(const void* p, uint32_t f) {
   return v;
 }
 
-template <int CODEC, typename XT> struct FastStep;
+template <int CODEC, typename XT, bool GR = false> struct FastStep;
 
-template <> struct FastStep<PSELL_FP16, __half> {
+template <bool GR> struct FastStep<PSELL_FP16, __half, GR> {
   using Acc = float;
   __device__ static void run(uint32_t w, uint32_t& c2, const __half* x, float& acc, uint32_t, uint32_t) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? 0xFFFEu : 0xFFFFFFFEu);
-    const unsigned short xb = gather_u16(xbyte(x, c2), f);
+    const unsigned short xb = gather_u16<GR>(xbyte(x, c2), f);
     asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
         " @p fma.rn.f32.f16 %0, hi, %3, %0;\n}" : "+f"(acc) : "r"(f), "r"(w), "h"(xb));
   }
 };
-template <> struct FastStep<PSELL_FP16, float> {
+template <bool GR> struct FastStep<PSELL_FP16, float, GR> {
   using Acc = float;
   __device__ static void run(uint32_t w, uint32_t& c2, const float* x, float& acc, uint32_t, uint32_t) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? 0xFFFEu : 0xFFFFFFFEu);
-    const float xv = gather_f32(xbyte(x, c2), f);
+    const float xv = gather_f32<GR>(xbyte(x, c2), f);
     asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n .reg .f32 v;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
         " cvt.f32.f16 v, hi;\n @p fma.rn.f32 %0, v, %3, %0;\n}" : "+f"(acc) : "r"(f), "r"(w), "f"(xv));
   }
 };
-template <> struct FastStep<PSELL_E8MY, float> {
+template <bool GR> struct FastStep<PSELL_E8MY, float, GR> {
   using Acc = float;
   // m_real = 2^(D+1) - 2 (delta field << 1), vmask = ~(2^(D+1) - 1) (value bits)
   __device__ static void run(uint32_t w, uint32_t& c2, const float* x, float& acc, uint32_t m_real,
                              uint32_t vmask) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? m_real : 0xFFFFFFFEu);
-    const float xv = gather_f32(xbyte(x, c2), f);
+    const float xv = gather_f32<GR>(xbyte(x, c2), f);
     const float v = __uint_as_float(w & vmask);
     asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
         : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
   }
 };
-template <> struct FastStep<PSELL_E8MY, __half> {
+template <bool GR> struct FastStep<PSELL_E8MY, __half, GR> {
   using Acc = float;
   __device__ static void run(uint32_t w, uint32_t& c2, const __half* x, float& acc, uint32_t m_real,
                              uint32_t vmask) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? m_real : 0xFFFFFFFEu);
-    const float xv = __half2float(__ushort_as_half(gather_u16(xbyte(x, c2), f)));
+    const float xv = __half2float(__ushort_as_half(gather_u16<GR>(xbyte(x, c2), f)));
     const float v = __uint_as_float(w & vmask);
     asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
         : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
@@ -495,9 +496,9 @@ done:
 // chunks, so the two per-slice latency chains (offset -> words -> x -> y)
 // overlap inside one warp.  Aimed at narrow slices (7-point rows: ~9 steps),
 // where one slice per warp leaves the chain exposed.
-template <int CODEC, typename XT, bool DOT, int U>
+template <int CODEC, typename XT, bool DOT, int U, bool GR = false>
 __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) {
-  using S = FastStep<CODEC, XT>;
+  using S = FastStep<CODEC, XT, GR>;
   if constexpr (DOT) {
     if (a.skip && *a.skip) return;
   }
@@ -1245,7 +1246,7 @@ __global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const SpmvArgs a) 
   finish_dot<DOT>(a, dotv);
 }
 
-template <int CODEC, typename XT, bool REF, bool DOT>
+template <int CODEC, typename XT, bool REF, bool DOT, bool GR = false>
 static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
   if (a.c == 32) {
     const long long rows = a.n_slices * 32;
@@ -1273,7 +1274,7 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
           } else if (dual_slices(a.n_slices) && du == 12)
             spmv_dual_kernel<CODEC, XT, DOT, 12><<<gd, kBlock, 0, st>>>(a);
           else if (dual_slices(a.n_slices))
-            spmv_dual_kernel<CODEC, XT, DOT, 8><<<gd, kBlock, 0, st>>>(a);
+            spmv_dual_kernel<CODEC, XT, DOT, 8, GR><<<gd, kBlock, 0, st>>>(a);
           else if (nt == 64) spmv_fast_kernel<CODEC, XT, DOT, 8, 64><<<gnt, 64, 0, st>>>(a);
           else if (nt == 128) spmv_fast_kernel<CODEC, XT, DOT, 8, 128><<<gnt, 128, 0, st>>>(a);
           else spmv_fast_kernel<CODEC, XT, DOT, 8, 256><<<gnt, 256, 0, st>>>(a);
@@ -1475,7 +1476,7 @@ int psell_spmv_seg_checkpoints(const psell_desc* d, const void* pack, const int6
 namespace psell {
 template <int CODEC, typename XT>
 static void launch_segmented(const SpmvArgs& a, long long n_seg, long long n_long, cudaStream_t st) {
-  launch_spmv<CODEC, XT, false, false>(a, st);  // short slices (long ones are skipped)
+  launch_spmv<CODEC, XT, false, false, true>(a, st);  // short slices (long ones are skipped); flag-predicated gathers
   if (n_seg > 0)
     spmv_seg_kernel<CODEC, XT, 8><<<(unsigned)ceil_div(n_seg * 32, kBlock), kBlock, 0, st>>>(a, n_seg);
   if (n_long > 0)
