@@ -40,9 +40,10 @@ struct SpmvArgs {
   // long-slice segmentation (0 = off): slices wider than seg_len steps run as
   // segments (see spmv_seg_kernel)
   int seg_len;
-  // bulk L2 prefetch of the slice pair's words at warp start (dual kernel: 27-point
-  // 359 -> 325 us).  PSELL_L2PF=0 disables, =2 also prefetches the next pair in
-  // the persistent pair kernel (measured slower: 166 -> 187 us on 7-point).
+  // bulk L2 prefetch of each slice pair's words at warp start (dual kernel,
+  // non-persistent pair kernel: 27-point 359 -> 325 us).  PSELL_L2PF=0 disables
+  // (A/B).  Prefetching the next pair in the persistent pair kernel was measured
+  // slower (7-point 166 -> 180-187 us) and is not implemented.
   int l2pf;
   const int32_t* seg_slice;   // [n_seg] slice of each segment
   const int32_t* seg_q0;      // [n_seg] first step of each segment
@@ -748,7 +749,7 @@ __global__ void __launch_bounds__(kBlock) seg_prefix_kernel(const SpmvArgs a, lo
 
 template <int CODEC, typename XT, int U>
 __global__ void __launch_bounds__(kBlock, 6) spmv_seg_kernel(const SpmvArgs a, long long n_seg) {
-  using S = FastStep<CODEC, XT>;
+  using S = FastStep<CODEC, XT, true>;  // irregular rows: flag-predicated gathers
   const long long sg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (sg >= n_seg) return;
