@@ -420,10 +420,35 @@ def run_ours(args, cfg):
         # runs from its first stored column to its last
         touched = int(S.col_idx[-1].item()) - int(S.col_idx[0].item()) + 1 if S.nnz else 0
     nnz_local = S.nnz
-    del S
+    xt = getattr(torch, cfg["xdt"])
+    # vendor baseline on the same matrix (one GPU): cuSPARSE CSR SpMV through
+    # torch.sparse_csr_tensor @ x, CSR values in x's precision (the paper's cuCSR comparison)
+    vendor = None
+    if world == 1 and S.nnz < 2 ** 31 and not args.no_vendor:
+        try:
+            Acsr = torch.sparse_csr_tensor(S.row_ptr.to(torch.int32), S.col_idx, S.values.to(xt),
+                                           (S.n_rows, S.n_cols))
+            del S
+            torch.cuda.empty_cache()
+            xv = (torch.rand(Acsr.shape[1], device=dev) * 2 - 1).to(xt).unsqueeze(1)
+            for _ in range(3):
+                Acsr @ xv
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            v0.record()
+            for _ in range(20):
+                Acsr @ xv
+            v1.record()
+            torch.cuda.synchronize()
+            vendor = {"what": "cuSPARSE CSR SpMV via torch.sparse_csr_tensor @ x (values in x dtype), same matrix",
+                      "ms_per_step": v0.elapsed_time(v1) / 20}
+            del Acsr, xv
+        except Exception as e:  # noqa: BLE001
+            vendor = {"unavailable": repr(e)[:200]}
+    if "S" in locals():
+        del S
     torch.cuda.empty_cache()
 
-    xt = getattr(torch, cfg["xdt"])
     g = torch.Generator(device=dev)
     g.manual_seed(1234)
     x = (torch.rand(n, generator=g, device=dev, dtype=torch.float32) * 2 - 1).to(xt)
@@ -599,6 +624,8 @@ def run_ours(args, cfg):
                                       "api": "packsell_spmv(M, x_pinned_cpu, out=y_pinned_cpu), one blocking call per step"}},
             "gpu_launches": args.steps * launches_per_step,
             "variants_ms": {"register_pipeline (headline)": ms_local, "tma_bulk_stream": ms_regpipe},
+            "vendor_baseline": None if vendor is None else dict(
+                vendor, **({"speedup_packsell": vendor["ms_per_step"] / ms} if "ms_per_step" in vendor else {})),
             "clocks": clocks,
             "pcg": pcg,
         }
@@ -619,6 +646,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1048576, help="rows of the cpu_baseline sample (~10 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pcg", action="store_true", help="skip the config-5 PCG time-to-solution")
+    ap.add_argument("--no-vendor", action="store_true", help="skip the cuSPARSE CSR comparison")
     ap.add_argument("--pcg-nx", type=int, default=256)
     ap.add_argument("--pcg-m-in", type=int, default=50)
     ap.add_argument("--pcg-cpu-nx", type=int, default=32)
