@@ -1,0 +1,54 @@
+"""bench.py host logic on CPU: config table vs BASELINE.json, k_left formulas vs the oracle,
+partitions, the reference arm's CPU sample (oracle port) and its JSON contract."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import bench
+import oracle as O
+from paper_2604_13433_b200 import stencil
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_metric_matches_baseline_json():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        base = json.load(f)
+    assert bench.METRIC == base["metric"]
+    assert set(bench.CONFIGS) == {"c1", "c2", "c3", "c4"}
+
+
+@pytest.mark.parametrize("kind,nx", [("stencil27", 8), ("poisson3d", 8), ("poisson2d", 16)])
+def test_stencil_k_left_matches_oracle(kind, nx):
+    A = {"stencil27": stencil.stencil27, "poisson3d": stencil.poisson3d, "poisson2d": stencil.poisson2d}[kind](nx)
+    assert bench.stencil_k_left(kind, nx) == O.lower_bandwidth(A.row_ptr, A.col_idx)
+
+
+def test_partitions_cover_rows():
+    for key in ("c1", "c2", "c3"):
+        cfg = bench.CONFIGS[key]
+        n = bench.cfg_rows(cfg)
+        for world in (1, 2, 8):
+            slabs = bench.partition(cfg, world)
+            assert slabs[0][0] == 0 and slabs[-1][1] == n
+            assert all(b == c for (_, b), (c, _) in zip(slabs, slabs[1:]))
+            assert all(a % cfg["sigma"] == 0 for a, _ in slabs)
+
+
+def test_reference_arm_sample_runs(capsys):
+    """The CPU reference arm (oracle port) on a tiny sample prints the contract's JSON line."""
+    cfg = dict(bench.CONFIGS["c1"])
+
+    class A:
+        gpus, steps, warmup, ref_rows = 1, 1, 0, 4096
+    os.environ.pop("RANK", None)
+    r = bench.cpu_reference(cfg, 2, 4096, 1, 0)
+    assert r["gbs"] > 0 and r["workers"] == 2 and r["nnz"] > 0
+    bench.run_reference(A, cfg)
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["metric"] == bench.METRIC and line["higher_is_better"] is True
