@@ -7,6 +7,8 @@ side; the kernels only ever see raw pointers.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -37,15 +39,64 @@ def torch_dtype(np_dtype) -> torch.dtype:
 _PINNED_MIN = 4 << 20  # results from 4 MiB up land in page-locked memory
 
 
-def upload(a: np.ndarray, device=None) -> torch.Tensor:
+_CHUNK_MIN = int(os.environ.get("PSELL_H2D_CHUNK", str(1 << 20)))  # host-copy / DMA granule (bytes)
+_UPLOAD_THREADED_MIN = 16 << 20  # below this the pageable copy is as fast (scripts/upload_sweep.py)
+_pool = None
+
+
+def _copy_pool():
+    global _pool
+    if _pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        nt = int(os.environ.get("PSELL_H2D_THREADS", "4"))
+        _pool = ThreadPoolExecutor(max_workers=max(1, min(nt, os.cpu_count() or 1)), thread_name_prefix="psell-h2d")
+    return _pool
+
+
+def upload(a: np.ndarray, device=None, out: torch.Tensor = None) -> torch.Tensor:
     """Copy a host array to the device (unsigned types as same-width signed).
-    (Pageable H2D measured faster than staging through pinned memory: 1.8 vs 2.7 ms
-    for 33.5 MB, the driver pipelines its own bounce buffer.)"""
+
+    From 16 MiB up the array is copied into a page-locked block of torch's
+    caching host allocator by 4 threads (numpy releases the GIL for the copy),
+    chunks of max(1 MiB, size / 32), each chunk's DMA queued as soon as its
+    host copy lands.  A single-threaded copy (the driver's pageable bounce
+    buffer or one staging memcpy) runs at ~12 GB/s on the B200 hosts, a
+    quarter of PCIe: 134 MB 11.4 ms pageable vs 4.9 ms, 33.5 MB 1.6 vs 1.2 ms
+    (profiles/r01/upload_sweep.txt; 8 or 16 threads were no faster).  The pinned block returns to the cache when
+    its DMA has completed (the allocator records the copy's stream event), so
+    the call does not synchronise the device; `a` is no longer read on return.
+    """
     a = np.ascontiguousarray(a)
     s = _SIGNED.get(a.dtype)
     if s is not None:
         a = a.view(s)
-    return torch.from_numpy(a).to(device or DEVICE)
+    dev = device or DEVICE
+    if a.nbytes < _UPLOAD_THREADED_MIN or not torch.cuda.is_available():
+        t = torch.from_numpy(a).to(dev)
+        if out is None:
+            return t
+        out.copy_(t.view(out.shape))
+        return out
+    if out is None:
+        out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    if dst.numel() != src.size:
+        raise ValueError(f"upload: out has {dst.numel()} bytes, array {src.size}")
+    h = torch.empty(src.size, dtype=torch.uint8, pin_memory=True)
+    hn = h.numpy()
+
+    ck = max(_CHUNK_MIN, -(-src.size // 32) + 4095 & ~4095)
+
+    def fill(off):
+        hn[off:off + ck] = src[off:off + ck]
+
+    offs = range(0, src.size, ck)
+    futs = [_copy_pool().submit(fill, off) for off in offs]
+    for off, f in zip(offs, futs):
+        f.result()
+        dst[off:off + ck].copy_(h[off:off + ck], non_blocking=True)
+    return out
 
 
 def download(t: torch.Tensor, np_dtype) -> np.ndarray:
@@ -63,75 +114,6 @@ def download(t: torch.Tensor, np_dtype) -> np.ndarray:
     else:
         h = t.cpu().numpy()
     return h.view(np.dtype(np_dtype)) if h.dtype != np.dtype(np_dtype) else h
-
-
-_STAGE_BYTES = 16 << 20  # two 16 MiB page-locked halves, allocated once per process
-_stage = None
-
-
-def _staging():
-    global _stage
-    if _stage is None:
-        buf = torch.empty(2 * _STAGE_BYTES, dtype=torch.uint8, pin_memory=True)
-        _stage = (buf, [torch.cuda.Event(), torch.cuda.Event()])
-    return _stage
-
-
-def upload_pinned(a: np.ndarray, device=None, out: torch.Tensor = None) -> torch.Tensor:
-    """Host array -> device through a reused double-buffered page-locked stage.
-
-    Large solver vectors (134 MB at 256^3) would otherwise go through the
-    driver's pageable bounce buffer or a fresh cudaHostAlloc per call; the host
-    memcpy into one half overlaps the DMA of the other."""
-    a = np.ascontiguousarray(a)
-    s = _SIGNED.get(a.dtype)
-    if s is not None:
-        a = a.view(s)
-    if out is None:
-        out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=device or DEVICE)
-    src = a.reshape(-1).view(np.uint8)
-    dst = out.view(-1).view(torch.uint8)
-    buf, ev = _staging()
-    st = torch.cuda.current_stream()
-    for k, off in enumerate(range(0, src.size, _STAGE_BYTES)):
-        h = k & 1
-        m = min(_STAGE_BYTES, src.size - off)
-        ev[h].synchronize()  # the DMA that last read this half is done
-        half = buf[h * _STAGE_BYTES:h * _STAGE_BYTES + m]
-        half.numpy()[...] = src[off:off + m]
-        dst[off:off + m].copy_(half, non_blocking=True)
-        ev[h].record(st)
-    st.synchronize()
-    return out
-
-
-def download_pinned(t: torch.Tensor) -> np.ndarray:
-    """Device tensor -> new numpy array through the reused page-locked stage (double buffered)."""
-    t = t.contiguous()
-    np_dt = t.cpu().numpy().dtype if t.numel() == 0 else None
-    out = np.empty(t.numel() * t.element_size(), dtype=np.uint8)
-    src = t.view(-1).view(torch.uint8)
-    buf, ev = _staging()
-    st = torch.cuda.current_stream()
-    chunks = list(range(0, out.size, _STAGE_BYTES))
-    for k, off in enumerate(chunks):  # D2H of chunk k overlaps the host copy of chunk k-1
-        h = k & 1
-        m = min(_STAGE_BYTES, out.size - off)
-        buf[h * _STAGE_BYTES:h * _STAGE_BYTES + m].copy_(src[off:off + m], non_blocking=True)
-        ev[h].record(st)
-        if k:
-            pk, po = (k - 1) & 1, chunks[k - 1]
-            pm = min(_STAGE_BYTES, out.size - po)
-            ev[pk].synchronize()
-            out[po:po + pm] = buf[pk * _STAGE_BYTES:pk * _STAGE_BYTES + pm].numpy()
-    if chunks:
-        k = len(chunks) - 1
-        h, po = k & 1, chunks[k]
-        pm = min(_STAGE_BYTES, out.size - po)
-        ev[h].synchronize()
-        out[po:po + pm] = buf[h * _STAGE_BYTES:h * _STAGE_BYTES + pm].numpy()
-    dt = np_dt if np_dt is not None else T2NP_ALL[t.dtype]
-    return out.view(dt).reshape(tuple(t.shape))
 
 
 def empty(n: int, np_dtype, device=None) -> torch.Tensor:

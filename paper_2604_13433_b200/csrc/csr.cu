@@ -9,6 +9,9 @@
 // warp's col/value reads cover one contiguous span served by L1.
 #include "psell_internal.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace psell {
 
 template <typename XT> struct CsrOps;
@@ -56,9 +59,12 @@ __global__ void __launch_bounds__(kBlock) csr_spmv_kernel(long long n, const int
 // reference's sequential rounding order (bitwise equal to the thread-per-row
 // kernel) while HBM sees unit-stride streams instead of 256 interleaved rows.
 constexpr int kTile = 2048;  // 2048 x (4 + 8) B = 24 KB of shared memory
+#ifndef PSELL_CSR_MINB
+#define PSELL_CSR_MINB 4
+#endif
 
 template <typename XT>
-__global__ void __launch_bounds__(kBlock, 4) csr_spmv_tiled_kernel(long long n, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kBlock, PSELL_CSR_MINB) csr_spmv_tiled_kernel(long long n, const int64_t* __restrict__ row_ptr,
                                                                 const int32_t* __restrict__ col_idx,
                                                                 const double* __restrict__ values,
                                                                 const XT* __restrict__ x, XT* __restrict__ y) {
@@ -104,6 +110,120 @@ __global__ void __launch_bounds__(kBlock, 4) csr_spmv_tiled_kernel(long long n, 
   if (i < n) y[i] = acc;
 }
 
+// Pipelined variant (default): persistent CTAs (4 per SM) walk 256-row blocks
+// grid-stride; block k+1's col/value span is copied into the second half of a
+// double-buffered shared-memory stage with cp.async (no registers held) while
+// block k is computed, and block k+2's row_ptr bounds are loaded a block ahead.
+// Blocks whose span exceeds one stage fall back to the synchronous tile loop
+// in their own (idle) stage.  Same per-row order as the kernels above.
+constexpr int kPTile = 2048;  // entries per stage; 2 stages x 2048 x 12 B = 48 KB
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+struct CsrBounds {
+  long long s0, s1, rb, re;
+};
+
+template <typename XT>
+__global__ void __launch_bounds__(kBlock, 4) csr_spmv_pipe_kernel(long long n, long long nb,
+                                                               const int64_t* __restrict__ row_ptr,
+                                                               const int32_t* __restrict__ col_idx,
+                                                               const double* __restrict__ values,
+                                                               const XT* __restrict__ x, XT* __restrict__ y) {
+  using O = CsrOps<XT>;
+  __shared__ int32_t sc[2][kPTile];
+  __shared__ double sv[2][kPTile];
+  const int t = threadIdx.x;
+  auto bounds = [&](long long blk) {
+    CsrBounds b;
+    const long long r0 = blk * kBlock;
+    const long long r1 = r0 + kBlock < n ? r0 + kBlock : n;
+    b.s0 = row_ptr[r0];
+    b.s1 = row_ptr[r1];
+    b.rb = b.re = 0;
+    if (r0 + t < n) {
+      b.rb = row_ptr[r0 + t];
+      b.re = row_ptr[r0 + t + 1];
+    }
+    return b;
+  };
+  auto issue = [&](int buf, const CsrBounds& b) {
+    const int m = (int)(b.s1 - b.s0);
+    if (m <= kPTile) {
+      for (int k = t; k < m; k += kBlock) {
+        cp_async4(&sc[buf][k], col_idx + b.s0 + k);
+        cp_async8(&sv[buf][k], values + b.s0 + k);
+      }
+    }
+    cp_async_commit();
+  };
+  // the row's entries [a, e) of a tile, left to right, 8 gathers in flight
+  auto walk = [&](const int32_t* tc, const double* tv, int a, int e, XT& acc, bool& started) {
+    for (int j = a; j < e; j += 8) {
+      XT xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = (j + u < e) ? x[tc[j + u]] : O::zero();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j + u < e) {
+          const XT prod = O::mul(O::cv(tv[j + u]), xv[u]);
+          acc = started ? O::add(acc, prod) : prod;
+          started = true;
+        }
+      }
+    }
+  };
+  long long blk = blockIdx.x;
+  if (blk >= nb) return;
+  CsrBounds cur = bounds(blk);
+  issue(0, cur);
+  CsrBounds nxt = cur;
+  if (blk + gridDim.x < nb) nxt = bounds(blk + gridDim.x);
+  int buf = 0;
+  for (;;) {
+    const long long bn = blk + gridDim.x;
+    if (bn < nb) issue(buf ^ 1, nxt);
+    else cp_async_commit();
+    CsrBounds nn = nxt;
+    if (bn + gridDim.x < nb) nn = bounds(bn + gridDim.x);
+    cp_async_wait1();
+    __syncthreads();
+    XT acc = O::zero();
+    bool started = false;
+    const int m = (int)(cur.s1 - cur.s0);
+    if (m <= kPTile) {
+      walk(sc[buf], sv[buf], (int)(cur.rb - cur.s0), (int)(cur.re - cur.s0), acc, started);
+    } else {  // long rows: synchronous tiles through this block's (unused) stage
+      for (long long t0 = cur.s0; t0 < cur.s1; t0 += kPTile) {
+        const int mt = (int)(cur.s1 - t0 < kPTile ? cur.s1 - t0 : kPTile);
+        __syncthreads();
+        for (int k = t; k < mt; k += kBlock) {
+          sc[buf][k] = __ldcs(col_idx + t0 + k);
+          sv[buf][k] = __ldcs(values + t0 + k);
+        }
+        __syncthreads();
+        const int a = (int)((cur.rb > t0 ? cur.rb : t0) - t0);
+        const int e = (int)((cur.re < t0 + mt ? cur.re : t0 + mt) - t0);
+        walk(sc[buf], sv[buf], a, e, acc, started);
+      }
+    }
+    if (blk * kBlock + t < n) y[blk * kBlock + t] = acc;
+    __syncthreads();  // this stage is refilled by the next iteration's issue
+    if (bn >= nb) break;
+    blk = bn;
+    cur = nxt;
+    nxt = nn;
+    buf ^= 1;
+  }
+}
+
 }  // namespace psell
 
 using namespace psell;
@@ -114,6 +234,40 @@ extern "C" int psell_csr_spmv(int64_t n_rows, const int64_t* row_ptr, const int3
   if (n_rows <= 0) return ok(err);
   const unsigned grid = (unsigned)ceil_div(n_rows, kBlock);
   cudaStream_t st = as_stream(stream);
+  static int pipe = -1;  // PSELL_CSR=tiled selects the non-pipelined kernel (A/B)
+  if (pipe < 0) {
+    const char* e = getenv("PSELL_CSR");
+    pipe = !(e && strcmp(e, "tiled") == 0);
+  }
+  if (pipe) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const long long nb = ceil_div(n_rows, kBlock);
+    const unsigned pg = (unsigned)(nb < 4LL * sms ? nb : 4LL * sms);
+    switch (x_dtype) {
+      case PSELL_DT_F64:
+        csr_spmv_pipe_kernel<double><<<pg, kBlock, 0, st>>>(n_rows, nb, row_ptr, col_idx, values,
+                                                            static_cast<const double*>(x), static_cast<double*>(y));
+        break;
+      case PSELL_DT_F32:
+        csr_spmv_pipe_kernel<float><<<pg, kBlock, 0, st>>>(n_rows, nb, row_ptr, col_idx, values,
+                                                           static_cast<const float*>(x), static_cast<float*>(y));
+        break;
+      case PSELL_DT_F16:
+        csr_spmv_pipe_kernel<__half><<<pg, kBlock, 0, st>>>(n_rows, nb, row_ptr, col_idx, values,
+                                                            static_cast<const __half*>(x), static_cast<__half*>(y));
+        break;
+      default:
+        return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "unsupported x dtype");
+    }
+    PSELL_CHECK_LAUNCH(err, "psell_csr_spmv");
+    return ok(err);
+  }
   switch (x_dtype) {
     case PSELL_DT_F64:
       csr_spmv_tiled_kernel<double><<<grid, kBlock, 0, st>>>(n_rows, row_ptr, col_idx, values,

@@ -17,6 +17,13 @@ namespace psell {
 
 constexpr int kRB = PSELL_RED_BLOCKS;
 
+// grid-stride loops of the f64 vector kernels: 4 trips unrolled so each thread
+// has 4 independent loads per vector in flight (the per-thread summation order,
+// hence every result bit, is unchanged)
+#ifndef PSELL_GS_UNROLL
+#define PSELL_GS_UNROLL _Pragma("unroll 4")
+#endif
+
 __global__ void __launch_bounds__(1024) sum_partials_kernel(const double* __restrict__ parts,
                                                             long long np, int n_out,
                                                             double* __restrict__ out,
@@ -42,6 +49,7 @@ __global__ void __launch_bounds__(kBlock) dot_kernel(const T* __restrict__ a, co
                                                      long long n, double* __restrict__ parts) {
   __shared__ double sh[kBlock / 32];
   double v = 0.0;
+  PSELL_GS_UNROLL
   for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock)
     v += (double)a[i] * (double)b[i];
   v = block_sum<kBlock>(v, sh);
@@ -169,9 +177,7 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
   long long done = 0;
   if (VEC) {
     const long long n4 = n >> 2;
-    for (long long i4 = gt; i4 < n4; i4 += gs) {
-      float4 rv = reinterpret_cast<float4*>(r)[i4];
-      const float4 qv = reinterpret_cast<const float4*>(q)[i4];
+    auto step = [&](long long i4, float4 rv, const float4 qv) {
       float4 zv;
       const long long i = i4 * 4;
       if (x) {
@@ -194,7 +200,21 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
       v += (double)rv.y * (double)zv.y;
       v += (double)rv.z * (double)zv.z;
       v += (double)rv.w * (double)zv.w;
+    };
+    long long i4 = gt;
+    // two grid-stride elements per trip, all four loads issued first (same
+    // per-thread order of the dot sum as one element per trip)
+#ifndef PSELL_UPD_U1
+    for (; i4 + gs < n4; i4 += 2 * gs) {
+      const float4 r0 = reinterpret_cast<float4*>(r)[i4];
+      const float4 q0 = reinterpret_cast<const float4*>(q)[i4];
+      const float4 r1 = reinterpret_cast<float4*>(r)[i4 + gs];
+      const float4 q1 = reinterpret_cast<const float4*>(q)[i4 + gs];
+      step(i4, r0, q0);
+      step(i4 + gs, r1, q1);
     }
+#endif
+    for (; i4 < n4; i4 += gs) step(i4, reinterpret_cast<float4*>(r)[i4], reinterpret_cast<const float4*>(q)[i4]);
     done = n4 * 4;
   }
   for (long long i = done + gt; i < n; i += gs) {
@@ -269,6 +289,7 @@ __global__ void __launch_bounds__(kBlock) fcg_zr_kernel(long long n, const doubl
                                                         double* __restrict__ parts) {
   __shared__ double sh[kBlock / 32];
   double v0 = 0.0, v1 = 0.0;
+  PSELL_GS_UNROLL
   for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
     const double zi = z[i], ri = r[i];
     if (rp) v0 += __dmul_rn(zi, __dsub_rn(ri, rp[i]));
@@ -289,6 +310,7 @@ __global__ void __launch_bounds__(kBlock) pq_pr_kernel(long long n, const double
                                                        double* __restrict__ parts) {
   __shared__ double sh[kBlock / 32];
   double v0 = 0.0, v1 = 0.0;
+  PSELL_GS_UNROLL
   for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
     const double pi = p[i];
     v0 += __dmul_rn(pi, q[i]);
@@ -314,7 +336,28 @@ __global__ void __launch_bounds__(kBlock) axpy2_kernel(long long n, double* __re
   __shared__ double sh[kBlock / 32];
   const double a = coef[0];
   double v = 0.0;
-  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
+  const long long gs = (long long)kRB * kBlock;
+  long long i = (long long)blockIdx.x * kBlock + threadIdx.x;
+  // 4 trips per pass with every load issued before the first store (the
+  // compiler would otherwise re-order nothing across the x / r stores)
+  for (; i + 3 * gs < n; i += 4 * gs) {
+    double xv[4], rv[4], pv[4], qv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xv[u] = x[i + u * gs];
+      rv[u] = r[i + u * gs];
+      pv[u] = p[i + u * gs];
+      qv[u] = q[i + u * gs];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[i + u * gs] = __dadd_rn(xv[u], __dmul_rn(a, pv[u]));
+      const double rn = __dsub_rn(rv[u], __dmul_rn(a, qv[u]));
+      r[i + u * gs] = rn;
+      v += __dmul_rn(rn, rn);
+    }
+  }
+  for (; i < n; i += gs) {
     x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
     const double rn = __dsub_rn(r[i], __dmul_rn(a, q[i]));
     r[i] = rn;
@@ -340,6 +383,7 @@ __global__ void __launch_bounds__(kBlock) resid_kernel(long long n, const double
                                                        double* __restrict__ parts) {
   __shared__ double sh[kBlock / 32];
   double v = 0.0;
+  PSELL_GS_UNROLL
   for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
     const double d = __dsub_rn(b[i], ax[i]);
     v += __dmul_rn(d, d);
@@ -355,6 +399,7 @@ __global__ void __launch_bounds__(kBlock) precond_dot_kernel(long long n, double
                                                              double* __restrict__ parts) {
   __shared__ double sh[kBlock / 32];
   double v = 0.0;
+  PSELL_GS_UNROLL
   for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long long)kRB * kBlock) {
     const double ri = r[i];
     const double zi = inv ? __dmul_rn(ri, inv[i]) : ri;

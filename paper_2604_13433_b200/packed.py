@@ -469,7 +469,7 @@ def _decoded_row_lengths(M: PackSellMatrix) -> np.ndarray:
                                _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr), ctypes.byref(nnz),
                                _lib.stream_handle(), err)
     _lib.check(rc, err, M.fmt)
-    return np.diff(_dev.download_pinned(row_ptr))
+    return np.diff(_dev.download(row_ptr, np.int64))
 
 
 def _to_csr_device(M: PackSellMatrix):

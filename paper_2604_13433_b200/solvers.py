@@ -103,14 +103,22 @@ class SpmvBackend:
     the global vector and the result has the slab's rows.
     """
 
-    def __init__(self, name: str, matrix, kernel: Callable, source):
+    def __init__(self, name: str, matrix, kernel: Callable, source, kernel_into: Callable = None):
         self.name = name
         self.matrix = matrix
         self._kernel = kernel
+        self._into = kernel_into
         self.source = source
 
     def apply(self, x):
         return self._kernel(x)
+
+    def apply_into(self, x, out):
+        """out <- A x for device tensors (no temporary when the backend writes in place)."""
+        if self._into is not None:
+            return self._into(x, out)
+        out.copy_(self._kernel(x))
+        return out
 
     @property
     def is_packsell(self) -> bool:
@@ -124,7 +132,8 @@ def make_backend(A, name: str, c: int = 32, sigma: int = 256, mode: str = "impli
     `k_left` passes the global lower bandwidth when A is one rank's slab.
     """
     if name == "csr64":
-        return SpmvBackend(name, A, lambda x: csr_spmv(A, x, _dtype_of(x)), A)
+        return SpmvBackend(name, A, lambda x: csr_spmv(A, x, _dtype_of(x)), A,
+                           lambda x, out: csr_spmv(A, x, _dtype_of(x), out=out))
     if name in ("sell64", "sell32", "sell16"):
         from .sellfmt import build_sell, sell_spmv
         dt = {"sell64": np.float64, "sell32": np.float32, "sell16": np.float16}[name]
@@ -133,7 +142,7 @@ def make_backend(A, name: str, c: int = 32, sigma: int = 256, mode: str = "impli
     if name.startswith("packsell-"):
         fmt = codec.parse_format(name[len("packsell-"):])
         M = build_packsell(A, c, sigma, fmt, mode, _k_left_override=k_left)
-        return SpmvBackend(name, M, lambda x: packsell_spmv(M, x), A)
+        return SpmvBackend(name, M, lambda x: packsell_spmv(M, x), A, lambda x, out: packsell_spmv(M, x, out=out))
     raise ValueError(f"unknown backend {name!r}")
 
 
@@ -488,12 +497,10 @@ class _Outer:
     def apply(self, v, out):
         """out <- A v (v local slab; all-gathered to the global vector first)."""
         if self.G == 1:
-            out.copy_(self.backend.apply(v))
-            return out
+            return self.backend.apply_into(v, out)
         self.slab_of_full().copy_(v)
         _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
-        out.copy_(self.backend.apply(self.full))
-        return out
+        return self.backend.apply_into(self.full, out)
 
     def audit(self, report: SolveReport, x, bnorm, tol) -> SolveReport:
         """True residual in f64 on the device, demote drifted runs (solvers.py:152-168)."""
@@ -504,11 +511,11 @@ class _Outer:
         ax = self.vec()
         src = self.backend.source
         if self.G == 1:
-            ax.copy_(csr_spmv(src, x, np.float64))
+            csr_spmv(src, x, np.float64, out=ax)
         else:
             self.slab_of_full().copy_(x)
             _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
-            ax.copy_(csr_spmv(src, self.full, np.float64))
+            csr_spmv(src, self.full, np.float64, out=ax)
         self.lib.psell_resid(self.n, self.b.data_ptr(), ax.data_ptr(), d.p(d.partials), d.p(d.loc, 6), d.st())
         d.reduce(6, 1, 14)
         report.final_true_relres = float(np.sqrt(float(d.scal[14].item()))) / bnorm
@@ -584,7 +591,7 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
     torch.cuda.synchronize()
     report = SolveReport(converged, it, 0, history, 0.0, time.perf_counter() - t0, reason)
     report = o.audit(report, x, bnorm, cfg.tol)
-    report.x = _dev_mod().download_pinned(x)
+    report.x = _dev_mod().download(x, np.float64)
     return report
 
 
@@ -664,7 +671,7 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
     torch.cuda.synchronize()
     report = SolveReport(converged, it, inner_total, history, 0.0, time.perf_counter() - t0, reason)
     report = o.audit(report, x, bnorm, cfg.tol)
-    report.x = _dev_mod().download_pinned(x)
+    report.x = _dev_mod().download(x, np.float64)
     return report
 
 

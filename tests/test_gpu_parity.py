@@ -92,6 +92,24 @@ def test_csr_spmv_bitwise(golden_build):
             assert np.array_equal(_bits(y), _bits(z[f"c{i}_csr_{np.dtype(dt).name}"])), (i, dt)
 
 
+def test_csr_spmv_pipelined_bitwise_large():
+    """K4's persistent path at a size with many more 256-row blocks than resident
+    CTAs (each shared-memory stage refilled ~200 times), empty rows, and blocks
+    whose entries exceed one stage (the synchronous fallback): bitwise vs the oracle."""
+    rng = np.random.default_rng(7)
+    n = 300_000
+    lens = rng.integers(0, 12, n)
+    lens[rng.integers(0, n, 200)] = rng.integers(300, 3000, 200)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = rng.integers(0, n, int(rp[-1])).astype(np.int32)
+    v = rng.standard_normal(int(rp[-1]))
+    A = P.CsrMatrix(n, n, rp, ci, v)
+    for dt in (np.float32, np.float64):
+        x = rng.standard_normal(n).astype(dt)
+        y = P.csr_spmv(A, x, dt)
+        assert np.array_equal(_bits(y), _bits(O.csr_spmv(rp, ci, v, x, dt))), dt
+
+
 def test_errors_match_reference(golden_errors):
     def check(name, fn):
         g = golden_errors[name]
