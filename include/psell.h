@@ -209,6 +209,15 @@ PSELL_API int psell_csr_spmv(int64_t n_rows, const int64_t* row_ptr, const int32
                    const double* values, const void* x, int32_t x_dtype, void* y, void* stream,
                    psell_error* err);
 
+/* psell_csr_spmv in f64 fused with the PCG's p.q (solvers.py:197-198):
+ * y = A x (bitwise as psell_csr_spmv) and out1[0] = sum_i p_own[i] * y[i] over
+ * the slab's rows (p_own = this rank's slab of x), summed per CTA of the
+ * persistent grid in row order, then over CTAs in a fixed tree (deterministic).
+ * partials: >= 4 * SM count doubles. */
+PSELL_API int psell_csr_spmv_dot(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                       const double* values, const double* x, double* y, const double* p_own,
+                       double* partials, double* out1, void* stream, psell_error* err);
+
 /* ---- K3: solver vector kernels (solvers.py:87-93,171-308) ----
  * Reductions are deterministic: fixed-grid partials summed in a fixed tree.
  * Device scalar blocks (double* scal, int32_t* iflags) are described in

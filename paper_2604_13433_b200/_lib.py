@@ -70,6 +70,7 @@ _SIGS = {
     "psell_pack_words": (c_int32, [_D, _P, _P, _P, c_int64, _P, _P, _E]),
     "psell_unpack_words": (c_int32, [_D, _P, c_int64, _P, _P, _P, _P, _E]),
     "psell_csr_spmv": (c_int32, [c_int64, _P, _P, _P, _P, c_int32, _P, _P, _E]),
+    "psell_csr_spmv_dot": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _E]),
     "psell_halo_pack": (c_int32, [c_int64, _P, _P, _P, c_int32, _P]),
     "psell_halo_unpack": (c_int32, [c_int64, _P, _P, _P, c_int32, _P]),
     "psell_backward_error": (c_int32, [c_int64, c_int64, _P, _P, _P, _P, c_int32, _P, c_int32, _P, _P, _E]),

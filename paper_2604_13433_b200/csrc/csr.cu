@@ -131,13 +131,16 @@ struct CsrBounds {
   long long s0, s1, rb, re;
 };
 
-template <typename XT>
+template <typename XT, bool DOT = false>
 __global__ void __launch_bounds__(kBlock, 4) csr_spmv_pipe_kernel(long long n, long long nb,
                                                                const int64_t* __restrict__ row_ptr,
                                                                const int32_t* __restrict__ col_idx,
                                                                const double* __restrict__ values,
-                                                               const XT* __restrict__ x, XT* __restrict__ y) {
+                                                               const XT* __restrict__ x, XT* __restrict__ y,
+                                                               const double* __restrict__ p_own = nullptr,
+                                                               double* __restrict__ parts = nullptr) {
   using O = CsrOps<XT>;
+  double dotv = 0.0;  // DOT: this thread's rows of p_own . y, in row order
   __shared__ int32_t sc[2][kPTile];
   __shared__ double sv[2][kPTile];
   const int t = threadIdx.x;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(kBlock, 4) csr_spmv_pipe_kernel(long long n, l
     }
   };
   long long blk = blockIdx.x;
-  if (blk >= nb) return;
+  if (blk >= nb) return;  // (grid <= nb: every CTA has a block)
   CsrBounds cur = bounds(blk);
   issue(0, cur);
   CsrBounds nxt = cur;
@@ -214,7 +217,10 @@ __global__ void __launch_bounds__(kBlock, 4) csr_spmv_pipe_kernel(long long n, l
         walk(sc[buf], sv[buf], a, e, acc, started);
       }
     }
-    if (blk * kBlock + t < n) y[blk * kBlock + t] = acc;
+    if (blk * kBlock + t < n) {
+      y[blk * kBlock + t] = acc;
+      if constexpr (DOT) dotv += __dmul_rn(p_own[blk * kBlock + t], (double)acc);
+    }
     __syncthreads();  // this stage is refilled by the next iteration's issue
     if (bn >= nb) break;
     blk = bn;
@@ -222,11 +228,52 @@ __global__ void __launch_bounds__(kBlock, 4) csr_spmv_pipe_kernel(long long n, l
     nxt = nn;
     buf ^= 1;
   }
+  if constexpr (DOT) {  // the stages are idle now (last iteration ended on a barrier)
+    const double tsum = block_sum<kBlock>(dotv, sv[0]);
+    if (t == 0) parts[blockIdx.x] = tsum;
+  }
+}
+
+__global__ void __launch_bounds__(1024) csr_dot_finalize_kernel(const double* __restrict__ parts, int np,
+                                                                double* __restrict__ out) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < np; i += 1024) v += parts[i];
+  const double tsum = block_sum<1024>(v, sh);
+  if (threadIdx.x == 0) out[0] = tsum;
 }
 
 }  // namespace psell
 
 using namespace psell;
+
+static unsigned csr_pipe_grid(long long nb) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return (unsigned)(nb < 4LL * sms ? nb : 4LL * sms);
+}
+
+extern "C" int psell_csr_spmv_dot(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                                  const double* values, const double* x, double* y, const double* p_own,
+                                  double* partials, double* out1, void* stream, psell_error* err) {
+  cudaStream_t st = as_stream(stream);
+  if (n_rows <= 0) {
+    cudaMemsetAsync(out1, 0, sizeof(double), st);
+    return ok(err);
+  }
+  const long long nb = ceil_div(n_rows, kBlock);
+  const unsigned pg = csr_pipe_grid(nb);
+  csr_spmv_pipe_kernel<double, true><<<pg, kBlock, 0, st>>>(n_rows, nb, row_ptr, col_idx, values, x, y, p_own,
+                                                            partials);
+  csr_dot_finalize_kernel<<<1, 1024, 0, st>>>(partials, (int)pg, out1);
+  PSELL_CHECK_LAUNCH(err, "psell_csr_spmv_dot");
+  return ok(err);
+}
 
 extern "C" int psell_csr_spmv(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
                               const double* values, const void* x, int32_t x_dtype, void* y,
@@ -240,15 +287,8 @@ extern "C" int psell_csr_spmv(int64_t n_rows, const int64_t* row_ptr, const int3
     pipe = !(e && strcmp(e, "tiled") == 0);
   }
   if (pipe) {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (sms <= 0) sms = 148;
-    }
     const long long nb = ceil_div(n_rows, kBlock);
-    const unsigned pg = (unsigned)(nb < 4LL * sms ? nb : 4LL * sms);
+    const unsigned pg = csr_pipe_grid(nb);
     switch (x_dtype) {
       case PSELL_DT_F64:
         csr_spmv_pipe_kernel<double><<<pg, kBlock, 0, st>>>(n_rows, nb, row_ptr, col_idx, values,

@@ -210,6 +210,19 @@ class _Dev:
         g, stride = self.gather()
         self.lib.psell_sum_strided(self.p(g, k0), self.G, stride, n_out, self.p(self.scal, dst), self.st())
 
+    def status(self, i: int, j: int):
+        """(flags[0], scal[i], scal[j]) on the host: two small D2H copies into page-locked
+        buffers and one stream sync (no gather kernels on the per-iteration path)."""
+        torch = self.torch
+        if not hasattr(self, "_h_scal"):
+            self._h_scal = torch.zeros(32, dtype=torch.float64, pin_memory=True)
+            self._h_flags = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        self._h_scal.copy_(self.scal, non_blocking=True)
+        self._h_flags.copy_(self.flags, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        hs = self._h_scal.numpy()
+        return int(self._h_flags[0]), float(hs[i]), float(hs[j])
+
     def norm(self, a, slot: int = 15) -> float:
         """sqrt of the global a.a (solvers.py:92-93)."""
         self.lib.psell_dot(a.data_ptr(), a.data_ptr(), 2 if a.dtype == self.torch.float64 else 1, a.numel(),
@@ -502,6 +515,24 @@ class _Outer:
         _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
         return self.backend.apply_into(self.full, out)
 
+    def apply_pq(self, p, q, slot: int) -> bool:
+        """q <- A p and loc[slot] <- this rank's p.q in one fused K4 launch when the
+        operator is the f64 CSR (FP64 PCG); False (nothing done) otherwise."""
+        if self.backend.name != "csr64" or p.dtype != self.torch.float64:
+            return False
+        D = self.backend.source.to_device()
+        x = p
+        if self.G > 1:
+            self.slab_of_full().copy_(p)
+            x = _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
+        L, d = self.d.L, self.d
+        err = L.PsellError()
+        rc = self.lib.psell_csr_spmv_dot(D.n_rows, L.ptr(D.row_ptr), L.ptr(D.col_idx), L.ptr(D.values),
+                                         x.data_ptr(), q.data_ptr(), p.data_ptr(), d.p(d.partials),
+                                         d.p(d.loc, slot), d.st(), err)
+        L.check(rc, err)
+        return True
+
     def audit(self, report: SolveReport, x, bnorm, tol) -> SolveReport:
         """True residual in f64 on the device, demote drifted runs (solvers.py:152-168)."""
         d = self.d
@@ -564,24 +595,31 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
         if history[-1] < cfg.tol:
             converged = True
             break
-        o.apply(p, q)
-        lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), None, d.p(d.partials), d.p(d.loc, 0), st)
+        if not o.apply_pq(p, q, 0):
+            o.apply(p, q)
+            lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), None, d.p(d.partials), d.p(d.loc, 0), st)
         d.reduce(0, 1, 10)                                                 # scal10 = pq
         d.flags.zero_()
         lib.psell_scalar_div(d.p(d.scal, 4), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)
         lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
                         d.p(d.flags), d.p(d.partials), d.p(d.loc, 2), st)
         d.reduce(2, 1, 12)                                                 # scal12 = rr
-        status = torch.stack([d.flags[0].to(torch.float64), d.scal[10], d.scal[12]]).cpu().numpy()
-        if status[0]:
-            reason = f"breakdown: non-positive curvature p'Ap = {float(status[1])!r} at iteration {it}"
+        flag, pq, rr = d.status(10, 12)
+        if flag:
+            reason = f"breakdown: non-positive curvature p'Ap = {pq!r} at iteration {it}"
             break
         it += 1
-        history.append(float(np.sqrt(status[2])) / bnorm)
-        lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), invp, d.p(d.partials), d.p(d.loc, 3), st)
-        d.reduce(3, 1, 5)                                                  # scal5 = rz_new
-        lib.psell_scalar_div(d.p(d.scal, 5), d.p(d.scal, 4), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
-        lib.psell_sum_strided(d.p(d.scal, 5), 1, 1, 1, d.p(d.scal, 4), st)                        # rz = rz_new
+        history.append(float(np.sqrt(rr)) / bnorm)
+        if invp is None:
+            # identity: z = r, and r.z is the r.r just reduced -- the same kernel
+            # grid, per-thread order and tree as psell_precond_dot, so the same bits
+            rz_slot = 12
+        else:
+            lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), invp, d.p(d.partials), d.p(d.loc, 3), st)
+            d.reduce(3, 1, 5)                                              # scal5 = rz_new
+            rz_slot = 5
+        lib.psell_scalar_div(d.p(d.scal, rz_slot), d.p(d.scal, 4), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
+        lib.psell_sum_strided(d.p(d.scal, rz_slot), 1, 1, 1, d.p(d.scal, 4), st)                   # rz = rz_new
         lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
     else:
         reason = f"maximum iterations ({cfg.max_outer}) reached"
@@ -657,12 +695,12 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
         lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
                         d.p(d.flags), d.p(d.partials), d.p(d.loc, 4), st)
         d.reduce(4, 1, 12)                                 # scal12 = r.r
-        status = torch.stack([d.flags[0].to(torch.float64), d.scal[10], d.scal[12]]).cpu().numpy()
-        if status[0]:
-            reason = f"breakdown: non-positive curvature p'Ap = {float(status[1])!r} at iteration {it}"
+        flag, pq, rr = d.status(10, 12)
+        if flag:
+            reason = f"breakdown: non-positive curvature p'Ap = {pq!r} at iteration {it}"
             break
         it += 1
-        history.append(float(np.sqrt(status[2])) / bnorm)
+        history.append(float(np.sqrt(rr)) / bnorm)
     else:
         reason = f"maximum iterations ({cfg.max_outer}) reached"
     if not converged and history[-1] < cfg.tol:

@@ -110,6 +110,39 @@ def test_csr_spmv_pipelined_bitwise_large():
         assert np.array_equal(_bits(y), _bits(O.csr_spmv(rp, ci, v, x, dt))), dt
 
 
+def test_csr_spmv_dot_fused():
+    """psell_csr_spmv_dot (FP64 PCG's q = A p with p.q): y bitwise equal to csr_spmv,
+    the dot within FP64 summation error of the exact one, identical run to run."""
+    import torch
+    from paper_2604_13433_b200 import _lib
+    rng = np.random.default_rng(8)
+    n = 250_000
+    lens = rng.integers(0, 10, n)
+    lens[rng.integers(0, n, 50)] = 2500
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = rng.integers(0, n, int(rp[-1])).astype(np.int32)
+    A = P.CsrMatrix(n, n, rp, ci, rng.standard_normal(int(rp[-1])))
+    x = rng.standard_normal(n)
+    want = O.csr_spmv(rp, ci, A.values, x, np.float64)
+    D = A.to_device()
+    xd = torch.tensor(x, device="cuda")
+    outs = []
+    for _ in range(2):
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        parts = torch.zeros(8192, dtype=torch.float64, device="cuda")
+        dot = torch.zeros(1, dtype=torch.float64, device="cuda")
+        err = _lib.PsellError()
+        rc = _lib.lib().psell_csr_spmv_dot(n, _lib.ptr(D.row_ptr), _lib.ptr(D.col_idx), _lib.ptr(D.values),
+                                           xd.data_ptr(), y.data_ptr(), xd.data_ptr(), parts.data_ptr(),
+                                           dot.data_ptr(), _lib.stream_handle(), err)
+        _lib.check(rc, err)
+        assert np.array_equal(_bits(y.cpu().numpy()), _bits(want))
+        outs.append(float(dot.item()))
+    exact = float(np.sum(x * want))
+    assert abs(outs[0] - exact) <= 1e-12 * float(np.sum(np.abs(x * want)))
+    assert outs[0] == outs[1]
+
+
 def test_errors_match_reference(golden_errors):
     def check(name, fn):
         g = golden_errors[name]
