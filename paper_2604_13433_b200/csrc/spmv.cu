@@ -190,6 +190,9 @@ __device__ __forceinline__ void finish_dot(const SpmvArgs& a, double v) {
 }
 
 constexpr int kWarpsPerCta = kBlock / 32;
+#ifndef PSELL_PAIR_MINB
+#define PSELL_PAIR_MINB 6  // resident 256-thread pair-kernel CTAs per SM the register budget is sized for (40 regs)
+#endif
 
 // dual-slice kernel switch (PSELL_DUAL=1 forces it on, =0 off; A/B)
 static bool dual_slices(long long n_slices) {
@@ -230,11 +233,11 @@ static int pair_nt(bool dot) {
 // Returns its grid (0 = not used).
 static int sm_count();
 static unsigned pair_persist_grid(long long n_slices, bool dot) {
-  int per_sm = 6;
+  int per_sm = PSELL_PAIR_MINB;
   if (const char* e = getenv("PSELL_PAIR_PERSIST")) per_sm = atoi(e);
   (void)dot;
   if (per_sm <= 0) return 0;
-  if (per_sm > 6) per_sm = 6;
+  if (per_sm > PSELL_PAIR_MINB) per_sm = PSELL_PAIR_MINB;
   const long long full = ceil_div(ceil_div(n_slices, 2), kWarpsPerCta);
   const long long cap = (long long)sm_count() * per_sm;
   return (unsigned)(full < cap ? full : cap);
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
 // division by sigma; the perm bytes are loaded before the word stream so
 // their latency hides under it.
 template <int CODEC, typename XT, bool DOT, int U, bool HOIST, int NT = kBlock, bool PERSIST = false>
-__global__ void __launch_bounds__(NT, 6 * kBlock / NT) spmv_pair_kernel(const SpmvArgs a) {
+__global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_kernel(const SpmvArgs a) {
     using S = FastStep<CODEC, XT>;
   if constexpr (DOT) {
     if (a.skip && *a.skip) return;
