@@ -11,6 +11,9 @@
 // accumulator from 0, one rounding per product and per sum (sell.py:181-204).
 #include "psell_internal.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace psell {
 
 template <typename V> __device__ __forceinline__ V from_f64(double v);
@@ -102,9 +105,74 @@ __global__ void __launch_bounds__(kBlock) sell_spmv_kernel(const VT* __restrict_
   y[out] = acc;
 }
 
+// C == 32 fast path: a warp per slice (lane = row), 8-step chunks whose value
+// and column loads (coalesced 128-B lines, evict-first) are all issued before
+// the 8 gathers, which are issued before the first dependent add; 32-bit index
+// math.  Same per-row operation order as sell_spmv_kernel (bitwise equal).
+// PSELL_SELL=generic forces the one-thread-per-row kernel (A/B)
+static bool sell_generic() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PSELL_SELL");
+    v = e && strcmp(e, "generic") == 0;
+  }
+  return v != 0;
+}
+
+template <typename VT, typename XT>
+__global__ void __launch_bounds__(kBlock, 6) sell_spmv_c32_kernel(const VT* __restrict__ val,
+                                                                  const int32_t* __restrict__ col,
+                                                                  const int64_t* __restrict__ offset,
+                                                                  const void* perm, int perm_bytes, int implicit,
+                                                                  unsigned sigma, long long n_rows,
+                                                                  long long n_slices, const XT* __restrict__ x,
+                                                                  XT* __restrict__ y) {
+  constexpr int U = 8;
+  const long long k = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= n_slices) return;
+  const long long o = offset[k];
+  const int width = (int)((offset[k + 1] - o) >> 5);
+  const VT* pv = val + o + lane;
+  const int32_t* pc = col + o + lane;
+  XT acc = RefOps<XT>::zero();
+  for (int q = 0; q < width; q += U) {
+    VT v[U];
+    int32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool in = q + u < width;
+      v[u] = in ? __ldcs(pv + (q + u) * 32) : VT(0);
+      c[u] = in ? __ldcs(pc + (q + u) * 32) : 0;
+    }
+    XT xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = x[c[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u < width) acc = RefOps<XT>::step(acc, vcast<VT, XT>(v[u]), xv[u]);
+  }
+  const unsigned s = (unsigned)(k * 32) + lane;
+  if ((long long)s >= n_rows) return;
+  unsigned out = s;
+  if (implicit) {
+    const unsigned pp = perm_bytes == 1 ? (unsigned)static_cast<const uint8_t*>(perm)[s]
+                                        : (unsigned)static_cast<const uint16_t*>(perm)[s];
+    out = (s / sigma) * sigma + pp;
+  }
+  y[out] = acc;
+}
+
 template <typename VT, typename XT>
 static void launch_sell(const psell_desc* d, const void* val, const int32_t* col, const int64_t* offset,
                         const void* perm, const void* x, void* y, cudaStream_t st) {
+  if (d->c == 32 && d->n_rows < (1LL << 31) && !sell_generic()) {
+    const long long ns = ceil_div(d->n_rows, 32);
+    sell_spmv_c32_kernel<VT, XT><<<(unsigned)ceil_div(ns * 32, kBlock), kBlock, 0, st>>>(
+        static_cast<const VT*>(val), col, offset, perm, d->sigma <= 256 ? 1 : 2, d->mode == PSELL_MODE_IMPLICIT,
+        (unsigned)d->sigma, d->n_rows, ns, static_cast<const XT*>(x), static_cast<XT*>(y));
+    return;
+  }
   const unsigned grid = (unsigned)ceil_div(d->n_rows, kBlock);
   sell_spmv_kernel<VT, XT><<<grid, kBlock, 0, st>>>(
       static_cast<const VT*>(val), col, offset, perm, d->sigma <= 256 ? 1 : 2, d->mode == PSELL_MODE_IMPLICIT,

@@ -106,8 +106,10 @@ def build_sell(A, c: int = 32, sigma: int = 256, mode: str = "implicit", value_d
                       n_padding=n_stored - D.nnz, value_dtype=vdt)
 
 
-def sell_spmv(M: SellMatrix, x):
-    """y = M x in x's precision, numpy rounding order (sell.py:181-204)."""
+def sell_spmv(M: SellMatrix, x, *, out=None):
+    """y = M x in x's precision, numpy rounding order (sell.py:181-204).
+
+    `out` (device x only): contiguous CUDA tensor of n_rows entries in x's dtype."""
     import torch
     from . import _dev, _lib
     lib = _lib.lib()
@@ -123,7 +125,13 @@ def sell_spmv(M: SellMatrix, x):
         xd = _dev.upload(x)
     if wd not in _dev.DT_CODE:
         raise TypeError(f"unsupported x dtype {wd}")
-    y = _dev.empty(M.n_rows, wd)
+    if out is not None:
+        if not on_dev or not (out.is_cuda and out.is_contiguous() and out.numel() == M.n_rows
+                              and out.dtype == xd.dtype and out.device == xd.device):
+            raise ValueError("sell_spmv: out must be a contiguous CUDA tensor of n_rows entries in x's dtype")
+        y = out
+    else:
+        y = _dev.empty(M.n_rows, wd)
     err = _lib.PsellError()
     rc = lib.psell_sell_spmv(M.desc(), _lib.ptr(M.d_val), _dev.DT_CODE[M.value_dtype], _lib.ptr(M.d_col),
                              _lib.ptr(M.d_offset), _lib.ptr(M.d_perm), _lib.ptr(xd), _dev.DT_CODE[wd], _lib.ptr(y),

@@ -138,7 +138,7 @@ def make_backend(A, name: str, c: int = 32, sigma: int = 256, mode: str = "impli
         from .sellfmt import build_sell, sell_spmv
         dt = {"sell64": np.float64, "sell32": np.float32, "sell16": np.float16}[name]
         S = build_sell(A, c, sigma, mode, value_dtype=dt)
-        return SpmvBackend(name, S, lambda x: sell_spmv(S, x), A)
+        return SpmvBackend(name, S, lambda x: sell_spmv(S, x), A, lambda x, out: sell_spmv(S, x, out=out))
     if name.startswith("packsell-"):
         fmt = codec.parse_format(name[len("packsell-"):])
         M = build_packsell(A, c, sigma, fmt, mode, _k_left_override=k_left)
@@ -386,14 +386,18 @@ class _GenericInner:
     """Inner PCG (solvers.py:278-308) on any device backend: the SELL-C-sigma / CSR
     comparators in f32 (the FP32 IO-CG of config 5) and every backend in f64
     (inner_precision="real64").  One GPU.  The same K3 scalar kernels as _InnerPCG
-    (breakdown flags, alpha / beta on the device); f32 vectors use the f32 update /
-    direction kernels, f64 vectors the outer loop's f64 kernels; the operator is
-    backend.apply on device vectors, p.q a fixed-grid FP64 dot."""
+    (breakdown flags, alpha / beta on the device).  f32: the _InnerPCG launch
+    structure (fused r/z update + beta, fused x / direction) captured in one CUDA
+    graph per backend, with the operator's SpMV and a fixed-grid FP64 p.q in place
+    of the fused PackSELL SpMV + p.q + alpha; f64: eager, the outer loop's f64
+    kernels."""
 
-    def __init__(self, backend, m_in, dtype, inv):
+    def __init__(self, backend, m_in, dtype, inv, use_graph: bool = True):
         import torch
         from . import _dev, _lib
         self.torch = torch
+        self.use_graph = use_graph
+        self.graph, self.graph_in, self._io = None, None, None
         self.backend = backend
         self.m_in = int(m_in)
         self.tdt = _dev.torch_dtype(dtype)
@@ -407,45 +411,82 @@ class _GenericInner:
         if self.n != n:
             t = self.torch
             self.n = n
-            self.x, self.r, self.p = (t.zeros(n, dtype=self.tdt, device="cuda") for _ in range(3))
+            self.x, self.r, self.p, self.q = (t.zeros(n, dtype=self.tdt, device="cuda") for _ in range(4))
             self.z = t.zeros(n, dtype=self.tdt, device="cuda") if self.inv is not None else self.r
+            self.graph = None
 
-    def solve(self, r64, z64) -> int:
-        d, lib, L = self.d, self.d.lib, self.d.L
-        n = int(r64.numel())
-        self._alloc(n)
+    def buffers(self):
+        """Persistent f64 (r, z) for the outer loop (the f32 graph is bound to them)."""
+        if getattr(self, "_io", None) is None:
+            n = self.backend.source.n_rows
+            f64 = self.torch.float64
+            self._io = (self.torch.zeros(n, dtype=f64, device="cuda"), self.torch.zeros(n, dtype=f64, device="cuda"))
+        return self._io
+
+    def _sequence_f32(self, r64, z64):
+        """The f32 inner loop in the _InnerPCG launch structure (SpMV; p.q + alpha;
+        r/z update + r.z + beta in one launch; x += alpha p with p = z + beta p)."""
+        d, lib = self.d, self.d.lib
+        n = self.n
+        st = d.st()
+        inv = None if self.inv is None else self.inv.data_ptr()
+        x, r, z, p, q = self.x, self.r, self.z, self.p, self.q
+        lib.psell_ipcg_begin(n, r64.data_ptr(), x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), inv,
+                             d.p(d.partials), d.p(d.loc, 0), st)
+        lib.psell_ipcg_set_rz(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), st)
+        for _ in range(self.m_in):
+            self.backend.apply_into(p, q)
+            lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
+            lib.psell_ipcg_alpha(d.p(d.loc, 1), 1, 8, d.p(d.scal), d.p(d.flags), st)
+            lib.psell_ipcg_update_beta(n, None, r.data_ptr(), z.data_ptr(), p.data_ptr(), q.data_ptr(), inv,
+                                       d.p(d.scal), d.p(d.flags), d.p(d.partials), d.p(d.ticket, d.tstride), st)
+            lib.psell_ipcg_direction_x(n, p.data_ptr(), z.data_ptr(), x.data_ptr(), d.p(d.scal), d.p(d.flags), st)
+        lib.psell_ipcg_end(n, x.data_ptr(), z64.data_ptr(), st)
+
+    def _eager(self, r64, z64):
+        """The loop launched op by op (f64 vectors, or use_graph=False)."""
+        d, lib = self.d, self.d.lib
+        n = self.n
         st = d.st()
         inv = None if self.inv is None else self.inv.data_ptr()
         x, r, z, p = self.x, self.r, self.z, self.p
         if self.f32:
-            lib.psell_ipcg_begin(n, r64.data_ptr(), x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), inv,
-                                 d.p(d.partials), d.p(d.loc, 0), st)
-        else:
-            x.zero_()
-            r.copy_(r64)
-            lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
-            lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
+            self._sequence_f32(r64, z64)
+            return
+        x.zero_()
+        r.copy_(r64)
+        lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
+        lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
         lib.psell_ipcg_set_rz(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), st)
         for _ in range(self.m_in):
             q = self.backend.apply(p)
             lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
             lib.psell_ipcg_alpha(d.p(d.loc, 1), 1, 8, d.p(d.scal), d.p(d.flags), st)
-            if self.f32:
-                lib.psell_ipcg_update(n, x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), q.data_ptr(), inv,
-                                      d.p(d.scal), d.p(d.flags), d.p(d.partials), d.p(d.loc, 2), st)
-            else:
-                lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 2),
-                                d.p(d.flags), d.p(d.partials), d.p(d.loc, 3), st)
-                lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 2), st)
+            lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 2),
+                            d.p(d.flags), d.p(d.partials), d.p(d.loc, 3), st)
+            lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 2), st)
             lib.psell_ipcg_beta(d.p(d.loc, 2), 1, 8, d.p(d.scal), d.p(d.flags), st)
-            if self.f32:
-                lib.psell_ipcg_direction(n, p.data_ptr(), z.data_ptr(), d.p(d.scal), d.p(d.flags), st)
-            else:
-                lib.psell_xpby_checked(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 3), d.p(d.flags), st)
-        if self.f32:
-            lib.psell_ipcg_end(n, x.data_ptr(), z64.data_ptr(), st)
+            lib.psell_xpby_checked(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 3), d.p(d.flags), st)
+        z64.copy_(x)
+
+    def solve(self, r64, z64) -> int:
+        d = self.d
+        self._alloc(int(r64.numel()))
+        if self.f32 and self.use_graph:
+            torch = self.torch
+            if self.graph is None or self.graph_in[0] is not r64 or self.graph_in[1] is not z64:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    self._sequence_f32(r64, z64)  # warm-up outside capture
+                torch.cuda.current_stream().wait_stream(s)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._sequence_f32(r64, z64)
+                self.graph, self.graph_in = g, (r64, z64)
+            self.graph.replay()
         else:
-            z64.copy_(x)
+            self._eager(r64, z64)
         flags = d.flags[:2].cpu().numpy()
         if int(flags[0]):
             log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate",
@@ -743,6 +784,10 @@ def iocg(A, b, cfg: SolveConfig = None, *, backend: SpmvBackend = None, comm=Non
     else:
         if comm is not None and comm.world > 1:
             raise NotImplementedError("distributed iocg needs a PackSELL inner backend in real32")
-        inner = _GenericInner(backend, cfg.m_in, dtype, inv)
+        key = ("generic", cfg.m_in, cfg.preconditioner, np.dtype(dtype).name, use_graph)
+        cache = backend.__dict__.setdefault("_inner_cache", {})
+        inner = cache.get(key)
+        if inner is None:
+            inner = cache[key] = _GenericInner(backend, cfg.m_in, dtype, inv, use_graph=use_graph)
     outer = make_backend(A, "csr64")
     return fcg(outer, b, cfg, _inner=inner, comm=comm)

@@ -15,10 +15,21 @@ for c in c2 c3 c4; do
 done
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_dual -s 3 -c 1 -o gpurun_out/ev/prof_c2 \
     python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline --no-pcg > /dev/null 2>&1
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_dual -s 3 -c 1 -o gpurun_out/ev/prof_c3 \
+    python bench.py --config c3 --steps 5 --warmup 3 --no-cpu-baseline --no-pcg > /dev/null 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_dual -s 3 -c 1 -o gpurun_out/ev/prof_c4 \
     python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline --no-pcg > /dev/null 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:spmv_pair -s 3 -c 1 -o gpurun_out/ev/prof_c5 \
     python scripts/prof_c5_spmv.py > /dev/null 2>&1
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv \
     --log-file gpurun_out/ev/launches_pcg_iter.csv python scripts/pcg_iter.py 64 > /dev/null 2>&1
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:csr_spmv_pipe -s 3 -c 1 -o gpurun_out/ev/prof_csr \
+    python scripts/csr_ab.py > /dev/null 2>&1
+timeout -s KILL 300 python scripts/iocg_kernels.py > gpurun_out/ev/iocg_kernels.txt 2>&1
+timeout -s KILL 300 python scripts/pcg64_kernels.py > gpurun_out/ev/pcg64_kernels.txt 2>&1
+# summaries of every capture; only the c2 / c5 reports travel back (gpurun_out is capped at 64 MiB)
+for r in c2 c3 c4 c5 csr; do
+  [ -f gpurun_out/ev/prof_$r.ncu-rep ] && python scripts/ncu_summary.py gpurun_out/ev/prof_$r.ncu-rep $r > gpurun_out/ev/ncu_$r.json
+done
+rm -f gpurun_out/ev/prof_c3.ncu-rep gpurun_out/ev/prof_c4.ncu-rep gpurun_out/ev/prof_csr.ncu-rep
 tail -2 gpurun_out/ev/pytest_gpu.log; tail -1 gpurun_out/ev/smoke.log
