@@ -32,7 +32,7 @@ for vdt, dt in ((np.float32, torch.float32), (np.float16, torch.float16)):
     Sm = P.build_sell(S, 32, 256, "implicit", vdt)
     x = x32.to(dt)
     y = P.sell_spmv(Sm, x)
-    us = timed(lambda: P.sell_spmv(Sm, x), reps=20) * 1e3
+    us = timed(lambda: P.sell_spmv(Sm, x, out=y), reps=20) * 1e3
     print(f"{'SELL-C-sigma ' + np.dtype(vdt).name:36s} {P.backward_error(S, x, y):15.3e} {us:9.1f}")
     del Sm
     torch.cuda.empty_cache()

@@ -27,6 +27,12 @@ timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k re
     python scripts/csr_ab.py > /dev/null 2>&1
 timeout -s KILL 300 python scripts/iocg_kernels.py > gpurun_out/ev/iocg_kernels.txt 2>&1
 timeout -s KILL 300 python scripts/pcg64_kernels.py > gpurun_out/ev/pcg64_kernels.txt 2>&1
+timeout -s KILL 300 python scripts/sell_iocg.py > gpurun_out/ev/sell_iocg.txt 2>&1
+PYTHONPATH=$PWD:$PWD/scripts timeout -s KILL 300 python scripts/accuracy_sell.py > gpurun_out/ev/accuracy_sell.txt 2>&1
+PYTHONPATH=$PWD:$PWD/scripts timeout -s KILL 300 python scripts/cusparse_ab.py > gpurun_out/ev/cusparse_ab.txt 2>&1
+timeout -s KILL 200 python scripts/csr_ab.py > gpurun_out/ev/csr_time.txt 2>&1
+timeout -s KILL 300 python scripts/spmv_time.py c2 c3 c5 > gpurun_out/ev/spmv_time.txt 2>&1
+timeout -s KILL 200 python scripts/upload_probe.py > gpurun_out/ev/upload_probe.txt 2>&1
 # summaries of every capture; only the c2 / c5 reports travel back (gpurun_out is capped at 64 MiB)
 for r in c2 c3 c4 c5 csr; do
   [ -f gpurun_out/ev/prof_$r.ncu-rep ] && python scripts/ncu_summary.py gpurun_out/ev/prof_$r.ncu-rep $r > gpurun_out/ev/ncu_$r.json
