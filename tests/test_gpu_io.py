@@ -244,3 +244,21 @@ def test_footprint_bits_vs_reference():
         fp = P.footprint_bits(M)
         assert (fp.pack_bits, fp.sell_equiv_bits) == (m["pack_bits"], m["sell_equiv_bits"]), i
         assert fp.ratio == m["ratio"], i
+
+
+def test_host_device_staging_round_trip():
+    """_dev.upload's threaded page-locked path (>= 16 MiB, ragged chunk tail, unsigned
+    types re-viewed as signed, `out=`) and download's page-locked view: bit-exact."""
+    import torch
+    from paper_2604_13433_b200 import _dev
+    rng = np.random.default_rng(21)
+    for dt, n in ((np.float64, 5_000_003), (np.uint32, 4_194_305), (np.float16, 9_000_001)):
+        a = (rng.standard_normal(n) * 100).astype(dt) if dt != np.uint32 else rng.integers(0, 2**32, n, dtype=np.uint32)
+        t = _dev.upload(a)
+        assert t.is_cuda and t.numel() == n
+        back = _dev.download(t, dt)
+        assert back.dtype == dt and np.array_equal(back.view(np.uint8), a.view(np.uint8))
+        out = torch.empty_like(t)
+        assert _dev.upload(a, out=out) is out and torch.equal(out, t)
+    with pytest.raises(ValueError):
+        _dev.upload(np.zeros(5_000_000), out=torch.empty(10, dtype=torch.float64, device="cuda"))
