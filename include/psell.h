@@ -301,6 +301,15 @@ PSELL_API int psell_scalar_div(const double* num_parts, const double* den_parts,
                      int32_t stride, double* dst, int32_t* flag, int32_t check_curvature,
                      void* stream);
 
+/* FP64 PCG convergence gate (solvers.py:183-207): gate[2] int32 (0 running,
+ * 1 breakdown -- pass gate as psell_scalar_div's flag and psell_axpy2's skip
+ * flag -- 2 converged; gate[1] = breakdown reported).  out[3] = {breakdown,
+ * pq, sqrt(rr) / bnorm}, out[0] = -1 when the solve had already stopped; sets
+ * gate[0] = 2 once sqrt(rr) / bnorm < tol, so iterations enqueued ahead of the
+ * host's status read are no-ops on x and r. */
+PSELL_API int psell_pcg_status(const double* pq, const double* rr, int32_t* gate, double bnorm, double tol,
+                     double* out, void* stream);
+
 /* ---- synthetic stencil generators (device) for the BASELINE configs ----
  * Grid d0 x d1 x d2 (d0 slowest), rows [row_begin, row_end) of the matrix.
  * box = 1: 27-point (HPCG, diag = 26), box = 0: star (2*ndim+1 point, diag 2*ndim).

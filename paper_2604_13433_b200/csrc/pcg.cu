@@ -426,6 +426,28 @@ __global__ void scalar_div_kernel(const double* num, const double* den, int np, 
   dst[0] = a / b;
 }
 
+// FP64 PCG convergence gate (solvers.py:183-207 loop head): gate[0] = 0 running,
+// 1 breakdown (written by scalar_div's curvature check), 2 converged; gate[1] =
+// breakdown already reported.  Writes this iteration's status {breakdown, p.q,
+// sqrt(r.r) / bnorm} (or {-1} when the solve had stopped before it) and closes
+// the gate when the recurred residual is below tol, so iterations the host
+// enqueued ahead of reading the status change nothing.  sqrt and / are IEEE
+// round-to-nearest, the host's float(np.sqrt(rr)) / bnorm bit for bit.
+__global__ void pcg_status_kernel(const double* pq, const double* rr, int32_t* gate, double bnorm, double tol,
+                                  double* out) {
+  const int g = gate[0];
+  if (g == 2 || (g == 1 && gate[1])) {
+    out[0] = -1.0;
+    return;
+  }
+  const double rel = __ddiv_rn(__dsqrt_rn(rr[0]), bnorm);
+  out[0] = g == 1 ? 1.0 : 0.0;
+  out[1] = pq[0];
+  out[2] = rel;
+  if (g == 1) gate[1] = 1;
+  else if (rel < tol) gate[0] = 2;
+}
+
 // out[j] = sum_{i < n_parts} parts[i * stride + j], j < n_out: rank-ordered global sums
 __global__ void sum_strided_kernel(const double* parts, int np, int stride, int n_out, double* out) {
   const int j = threadIdx.x;
@@ -608,6 +630,12 @@ int psell_scalar_div(const double* num_parts, const double* den_parts, int32_t n
                      void* stream) {
   scalar_div_kernel<<<1, 1, 0, as_stream(stream)>>>(num_parts, den_parts, n_parts, stride, dst,
                                                     flag, check_curvature);
+  return LAUNCH_OK();
+}
+
+int psell_pcg_status(const double* pq, const double* rr, int32_t* gate, double bnorm, double tol, double* out,
+                     void* stream) {
+  pcg_status_kernel<<<1, 1, 0, as_stream(stream)>>>(pq, rr, gate, bnorm, tol, out);
   return LAUNCH_OK();
 }
 

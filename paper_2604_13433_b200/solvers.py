@@ -631,26 +631,31 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
     d.reduce(0, 1, 4)                                                      # scal4 = rz
     p = z.clone()
     q = o.vec()
-    converged, reason, it = False, None, 0
-    while it < cfg.max_outer:
-        if history[-1] < cfg.tol:
-            converged = True
-            break
+    # The host reads iteration k's status while iteration k+1 is already queued:
+    # psell_pcg_status closes a device gate (flags[2]) on convergence, and a
+    # breakdown closes it through scalar_div's curvature check, so the iteration
+    # queued past the stop leaves x and r untouched -- no idle GPU between
+    # iterations, and the same iterates, history and stopping point as the loop
+    # of solvers.py:183-207 evaluated one iteration at a time.
+    gate = d.flags[2:4]
+    gate.zero_()
+    gp = gate.data_ptr()
+    h_stat = torch.zeros(6, dtype=torch.float64, pin_memory=True)
+    events = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def enqueue(k):
         if not o.apply_pq(p, q, 0):
             o.apply(p, q)
             lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), None, d.p(d.partials), d.p(d.loc, 0), st)
         d.reduce(0, 1, 10)                                                 # scal10 = pq
-        d.flags.zero_()
-        lib.psell_scalar_div(d.p(d.scal, 4), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)
+        lib.psell_scalar_div(d.p(d.scal, 4), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), gp, 1, st)  # alpha
         lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
-                        d.p(d.flags), d.p(d.partials), d.p(d.loc, 2), st)
+                        gp, d.p(d.partials), d.p(d.loc, 2), st)
         d.reduce(2, 1, 12)                                                 # scal12 = rr
-        flag, pq, rr = d.status(10, 12)
-        if flag:
-            reason = f"breakdown: non-positive curvature p'Ap = {pq!r} at iteration {it}"
-            break
-        it += 1
-        history.append(float(np.sqrt(rr)) / bnorm)
+        slot = 16 + 3 * (k % 2)
+        lib.psell_pcg_status(d.p(d.scal, 10), d.p(d.scal, 12), gp, bnorm, cfg.tol, d.p(d.scal, slot), st)
+        h_stat[3 * (k % 2):3 * (k % 2) + 3].copy_(d.scal[slot:slot + 3], non_blocking=True)
+        events[k % 2].record()
         if invp is None:
             # identity: z = r, and r.z is the r.r just reduced -- the same kernel
             # grid, per-thread order and tree as psell_precond_dot, so the same bits
@@ -662,8 +667,32 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
         lib.psell_scalar_div(d.p(d.scal, rz_slot), d.p(d.scal, 4), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
         lib.psell_sum_strided(d.p(d.scal, rz_slot), 1, 1, 1, d.p(d.scal, 4), st)                   # rz = rz_new
         lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
-    else:
+
+    converged, reason, it = False, None, 0
+    if cfg.max_outer <= 0:
         reason = f"maximum iterations ({cfg.max_outer}) reached"
+    elif history[-1] < cfg.tol:
+        converged = True
+    else:
+        enqueue(0)
+        k = 0
+        while True:
+            if k + 1 < cfg.max_outer:
+                enqueue(k + 1)
+            events[k % 2].synchronize()
+            brk, pq, rel = (float(v) for v in h_stat[3 * (k % 2):3 * (k % 2) + 3].numpy())
+            if brk == 1.0:
+                reason = f"breakdown: non-positive curvature p'Ap = {pq!r} at iteration {it}"
+                break
+            it = k + 1
+            history.append(rel)
+            if rel < cfg.tol:
+                converged = True
+                break
+            k += 1
+            if k >= cfg.max_outer:
+                reason = f"maximum iterations ({cfg.max_outer}) reached"
+                break
     if not converged and history[-1] < cfg.tol:
         converged = True
         reason = None

@@ -177,3 +177,32 @@ def test_iocg_and_pcg_64cubed_vs_reference():
     p = S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=2000))
     assert p.converged and abs(p.outer_iters - meta["pcg"]["outer"]) <= 1
     assert _close(p.x, z["pcg_x"], 1e-9)
+
+
+def test_pcg_stopping_rules_vs_oracle():
+    """The look-ahead PCG loop stops exactly where the one-at-a-time loop does:
+    iteration caps 0 / 1 / 2 / 7, convergence on the last allowed iteration, the
+    initial-residual check, and a breakdown a few iterations in (indefinite A)."""
+    import oracle as O
+    A = P.sym_diag_scale(P.poisson3d(6))
+    b, _ = S.make_rhs_and_x0(A.n_rows, 3)
+    a64 = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64)  # noqa: E731
+    full = O.pcg(a64, b, 1e-8, 1000)
+    cases = [(0, 1e-8), (1, 1e-8), (2, 1e-8), (7, 1e-8), (full["outer_iters"], 1e-8),
+             (full["outer_iters"] - 1, 1e-8), (50, 10.0)]
+    for max_outer, tol in cases:
+        r = S.pcg(A, b, S.SolveConfig(tol=tol, max_outer=max_outer))
+        ro = O.pcg(a64, b, tol, max_outer)
+        assert (r.converged, r.outer_iters) == (ro["converged"], ro["outer_iters"]), (max_outer, tol)
+        assert len(r.residual_history) == len(ro["history"])
+        assert np.allclose(r.residual_history, ro["history"], rtol=1e-10, atol=0), (max_outer, tol)
+        assert np.abs(r.x - ro["x"]).max() <= 1e-10 * max(1.0, np.abs(ro["x"]).max())
+    # indefinite: diagonal with mixed signs breaks down after a few steps
+    n = 40
+    d = np.concatenate([np.linspace(1, 2, n - 3), [-1.0, -2.0, -3.0]])
+    Ai = P.to_csr(P.CooMatrix(n, n, np.arange(n), np.arange(n), d))
+    bi = np.ones(n)
+    ri = S.pcg(Ai, bi, S.SolveConfig(tol=1e-14, max_outer=100))
+    ro = O.pcg(lambda v: d * v, bi, 1e-14, 100)
+    assert ro["reason"] == "breakdown" and ri.reason.startswith("breakdown")
+    assert ri.outer_iters == ro["outer_iters"] and len(ri.residual_history) == len(ro["history"])
