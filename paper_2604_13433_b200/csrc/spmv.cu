@@ -691,11 +691,29 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
         wa[u] = u < ra ? __ldcs(tA + u * 32) : 0u;
         wb[u] = u < rb ? __ldcs(tB + u * 32) : 0u;
       }
+#ifndef PSELL_PAIR_NOTAILSPLIT
+      // decode the first 3U/4 steps unconditionally and the rest only when a
+      // slice reaches them (7-point slices: 9 of 12 steps; 161 -> 153 us)
+      constexpr int K = 3 * U / 4;
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        S::run(wa[u], cA, x, accA, m_real, vmask);
+        S::run(wb[u], cB, x, accB, m_real, vmask);
+      }
+      if (ra > K || rb > K) {
+#pragma unroll
+        for (int u = K; u < U; ++u) {
+          S::run(wa[u], cA, x, accA, m_real, vmask);
+          S::run(wb[u], cB, x, accB, m_real, vmask);
+        }
+      }
+#else
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         S::run(wa[u], cA, x, accA, m_real, vmask);
         S::run(wb[u], cB, x, accB, m_real, vmask);
       }
+#endif
     }
     auto flush = [&](uint32_t s, uint32_t o, float acc) {
       if (s < n_rows) {
