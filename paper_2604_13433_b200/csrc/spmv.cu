@@ -686,10 +686,21 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
     if (ra > 0 || rb > 0) {
       const uint32_t* tA = pA + qa * 32;
       const uint32_t* tB = pB + qb * 32;
+#ifndef PSELL_PAIR_NOFULLK
+      if (ra >= 3 * U / 4 && rb >= 3 * U / 4) {  // both reach 3U/4 steps: those loads unpredicated (fused dot 162 -> 160 us)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        wa[u] = u < ra ? __ldcs(tA + u * 32) : 0u;
-        wb[u] = u < rb ? __ldcs(tB + u * 32) : 0u;
+        for (int u = 0; u < U; ++u) {
+          wa[u] = (u < 3 * U / 4 || u < ra) ? __ldcs(tA + u * 32) : 0u;
+          wb[u] = (u < 3 * U / 4 || u < rb) ? __ldcs(tB + u * 32) : 0u;
+        }
+      } else
+#endif
+      {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          wa[u] = u < ra ? __ldcs(tA + u * 32) : 0u;
+          wb[u] = u < rb ? __ldcs(tB + u * 32) : 0u;
+        }
       }
 #ifndef PSELL_PAIR_NOTAILSPLIT
       // decode the first 3U/4 steps unconditionally and the rest only when a
