@@ -190,6 +190,17 @@ __device__ __forceinline__ void finish_dot(const SpmvArgs& a, double v) {
 }
 
 constexpr int kWarpsPerCta = kBlock / 32;
+#ifndef PSELL_PAIR_U
+#define PSELL_PAIR_U 12  // tail steps of the persistent pair kernel
+#endif
+// split point of the pair kernel's tail: steps [0, K) always decoded, [K, U) only when reached
+template <int U> struct PairK {
+#ifdef PSELL_PAIR_K
+  static constexpr int K = PSELL_PAIR_K < U ? PSELL_PAIR_K : U;
+#else
+  static constexpr int K = 3 * U / 4;
+#endif
+};
 #ifndef PSELL_PAIR_MINB
 #define PSELL_PAIR_MINB 6  // resident 256-thread pair-kernel CTAs per SM the register budget is sized for (40 regs)
 #endif
@@ -687,11 +698,11 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
       const uint32_t* tA = pA + qa * 32;
       const uint32_t* tB = pB + qb * 32;
 #ifndef PSELL_PAIR_NOFULLK
-      if (ra >= 3 * U / 4 && rb >= 3 * U / 4) {  // both reach 3U/4 steps: those loads unpredicated (fused dot 162 -> 160 us)
+      if (ra >= PairK<U>::K && rb >= PairK<U>::K) {  // both reach 3U/4 steps: those loads unpredicated (fused dot 162 -> 160 us)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          wa[u] = (u < 3 * U / 4 || u < ra) ? __ldcs(tA + u * 32) : 0u;
-          wb[u] = (u < 3 * U / 4 || u < rb) ? __ldcs(tB + u * 32) : 0u;
+          wa[u] = (u < PairK<U>::K || u < ra) ? __ldcs(tA + u * 32) : 0u;
+          wb[u] = (u < PairK<U>::K || u < rb) ? __ldcs(tB + u * 32) : 0u;
         }
       } else
 #endif
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
 #ifndef PSELL_PAIR_NOTAILSPLIT
       // decode the first 3U/4 steps unconditionally and the rest only when a
       // slice reaches them (7-point slices: 9 of 12 steps; 161 -> 153 us)
-      constexpr int K = 3 * U / 4;
+      constexpr int K = PairK<U>::K;
 #pragma unroll
       for (int u = 0; u < K; ++u) {
         S::run(wa[u], cA, x, accA, m_real, vmask);
@@ -1311,7 +1322,7 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
             const int pn = pair_nt(DOT);
             const unsigned gp = (unsigned)ceil_div(ceil_div(a.n_slices, 2), pn / 32);
             const unsigned gpp = pair_persist_grid(a.n_slices, DOT);
-            if (gpp) spmv_pair_kernel<CODEC, XT, DOT, 12, true, kBlock, true><<<gpp, kBlock, 0, st>>>(a);
+            if (gpp) spmv_pair_kernel<CODEC, XT, DOT, PSELL_PAIR_U, true, kBlock, true><<<gpp, kBlock, 0, st>>>(a);
             else if (pn == 64) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 64><<<gp, 64, 0, st>>>(a);
             else if (pn == 128) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 128><<<gp, 128, 0, st>>>(a);
             else spmv_pair_kernel<CODEC, XT, DOT, 12, true><<<gd, kBlock, 0, st>>>(a);
