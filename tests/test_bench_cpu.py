@@ -4,7 +4,6 @@ partitions, the reference arm's CPU sample (oracle port) and its JSON contract."
 import json
 import os
 
-import numpy as np
 import pytest
 
 import bench

@@ -97,7 +97,6 @@ def test_inner_pcg_vs_oracle_f32():
     import torch
     A, b = _problem(10, 5)
     be = S.make_backend(A, "packsell-e8m14")
-    M = be.matrix
     OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, 256, O.preset("e8m14"), "implicit")
     zr, done = O.inner_pcg(lambda v: O.spmv(OM, v), b, 20, np.float32)
     inner = S._InnerPCG(be, 20)
@@ -106,7 +105,6 @@ def test_inner_pcg_vs_oracle_f32():
     assert k == done == 20
     zz = z.cpu().numpy()
     assert np.abs(zz - zr).max() / np.abs(zr).max() < 1e-4
-    del M
 
 
 def test_breakdown_and_zero_rhs():

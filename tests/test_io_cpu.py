@@ -64,7 +64,7 @@ def test_container_errors_match_reference(golden_container, name):
 
 
 def test_container_errors_from_path(golden_container, tmp_path):
-    z, meta = golden_container
+    z, _ = golden_container
     p = tmp_path / "t.psell"
     p.write_bytes(_corrupt(z["small_bytes"].tobytes(), "truncated_payload"))
     with pytest.raises(ContainerError, match="truncated"):
