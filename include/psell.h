@@ -243,6 +243,10 @@ PSELL_API int psell_ipcg_begin(int64_t n, const double* r64, float* x, float* r,
                      const float* inv_diag, double* partials, double* local_out, void* stream);
 PSELL_API int psell_ipcg_set_rz(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                       void* stream);
+/* psell_ipcg_set_rz with an outer loop's gate (psell_pcg_status): gate[0] != 0
+ * sets the inner breakdown flag, so the whole inner solve is a no-op. */
+PSELL_API int psell_ipcg_set_rz_gated(const double* parts, int32_t n_parts, int32_t stride, double* scal,
+                            int32_t* iflags, const int32_t* gate, void* stream);
 PSELL_API int psell_ipcg_alpha(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
                      void* stream);
 PSELL_API int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, const float* q,

@@ -79,6 +79,7 @@ _SIGS = {
     "psell_dot": (c_int32, [_P, _P, c_int32, c_int64, _P, _P, _P]),
     "psell_ipcg_begin": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psell_ipcg_set_rz": (c_int32, [_P, c_int32, c_int32, _P, _P, _P]),
+    "psell_ipcg_set_rz_gated": (c_int32, [_P, c_int32, c_int32, _P, _P, _P, _P]),
     "psell_ipcg_alpha": (c_int32, [_P, c_int32, c_int32, _P, _P, _P]),
     "psell_ipcg_update": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psell_ipcg_beta": (c_int32, [_P, c_int32, c_int32, _P, _P, _P]),

@@ -82,11 +82,16 @@ __global__ void __launch_bounds__(kBlock) ipcg_begin_kernel(long long n, const d
 }
 
 // scal: [0]=rz [1]=pq [2]=alpha [3]=beta [4]=rz_new ; iflags: [0]=breakdown [1]=done
-__global__ void ipcg_set_rz_kernel(const double* parts, int np, int stride, double* scal, int32_t* iflags) {
+// gate (optional): an outer loop's convergence gate (psell_pcg_status); when it is
+// closed the inner solve starts "broken down", so every kernel of the (captured)
+// inner loop returns at once -- the outer loop queues its next iteration before
+// reading the current one's status
+__global__ void ipcg_set_rz_kernel(const double* parts, int np, int stride, double* scal, int32_t* iflags,
+                                   const int32_t* gate) {
   double s = 0.0;
   for (int i = 0; i < np; ++i) s += parts[(long long)i * stride];
   scal[0] = s;
-  iflags[0] = 0;
+  iflags[0] = (gate && gate[0]) ? 1 : 0;
   iflags[1] = 0;
 }
 
@@ -505,7 +510,13 @@ int psell_ipcg_begin(int64_t n, const double* r64, float* x, float* r, float* z,
 }
 
 int psell_ipcg_set_rz(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags, void* stream) {
-  ipcg_set_rz_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, stride, scal, iflags);
+  ipcg_set_rz_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, stride, scal, iflags, nullptr);
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_set_rz_gated(const double* parts, int32_t n_parts, int32_t stride, double* scal, int32_t* iflags,
+                            const int32_t* gate, void* stream) {
+  ipcg_set_rz_kernel<<<1, 1, 0, as_stream(stream)>>>(parts, n_parts, stride, scal, iflags, gate);
   return LAUNCH_OK();
 }
 

@@ -301,6 +301,8 @@ class _InnerPCG:
         self.graph_in = None
         self.use_graph = use_graph and G == 1
         self._io = None
+        # outer-loop gate (fcg look-ahead): nonzero turns the whole inner solve into a no-op
+        self.gate = torch.zeros(2, dtype=torch.int32, device="cuda")
 
     def buffers(self):
         """Persistent f64 (r, z) the outer loop can hand to solve(): the captured graph
@@ -320,7 +322,7 @@ class _InnerPCG:
         lib.psell_ipcg_begin(self.n, r64.data_ptr(), self.x.data_ptr(), self.r.data_ptr(), self.z.data_ptr(),
                              self.p.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
         g, stride = d.gather()
-        lib.psell_ipcg_set_rz(d.p(g, 0), d.G, stride, d.p(d.scal), d.p(d.flags), st)
+        lib.psell_ipcg_set_rz_gated(d.p(g, 0), d.G, stride, d.p(d.scal), d.p(d.flags), self.gate.data_ptr(), st)
         if d.G == 1:
             # one GPU: 3 launches per iteration -- SpMV + p.q + alpha, r/z update + r.z + beta,
             # x += alpha p with p = z + beta p
@@ -357,6 +359,11 @@ class _InnerPCG:
 
     def solve(self, r64, z64) -> int:
         """z64 <- m_in f32 PCG steps on A z = r64 from zero; returns completed iterations."""
+        self.launch(r64, z64)
+        return _inner_done(self.d)
+
+    def launch(self, r64, z64):
+        """Queue the inner solve (no host synchronisation); d.flags[:2] = {breakdown, done}."""
         torch = self.torch
         if self.use_graph:
             if self.graph is None or self.graph_in is None or \
@@ -374,12 +381,16 @@ class _InnerPCG:
             self.graph.replay()
         else:
             self._sequence(r64, z64)
-        flags = self.d.flags[:2].cpu().numpy()
-        done = int(flags[1])
-        if int(flags[0]):
-            log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate",
-                        done, float(self.d.scal[1].item()))
-        return done
+
+
+def _inner_done(d, flags=None) -> int:
+    """Completed inner iterations from an inner solver's {breakdown, done} flags (logs a breakdown)."""
+    if flags is None:
+        flags = d.flags[:2].cpu().numpy()
+    if int(flags[0]):
+        log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate",
+                    int(flags[1]), float(d.scal[1].item()))
+    return int(flags[1])
 
 
 class _GenericInner:
@@ -398,6 +409,7 @@ class _GenericInner:
         self.torch = torch
         self.use_graph = use_graph
         self.graph, self.graph_in, self._io = None, None, None
+        self.gate = torch.zeros(2, dtype=torch.int32, device="cuda")  # see _InnerPCG.gate
         self.backend = backend
         self.m_in = int(m_in)
         self.tdt = _dev.torch_dtype(dtype)
@@ -433,7 +445,7 @@ class _GenericInner:
         x, r, z, p, q = self.x, self.r, self.z, self.p, self.q
         lib.psell_ipcg_begin(n, r64.data_ptr(), x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), inv,
                              d.p(d.partials), d.p(d.loc, 0), st)
-        lib.psell_ipcg_set_rz(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), st)
+        lib.psell_ipcg_set_rz_gated(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), self.gate.data_ptr(), st)
         for _ in range(self.m_in):
             self.backend.apply_into(p, q)
             lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
@@ -457,7 +469,7 @@ class _GenericInner:
         r.copy_(r64)
         lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv, d.p(d.partials), d.p(d.loc, 0), st)
         lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
-        lib.psell_ipcg_set_rz(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), st)
+        lib.psell_ipcg_set_rz_gated(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), self.gate.data_ptr(), st)
         for _ in range(self.m_in):
             q = self.backend.apply(p)
             lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
@@ -470,7 +482,11 @@ class _GenericInner:
         z64.copy_(x)
 
     def solve(self, r64, z64) -> int:
-        d = self.d
+        self.launch(r64, z64)
+        return _inner_done(self.d)
+
+    def launch(self, r64, z64):
+        """Queue the inner solve (no host synchronisation); d.flags[:2] = {breakdown, done}."""
         self._alloc(int(r64.numel()))
         if self.f32 and self.use_graph:
             torch = self.torch
@@ -487,11 +503,6 @@ class _GenericInner:
             self.graph.replay()
         else:
             self._eager(r64, z64)
-        flags = d.flags[:2].cpu().numpy()
-        if int(flags[0]):
-            log.warning("inner PCG breakdown at iteration %d (p'Ap=%r); returning current iterate",
-                        int(flags[1]), float(d.scal[1].item()))
-        return int(flags[1])
 
 
 # ----------------------------------------------------------------------------
@@ -732,26 +743,42 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
         r, z = o.b.clone(), o.vec()
     history = [d.norm(r) / bnorm]
     p, q, r_prev = o.vec(), o.vec(), o.vec()
-    converged, reason, it, first = False, None, 0, True
+    converged, reason, it = False, None, 0
     inner_total = 0
-    while it < cfg.max_outer:
-        if history[-1] < cfg.tol:
-            converged = True
-            break
+    # Look-ahead as in pcg: iteration k+1 (inner solve included) is queued before
+    # iteration k's status is read.  The gate closed by psell_pcg_status (or by a
+    # curvature breakdown in scalar_div) gates the outer x / r update and, through
+    # psell_ipcg_set_rz_gated, turns the queued inner solve into a no-op.  A host
+    # callable preconditioner needs r on the host every iteration: no look-ahead.
+    ahead = inner_preconditioner is None
+    gate = _inner.gate if (_inner is not None and hasattr(_inner, "gate")) else d.flags[2:4]
+    if _inner is not None and not hasattr(_inner, "launch"):
+        ahead = False
+    gate.zero_()
+    gp = gate.data_ptr()
+    h_stat = torch.zeros(6, dtype=torch.float64, pin_memory=True)
+    h_in = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+    events = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def enqueue(k):
+        slot = k % 2
         if _inner is not None:
-            inner_total += _inner.solve(r, z)
+            if ahead:
+                _inner.launch(r, z)
+                h_in[2 * slot:2 * slot + 2].copy_(_inner.d.flags[:2], non_blocking=True)
+            else:
+                h_in[2 * slot + 1] = _inner.solve(r, z)
         elif inner_preconditioner is not None:
             z.copy_(torch.as_tensor(np.asarray(inner_preconditioner(r.cpu().numpy()), dtype=np.float64)))
         elif inv is not None:
             lib.psell_precond_dot(n, z.data_ptr(), r.data_ptr(), inv.data_ptr(), d.p(d.partials), d.p(d.loc, 7), st)
         else:
             z.copy_(r)
-        lib.psell_fcg_zr(n, z.data_ptr(), r.data_ptr(), None if first else r_prev.data_ptr(),
+        lib.psell_fcg_zr(n, z.data_ptr(), r.data_ptr(), None if k == 0 else r_prev.data_ptr(),
                          d.p(d.partials), d.p(d.loc, 0), st)
         d.reduce(0, 2, 8)                                  # scal8 = z.(r - r_prev), scal9 = z.r
-        if first:
+        if k == 0:
             lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), None, st)
-            first = False
         else:
             lib.psell_scalar_div(d.p(d.scal, 8), d.p(d.scal, 6), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
             lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
@@ -760,19 +787,47 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
         o.apply(p, q)
         lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), r.data_ptr(), d.p(d.partials), d.p(d.loc, 2), st)
         d.reduce(2, 2, 10)                                 # scal10 = p.q, scal11 = p.r
-        d.flags.zero_()
-        lib.psell_scalar_div(d.p(d.scal, 11), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), d.p(d.flags), 1, st)
+        lib.psell_scalar_div(d.p(d.scal, 11), d.p(d.scal, 10), 1, 1, d.p(d.scal, 0), gp, 1, st)     # alpha
         lib.psell_axpy2(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal, 0),
-                        d.p(d.flags), d.p(d.partials), d.p(d.loc, 4), st)
+                        gp, d.p(d.partials), d.p(d.loc, 4), st)
         d.reduce(4, 1, 12)                                 # scal12 = r.r
-        flag, pq, rr = d.status(10, 12)
-        if flag:
-            reason = f"breakdown: non-positive curvature p'Ap = {pq!r} at iteration {it}"
-            break
-        it += 1
-        history.append(float(np.sqrt(rr)) / bnorm)
-    else:
+        sl = 16 + 3 * slot
+        lib.psell_pcg_status(d.p(d.scal, 10), d.p(d.scal, 12), gp, bnorm, cfg.tol, d.p(d.scal, sl), st)
+        h_stat[3 * slot:3 * slot + 3].copy_(d.scal[sl:sl + 3], non_blocking=True)
+        events[slot].record()
+
+    if cfg.max_outer <= 0:
         reason = f"maximum iterations ({cfg.max_outer}) reached"
+    elif history[-1] < cfg.tol:
+        converged = True
+    else:
+        enqueue(0)
+        k = 0
+        while True:
+            if ahead and k + 1 < cfg.max_outer:
+                enqueue(k + 1)
+            events[k % 2].synchronize()
+            if _inner is not None:
+                if ahead:
+                    inner_total += _inner_done(_inner.d, h_in[2 * (k % 2):2 * (k % 2) + 2].numpy())
+                else:
+                    inner_total += int(h_in[2 * (k % 2) + 1])
+            brk, pq, rel = (float(v) for v in h_stat[3 * (k % 2):3 * (k % 2) + 3].numpy())
+            if brk == 1.0:
+                reason = f"breakdown: non-positive curvature p'Ap = {pq!r} at iteration {it}"
+                break
+            it = k + 1
+            history.append(rel)
+            if rel < cfg.tol:
+                converged = True
+                break
+            k += 1
+            if k >= cfg.max_outer:
+                reason = f"maximum iterations ({cfg.max_outer}) reached"
+                break
+            if not ahead:
+                enqueue(k)
+    gate.zero_()  # leave the inner solver ungated for direct use
     if not converged and history[-1] < cfg.tol:
         converged = True
         reason = None

@@ -204,3 +204,30 @@ def test_pcg_stopping_rules_vs_oracle():
     ro = O.pcg(lambda v: d * v, bi, 1e-14, 100)
     assert ro["reason"] == "breakdown" and ri.reason.startswith("breakdown")
     assert ri.outer_iters == ro["outer_iters"] and len(ri.residual_history) == len(ro["history"])
+
+
+def test_iocg_stopping_rules_vs_oracle():
+    """IO-CG with the outer look-ahead stops where the reference loop does: caps 1 / 2 /
+    exact / one short, convergence, and counts only the inner iterations of outer
+    iterations that ran (the queued, gated one adds none); a direct inner solve after
+    an IO-CG solve is not gated."""
+    import oracle as O
+    import torch
+    A = P.sym_diag_scale(P.poisson3d(8))
+    b, _ = S.make_rhs_and_x0(A.n_rows, 4)
+    a64 = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64)  # noqa: E731
+    OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, 256, O.preset("e8m14"), "implicit")
+    inner = lambda v: O.spmv(OM, v)  # noqa: E731
+    full = O.iocg(a64, inner, b, 1e-9, 200, 10)
+    be = S.make_backend(A, "packsell-e8m14")
+    for max_outer in (1, 2, full["outer_iters"] - 1, full["outer_iters"], 200):
+        cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=10, a_backend="packsell-e8m14", max_outer=max_outer)
+        r = S.iocg(A, b, cfg, backend=be)
+        ro = O.iocg(a64, inner, b, 1e-9, max_outer, 10)
+        assert (r.converged, r.outer_iters, r.total_inner_iters) == \
+            (ro["converged"], ro["outer_iters"], ro["total_inner_iters"]), max_outer
+        assert len(r.residual_history) == len(ro["history"])
+        assert np.abs(r.x - ro["x"]).max() <= 1e-6 * np.abs(ro["x"]).max()
+    inner_solver = next(iter(be._inner_cache.values()))
+    z = torch.empty(A.n_rows, dtype=torch.float64, device="cuda")
+    assert inner_solver.solve(torch.as_tensor(b).cuda(), z) == 10
