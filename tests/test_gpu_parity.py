@@ -420,3 +420,34 @@ def test_spmv_argument_validation(rng):
         P.packsell_spmv(M, x.to(torch.int32))
     xs = torch.rand(180, device="cuda")[::2]  # strided view: made contiguous, same result
     assert torch.equal(P.packsell_spmv(M, xs), P.packsell_spmv(M, xs.contiguous()))
+
+
+def test_persistent_pair_kernel_at_scale(rng):
+    """The persistent pair kernel over many grid-stride trips per warp (1.2 M rows, far
+    more slice pairs than resident warps), narrow slices of mixed widths (tails split
+    at 9 steps, both slices reaching it or not) plus some wider than 12 steps (full
+    chunks and the longer slice's remainder): FMA SpMV within the bound of the
+    REF_ORDER kernel, in e8m14 / f32 x and fp16 / f16 x."""
+    n = 1_200_000
+    lens = rng.integers(3, 10, n)
+    lens[rng.integers(0, n, 3000)] = rng.integers(12, 20, 3000)
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.clip(rows + rng.integers(-120, 120, rows.size), 0, n - 1)
+    order = np.lexsort((cols, rows))
+    r, c = rows[order], cols[order]
+    keep = np.ones(r.size, bool)
+    keep[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+    r, c = r[keep], c[keep]
+    v = rng.uniform(0.01, 1, r.size) * rng.choice([-1.0, 1.0], r.size)
+    rp = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n))]).astype(np.int64)
+    A = P.CsrMatrix(n, n, rp, c.astype(np.int32), v)
+    for pre, dt in (("e8m14", np.float32), ("fp16", np.float16)):
+        M = P.build_packsell(A, 32, 256, P.parse_format(pre), "implicit")
+        assert M.spmv_flags() & 4, "expected the narrow (pair-kernel) path"
+        x = rng.uniform(-1, 1, n).astype(dt)
+        yr = P.packsell_spmv(M, x.astype(np.float32), ref_order=True).astype(np.float64)
+        yf = P.packsell_spmv(M, x).astype(np.float64)
+        lmax = int(np.max(np.diff(M.offset) // 32))
+        anorm = np.bincount(r, np.abs(P.quantize(P.parse_format(pre), v)), minlength=n).max()
+        err = np.abs(yf - yr).max() / (anorm * np.abs(x.astype(np.float64)).max())
+        assert err <= 2 * lmax * 2.0 ** -24 + (2.0 ** -11 if dt == np.float16 else 0.0), (pre, err)
