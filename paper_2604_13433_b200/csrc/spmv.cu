@@ -604,15 +604,20 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
       }
     }
     const uint32_t sig = (uint32_t)a.sigma;
+    // output rows: branch-free clamped perm loads, multiply-high division
+    const uint32_t nr = (uint32_t)a.n_rows;
+    auto out_row = [&](long long k) -> uint32_t {
+      const uint32_t s = (uint32_t)(k * 32) + lane;
+      if (a.mode != PSELL_MODE_IMPLICIT) return s;
+      const uint32_t sc = s < nr ? s : nr - 1u;
+      const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc)
+                                            : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
+      return fast_div((uint32_t)(k * 32), a.sig_m, a.sig_l) * sig + pp;
+    };
     auto flush = [&](long long k, float acc) {
       const uint32_t s = (uint32_t)(k * 32) + lane;
+      const uint32_t o = out_row(k);
       if ((long long)s < a.n_rows) {
-        uint32_t o = s;
-        if (a.mode == PSELL_MODE_IMPLICIT) {
-          const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)static_cast<const uint8_t*>(a.perm)[s]
-                                                : (uint32_t)static_cast<const uint16_t*>(a.perm)[s];
-          o = (s / sig) * sig + pp;
-        }
         XT yv;
         if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
         else yv = acc;
@@ -654,9 +659,11 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
     auto out_of = [&](uint32_t k, uint32_t s) -> uint32_t {
       if (!impl) return s;
       const uint32_t blk = fast_div(k * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma;
-      const uint32_t pp = s >= n_rows ? 0u
-                          : a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + s)
-                                              : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + s);
+      // rows past n_rows (last slice) read the last valid perm entry and are never
+      // stored: no divergent branch around the load (7-point 152.7 -> 145.6 us)
+      const uint32_t sc = s < n_rows ? s : n_rows - 1u;
+      const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc)
+                                            : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
       return blk + pp;
     };
     uint32_t oA = sA, oB = sB;
