@@ -541,26 +541,29 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
     const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
     const uint32_t se = (uint32_t)a.se, kl = (uint32_t)a.k_left;
     const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    // The fp16 x f16 instantiation (config 2) measured slower with each of the
+    // e8mY tunings below (multiply-high base division 324 -> 326 us, last-chunk
+    // split 324 -> 328 us, unpredicated full chunks 324 -> 328 us) and keeps the
+    // plain forms; e8mY / f32 x (config 3) takes all three (364 -> 351 us).
+    constexpr bool kTuned = !(CODEC == PSELL_FP16 && sizeof(XT) == 2);
     auto base2 = [&](long long k) -> uint32_t {
       const uint32_t g = (uint32_t)a.row0 + (uint32_t)(k * 32) + lane;
-      const uint32_t blk = (g / se) * se;
+      const uint32_t blk = !kTuned ? (g / se) * se : se == 1 ? g : fast_div(g, a.se_m, a.se_l) * se;
       const uint32_t d = blk > kl ? blk - kl : 0u;
       return 2u * (d < cmax ? d : cmax);
     };
     uint32_t cA = base2(kA), cB = base2(kB);
     float accA = 0.f, accB = 0.f;
     const int wmax = wA > wB ? wA : wB;
-    // e8mY / f32 x: all chunks but the last in the loop; the last one (<= U steps)
-    // after it, decoding its last quarter only when some slice reaches it (27-point
-    // 356 -> 354 us; fp16 x f16 measured 324 -> 328 us and keeps the single loop)
-    constexpr bool kTail2 = !(CODEC == PSELL_FP16 && sizeof(XT) == 2);
+    // kTuned: all chunks but the last in the loop; the last one (<= U steps) after
+    // it, decoding its last quarter only when some slice reaches it
+    constexpr bool kTail2 = kTuned;
     const int qlast = wmax > 0 ? ((wmax - 1) / U) * U : 0;
     for (int q = 0; q < (kTail2 ? qlast : wmax); q += U) {
       uint32_t a8[U], b8[U];
 #ifndef PSELL_DUAL_NOFULL
-      // full chunk of both slices: no per-word predicates (e8mY / f32 x: 27-point
-      // 364 -> 356 us; fp16 x f16 measured 324 -> 328 us and keeps the single path)
-      if (!(CODEC == PSELL_FP16 && sizeof(XT) == 2) && q + U <= wA && q + U <= wB) {
+      // kTuned: full chunk of both slices with no per-word predicates
+      if (kTuned && q + U <= wA && q + U <= wB) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           a8[u] = __ldcs(pA + (q + u) * 32);
