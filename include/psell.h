@@ -100,6 +100,10 @@ typedef struct psell_desc {
 PSELL_API const char* psell_version(void);
 PSELL_API int32_t psell_abi_version(void);
 
+/* Re-read the PSELL_* A/B environment knobs of the SpMV launchers (cached per
+ * call site otherwise: a getenv per launch is measurable on small matrices). */
+PSELL_API int32_t psell_reload_env(void);
+
 /* ---- K1: CSR -> PackSELL builder (replaces build_packsell, packed.py:176-239) ---- */
 
 PSELL_API size_t psell_build_workspace_bytes(const psell_desc* desc);

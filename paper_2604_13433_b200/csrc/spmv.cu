@@ -17,6 +17,8 @@
 // mapping without the warp-uniform fast path.
 #include "psell_internal.cuh"
 
+#include <atomic>
+
 namespace psell {
 
 struct SpmvArgs {
@@ -205,24 +207,47 @@ template <int U> struct PairK {
 #define PSELL_PAIR_MINB 6  // resident 256-thread pair-kernel CTAs per SM the register budget is sized for (40 regs)
 #endif
 
+// A/B knobs: getenv once per call site, re-read after psell_reload_env() (the
+// launch path of a small SpMV is host-bound; a getenv scans the environment)
+static std::atomic<unsigned> g_env_gen{1};
+struct EnvCache {
+  unsigned gen = 0;
+  bool set = false;
+  int val = 0;
+};
+static inline bool env_int(EnvCache& c, const char* name, int& v) {
+  const unsigned g = g_env_gen.load(std::memory_order_relaxed);
+  if (c.gen != g) {
+    const char* e = getenv(name);
+    c.set = e != nullptr;
+    c.val = e ? atoi(e) : 0;
+    c.gen = g;
+  }
+  v = c.val;
+  return c.set;
+}
+
 // dual-slice kernel switch (PSELL_DUAL=1 forces it on, =0 off; A/B)
 static bool dual_slices(long long n_slices) {
-  if (const char* e = getenv("PSELL_DUAL")) return atoi(e) != 0;
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_DUAL", v)) return v != 0;
   return n_slices >= 2;  // measured faster than one slice per warp on configs 2, 3, 5
 }
 
 // steps per chunk of the dual-slice kernel (PSELL_DUAL_U overrides: 8 | 12)
 static int dual_chunk(bool narrow) {
-  if (const char* e = getenv("PSELL_DUAL_U")) {
-    const int v = atoi(e);
-    if (v == 8 || v == 12) return v;
-  }
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_DUAL_U", v) && (v == 8 || v == 12)) return v;
   return narrow ? 12 : 8;  // 12 covers a whole 7-point slice in one chunk (sweep: +14 %)
 }
 
 // exact-tail pair kernel instead of the chunk-rounded dual kernel (PSELL_PAIR=0: dual, A/B)
 static bool pair_kernel() {
-  if (const char* e = getenv("PSELL_PAIR")) return atoi(e) != 0;
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_PAIR", v)) return v != 0;
   return true;
 }
 
@@ -230,10 +255,9 @@ static bool pair_kernel() {
 // measured ~2.5 % faster than 256 on 7-point slices (smaller CTAs retire sooner);
 // the fused-dot variant keeps 256 so its partial count (one per CTA) stays small.
 static int pair_nt(bool dot) {
-  if (const char* e = getenv("PSELL_PAIR_NT")) {
-    const int v = atoi(e);
-    if (v == 64 || v == 128 || v == 256) return v;
-  }
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_PAIR_NT", v) && (v == 64 || v == 128 || v == 256)) return v;
   return dot ? 256 : 128;
 }
 
@@ -245,7 +269,9 @@ static int pair_nt(bool dot) {
 static int sm_count();
 static unsigned pair_persist_grid(long long n_slices, bool dot) {
   int per_sm = PSELL_PAIR_MINB;
-  if (const char* e = getenv("PSELL_PAIR_PERSIST")) per_sm = atoi(e);
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_PAIR_PERSIST", v)) per_sm = v;
   (void)dot;
   if (per_sm <= 0) return 0;
   if (per_sm > PSELL_PAIR_MINB) per_sm = PSELL_PAIR_MINB;
@@ -256,16 +282,17 @@ static unsigned pair_persist_grid(long long n_slices, bool dot) {
 
 // pair kernel for wide slices too (PSELL_PAIR_WIDE=1, A/B; default: dual kernel)
 static bool pair_wide() {
-  if (const char* e = getenv("PSELL_PAIR_WIDE")) return atoi(e) != 0;
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_PAIR_WIDE", v)) return v != 0;
   return false;
 }
 
 // threads per CTA of the one-warp-per-slice kernel (PSELL_NT overrides, A/B)
 static int fast_nt() {
-  if (const char* e = getenv("PSELL_NT")) {
-    const int v = atoi(e);
-    if (v == 64 || v == 128 || v == 256) return v;
-  }
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_NT", v) && (v == 64 || v == 128 || v == 256)) return v;
   return 256;
 }
 
@@ -1286,14 +1313,22 @@ static void launch_tile(const SpmvArgs& a, cudaStream_t st) {
 
 // tile-TMA kernel for narrow slices instead of the persistent pair kernel (PSELL_TILE=1, A/B)
 static bool tile_kernel() {
-  if (const char* e = getenv("PSELL_TILE")) return atoi(e) != 0;
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_TILE", v)) return v != 0;
   return false;
 }
 
-static int sm_count() {
-  int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
+static int sm_count() {  // per device, queried once
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
 }
 
 // grid of the C = 32 launch: persistent for the TMA ring, one warp per slice otherwise
@@ -1448,7 +1483,9 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   magic_div((uint32_t)(a.se > 0 ? a.se : 1), a.se_m, a.se_l);
   magic_div((uint32_t)(a.sigma > 0 ? a.sigma : 1), a.sig_m, a.sig_l);
   a.l2pf = 1;
-  if (const char* e = getenv("PSELL_L2PF")) a.l2pf = atoi(e);
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_L2PF", v)) a.l2pf = v;
   return PSELL_OK;
 }
 
@@ -1733,3 +1770,8 @@ int psell_to_csr_fill(const psell_desc* d, const void* pack, const int64_t* offs
 }
 
 }  // extern "C"
+
+extern "C" PSELL_API int32_t psell_reload_env(void) {
+  g_env_gen.fetch_add(1, std::memory_order_relaxed);
+  return 0;
+}

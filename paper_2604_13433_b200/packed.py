@@ -182,12 +182,17 @@ class PackSellMatrix:
 
     # -- device side
     def desc(self):
+        """The C descriptor (built once: the matrix is immutable)."""
+        d = self.__dict__.get("_desc_cache")
+        if d is not None:
+            return d
         from . import _lib
         d = _lib.PsellDesc()
         d.w, d.d, d.codec = self.fmt.w, self.fmt.d, _lib.CODEC_IDS[self.fmt.codec]
         d.c, d.sigma, d.mode = self.c, self.sigma, _lib.MODE_IDS[self.mode]
         d.n_rows, d.n_cols, d.row0 = self.n_rows, self.n_cols, self.row0
         d.k_left, d.nnz = self.k_left, self.counts.nnz_real
+        self.__dict__["_desc_cache"] = d
         return d
 
     def spmv_flags(self) -> int:
@@ -325,8 +330,20 @@ def _seg_schedule(M: PackSellMatrix):
     return s
 
 
+_MODS = None
+
+
+def _mods():
+    """(_dev, _lib), imported on first use (they pull in torch / the library)."""
+    global _MODS
+    if _MODS is None:
+        from . import _dev, _lib
+        _MODS = (_dev, _lib)
+    return _MODS
+
+
 def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool, pipe: int = 0):
-    from . import _dev, _lib
+    _dev, _lib = _mods()
     lib = _lib.lib()
     err = _lib.PsellError()
     if not ref_order and not pipe and M.fmt.codec != codec.FP32EMBED and xd.dtype in _SEG_DTYPES:
@@ -359,21 +376,24 @@ def packsell_spmv(M: PackSellMatrix, x, *, ref_order: bool = False, out=None, _p
     reference's numpy rounding bit for bit.
     """
     import torch
-    from . import _dev
-    if _is_tensor(x):
+    _dev = _mods()[0]
+    if isinstance(x, torch.Tensor):
         if x.dim() != 1:
             raise ValueError(f"x must be one-dimensional, got shape {tuple(x.shape)}")
-        if len(x) != M.n_cols:
-            raise ValueError(f"x has length {len(x)}, expected {M.n_cols}")
+        if x.shape[0] != M.n_cols:
+            raise ValueError(f"x has length {x.shape[0]}, expected {M.n_cols}")
         if x.dtype not in _dev.T_DT_CODE:
             raise TypeError(f"unsupported x dtype {x.dtype}")
-        if out is not None and (not _is_tensor(out) or out.dim() != 1 or out.numel() != M.n_rows
+        if out is not None and (not isinstance(out, torch.Tensor) or out.dim() != 1 or out.shape[0] != M.n_rows
                                 or out.dtype != x.dtype or not out.is_contiguous()):
             raise ValueError(f"out must be a contiguous {x.dtype} tensor of {M.n_rows} entries")
         if x.is_cuda:
-            if x.device != M.d_pack.device:
+            # device indices (ints) rather than torch.device objects: this is the
+            # per-call path of small SpMVs, which are host-bound
+            xi = x.get_device()
+            if xi != M.d_pack.get_device():
                 raise ValueError(f"x is on {x.device}, the matrix on {M.d_pack.device}")
-            if out is not None and out.device != x.device:
+            if out is not None and out.get_device() != xi:
                 raise ValueError(f"out must be on {x.device}")
             y = out if out is not None else torch.empty(M.n_rows, dtype=x.dtype, device=x.device)
             return _spmv_device(M, x.contiguous(), y, ref_order, _pipe)

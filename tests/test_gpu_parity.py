@@ -386,6 +386,10 @@ def test_tile_tma_kernel_equals_pair_kernel(monkeypatch, kind, nx):
     res = {}
     for tile in ("0", "1"):
         monkeypatch.setenv("PSELL_TILE", tile)
+        lib.psell_reload_env()  # the launchers cache their knobs
+        from paper_2604_13433_b200 import _dev
+        assert lib.psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode().startswith(
+            "spmv_tile" if tile == "1" else "spmv_pair")
         y = P.packsell_spmv(M, x)
         npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
         part = torch.zeros(npart, dtype=torch.float64, device="cuda")
@@ -396,6 +400,8 @@ def test_tile_tma_kernel_equals_pair_kernel(monkeypatch, kind, nx):
                                 _lib.stream_handle(), err)
         _lib.check(rc, err)
         res[tile] = (y.clone(), q.clone(), float(part.sum()))
+    monkeypatch.delenv("PSELL_TILE")
+    lib.psell_reload_env()
     assert torch.equal(res["0"][0], res["1"][0]) and torch.equal(res["0"][1], res["1"][1])
     assert res["0"][2] == pytest.approx(res["1"][2], rel=1e-12)
 
