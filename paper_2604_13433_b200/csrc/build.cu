@@ -30,7 +30,7 @@ struct BuildStats {
   long long n_dummy;
   long long nonfinite_pos;
   long long overflow_pos;
-  long long pad;
+  long long n_long;  // rows listed for the warp-per-row kernels (row_stats, then fill)
 };
 
 constexpr int kSortSmemMaxSigma = 2048;
@@ -45,6 +45,7 @@ struct BuildWs {
   long long* wwords;    // n_slices  width*C
   long long* scan_tmp;  // scan block sums
   uint32_t* sort_tmp;   // 4n  (only sigma > kSortSmemMaxSigma)
+  int32_t* long_rows;   // n   rows longer than kLongRow, walked one warp per row
   size_t bytes;
 };
 
@@ -70,6 +71,7 @@ static BuildWs carve(const psell_desc* d, void* base) {
   w.scan_tmp = reinterpret_cast<long long*>(take(8 * (size_t)(nb + kScanTile)));
   const bool big = d->mode != PSELL_MODE_NONE && d->sigma > kSortSmemMaxSigma;
   w.sort_tmp = reinterpret_cast<uint32_t*>(take(big ? 16 * (size_t)n : 0));
+  w.long_rows = reinterpret_cast<int32_t*>(take(4 * (size_t)n));
   w.bytes = off;
   return w;
 }
@@ -80,6 +82,20 @@ const int32_t* build_ws_order(const psell_desc* d, const void* ws) {
 }
 
 // Eq. 4 base offset of global row g (packed.py:40-52).
+constexpr long long kLongRow = 64;  // rows longer than this are walked by a whole warp
+
+// grid of the warp-per-long-row kernels: a resident wave (8 CTAs of 8 warps per SM)
+static unsigned long_grid() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return (unsigned)(8 * sms);
+}
+
 __device__ __forceinline__ long long base_of(long long g, long long se, long long k_left) {
   const long long blk = (g / se) * se;
   return blk > k_left ? blk - k_left : 0;
@@ -93,7 +109,7 @@ __global__ void init_stats_kernel(BuildStats* s, long long k_left) {
   s->n_dummy = 0;
   s->nonfinite_pos = kI64Max;
   s->overflow_pos = kI64Max;
-  s->pad = 0;
+  s->n_long = 0;
 }
 
 template <typename T, typename Op>
@@ -142,15 +158,23 @@ __global__ void lower_bandwidth_kernel(const int64_t* __restrict__ row_ptr,
 __global__ void row_stats_kernel(const int64_t* __restrict__ row_ptr,
                                  const int32_t* __restrict__ col_idx, long long n, long long row0,
                                  long long se, int d_bits, BuildStats* st,
-                                 uint32_t* __restrict__ counts) {
+                                 uint32_t* __restrict__ counts, int32_t* __restrict__ long_rows) {
   __shared__ long long sh[32];
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long dum = 0, fg = kI64Max, gmax = kI64Min;
+  const long long k_left = st->k_left;
+  const long long thr = 1ll << d_bits;
+  long long beg = 0, end = 0;
   if (i < n) {
-    const long long k_left = st->k_left;
-    const long long beg = row_ptr[i], end = row_ptr[i + 1];
+    beg = row_ptr[i];
+    end = row_ptr[i + 1];
+    if (end > beg) fg = (long long)col_idx[beg] - base_of(row0 + i, se, k_left);
+  }
+  // rows longer than kLongRow entries go to row_stats_long_kernel, one warp each
+  // (power-law rows: one thread per row left the kernel waiting on its longest row)
+  const bool lng = i < n && end - beg > kLongRow;
+  if (i < n && !lng) {
     long long prev = base_of(row0 + i, se, k_left);
-    const long long thr = 1ll << d_bits;
     for (long long j = beg; j < end; ++j) {
       const long long col = col_idx[j];
       const long long gap = col - prev;
@@ -158,15 +182,51 @@ __global__ void row_stats_kernel(const int64_t* __restrict__ row_ptr,
       dum += gap >= thr;
       gmax = gap > gmax ? gap : gmax;
     }
-    if (end > beg) fg = (long long)col_idx[beg] - base_of(row0 + i, se, k_left);
     counts[i] = (uint32_t)((end - beg) + dum);
   }
+  if (lng) long_rows[atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_long), 1ull)] = (int32_t)i;
   const long long sd = cta_reduce(dum, AddOp{}, 0ll, sh);
   const long long sf = cta_reduce(fg, MinOp{}, kI64Max, sh);
   const long long sg = cta_reduce(gmax, MaxOp{}, kI64Min, sh);
   if (threadIdx.x == 0) {
     if (sd) atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_dummy), (unsigned long long)sd);
     if (sf != kI64Max) atomicMin(&st->min_first_gap, sf);
+    if (sg != kI64Min) atomicMax(&st->max_gap, sg);
+  }
+}
+
+// row_stats for the listed long rows: one warp per row, 32 entries per trip
+__global__ void __launch_bounds__(kBlock) row_stats_long_kernel(const int64_t* __restrict__ row_ptr,
+                                                                const int32_t* __restrict__ col_idx,
+                                                                long long row0, long long se, int d_bits,
+                                                                BuildStats* st, uint32_t* __restrict__ counts,
+                                                                const int32_t* __restrict__ long_rows) {
+  __shared__ long long sh[32];
+  const long long nl = st->n_long;
+  const long long k_left = st->k_left;
+  const long long thr = 1ll << d_bits;
+  const int lane = threadIdx.x & 31;
+  long long dum = 0, gmax = kI64Min;
+  for (long long w = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; w < nl;
+       w += (long long)gridDim.x * (kBlock / 32)) {
+    const long long ri = long_rows[w];
+    const long long rb = row_ptr[ri], re = row_ptr[ri + 1];
+    const long long d0 = base_of(row0 + ri, se, k_left);
+    long long cnt = 0;
+    for (long long j = rb + lane; j < re; j += 32) {
+      const long long col = col_idx[j];
+      const long long gap = col - (j == rb ? d0 : (long long)col_idx[j - 1]);
+      cnt += gap >= thr;
+      gmax = gap > gmax ? gap : gmax;
+    }
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    dum += lane == 0 ? cnt : 0;
+    if (lane == 0) counts[ri] = (uint32_t)((re - rb) + cnt);
+  }
+  const long long sd = cta_reduce(dum, AddOp{}, 0ll, sh);
+  const long long sg = cta_reduce(gmax, MaxOp{}, kI64Min, sh);
+  if (threadIdx.x == 0) {
+    if (sd) atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_dummy), (unsigned long long)sd);
     if (sg != kI64Min) atomicMax(&st->max_gap, sg);
   }
 }
@@ -402,6 +462,7 @@ struct FillArgs {
   const int64_t* offset;
   void* pack;
   BuildStats* st;
+  int32_t* long_rows;  // storage rows longer than kLongRow (fill_long_kernel)
   long long n, n_slices, row0, se, k_left;
   int c;
   Fmt f;
@@ -415,13 +476,17 @@ __global__ void __launch_bounds__(kBlock) fill_kernel(FillArgs a) {
   __shared__ long long sh[32];
   const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
   long long bad_nf = kI64Max, bad_of = kI64Max;
+  const long long thr = 1ll << a.f.d;
+  const int sh_v = a.f.d + 1;
+  const long long stride = a.c;
+  // rows longer than kLongRow entries are listed for fill_long_kernel (one warp each)
+  bool lng = false;
   if (s < a.n_slices * a.c) {
     const long long k = s / a.c;
     const int lane = (int)(s - k * a.c);
     const long long o = a.offset[k];
     const long long width = (a.offset[k + 1] - o) / a.c;
     W* out = static_cast<W*>(a.pack) + o + lane;
-    const long long stride = a.c;
     long long q = 0;
     if (s < a.n) {
       const long long r = a.order ? (long long)a.order[s] : s;
@@ -431,9 +496,8 @@ __global__ void __launch_bounds__(kBlock) fill_kernel(FillArgs a) {
         const long long blk = (g / a.se) * a.se;
         return blk > a.k_left ? blk - a.k_left : 0ll;
       }();
-      const long long thr = 1ll << a.f.d;
-      const int sh_v = a.f.d + 1;
-      for (long long j = beg; j < end; ++j) {
+      lng = end - beg > kLongRow;
+      for (long long j = beg; j < (lng ? beg : end); ++j) {
         const long long col = a.col_idx[j];
         long long gap = col - prev;
         prev = col;
@@ -450,7 +514,75 @@ __global__ void __launch_bounds__(kBlock) fill_kernel(FillArgs a) {
         ++q;
       }
     }
-    for (; q < width; ++q) out[q * stride] = W(0);
+    if (!lng)
+      for (; q < width; ++q) out[q * stride] = W(0);
+  }
+  if (lng) a.long_rows[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->n_long), 1ull)] = (int32_t)s;
+  const long long m1 = cta_reduce(bad_nf, MinOp{}, kI64Max, sh);
+  const long long m2 = cta_reduce(bad_of, MinOp{}, kI64Max, sh);
+  if (threadIdx.x == 0) {
+    if (m1 != kI64Max) atomicMin(&a.st->nonfinite_pos, m1);
+    if (m2 != kI64Max) atomicMin(&a.st->overflow_pos, m2);
+  }
+}
+
+// fill of the listed long storage rows: one warp per row, 32 entries per trip, the
+// word positions from a warp prefix sum of (1 + dummy) -- the same words at the
+// same places as the sequential walk of fill_kernel
+template <typename W>
+__global__ void __launch_bounds__(kBlock) fill_long_kernel(FillArgs a) {
+  __shared__ long long sh[32];
+  long long bad_nf = kI64Max, bad_of = kI64Max;
+  const long long thr = 1ll << a.f.d;
+  const int sh_v = a.f.d + 1;
+  const long long stride = a.c;
+  const long long nl = a.st->n_long;
+  const int wl = threadIdx.x & 31;
+  for (long long w = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; w < nl;
+       w += (long long)gridDim.x * (kBlock / 32)) {
+    const long long s = a.long_rows[w];
+    const long long k = s / a.c;
+    const long long o = a.offset[k];
+    const long long width = (a.offset[k + 1] - o) / a.c;
+    W* out = static_cast<W*>(a.pack) + o + (s - k * a.c);
+    const long long r = a.order ? (long long)a.order[s] : s;
+    const long long rb = a.row_ptr[r], re = a.row_ptr[r + 1];
+    const long long d0 = [&] {
+      const long long g = a.row0 + r;
+      const long long blk = (g / a.se) * a.se;
+      return blk > a.k_left ? blk - a.k_left : 0ll;
+    }();
+    long long q0 = 0;  // words stored before this trip
+    for (long long j0 = rb; j0 < re; j0 += 32) {
+      const long long j = j0 + wl;
+      const bool in = j < re;
+      long long gap = 0;
+      W pat = 0;
+      if (in) {
+        const long long col = a.col_idx[j];
+        gap = col - (j == rb ? d0 : (long long)a.col_idx[j - 1]);
+        int stc = ENC_OK;
+        pat = (W)encode_value(a.f, a.values[j], stc);
+        if (stc == ENC_NONFINITE) bad_nf = j < bad_nf ? j : bad_nf;
+        else if (stc == ENC_OVERFLOW) bad_of = j < bad_of ? j : bad_of;
+      }
+      const int dm = in && gap >= thr;
+      int inc = in ? 1 + dm : 0;  // inclusive scan of words per entry
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, sft);
+        if (wl >= sft) inc += t;
+      }
+      if (in) {
+        const long long qr = q0 + inc - 1;  // this entry's real word
+        if (dm) {
+          out[(qr - 1) * stride] = ((W)gap) << 1;
+          gap = 0;
+        }
+        out[qr * stride] = (pat << sh_v) | (((W)gap) << 1) | W(1);
+      }
+      q0 += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    for (long long q = q0 + wl; q < width; q += 32) out[q * stride] = W(0);
   }
   const long long m1 = cta_reduce(bad_nf, MinOp{}, kI64Max, sh);
   const long long m2 = cta_reduce(bad_of, MinOp{}, kI64Max, sh);
@@ -534,7 +666,9 @@ int psell_build_plan(const psell_desc* d, const int64_t* row_ptr, const int32_t*
     if (d->k_left < 0)
       lower_bandwidth_kernel<<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, w.stats);
     row_stats_kernel<<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, se, d->d,
-                                                   w.stats, w.counts);
+                                                   w.stats, w.counts, w.long_rows);
+    row_stats_long_kernel<<<long_grid(), kBlock, 0, st>>>(row_ptr, col_idx, d->row0, se, d->d, w.stats,
+                                                          w.counts, w.long_rows);
   }
   PSELL_CHECK_LAUNCH(err, "row_stats");
   BuildStats hs;
@@ -608,6 +742,7 @@ int psell_build_fill(const psell_desc* d, const int64_t* row_ptr, const int32_t*
   a.offset = offset;
   a.pack = pack;
   a.st = w.stats;
+  a.long_rows = w.long_rows;
   a.n = n;
   a.n_slices = ns;
   a.row0 = d->row0;
@@ -619,8 +754,14 @@ int psell_build_fill(const psell_desc* d, const int64_t* row_ptr, const int32_t*
   const long long rows = ns * d->c;
   if (rows > 0) {
     const unsigned grid = (unsigned)ceil_div(rows, kBlock);
-    if (d->w == 32) fill_kernel<uint32_t><<<grid, kBlock, 0, st>>>(a);
-    else fill_kernel<uint64_t><<<grid, kBlock, 0, st>>>(a);
+    PSELL_CUDA(cudaMemsetAsync(&w.stats->n_long, 0, sizeof(long long), st), err);
+    if (d->w == 32) {
+      fill_kernel<uint32_t><<<grid, kBlock, 0, st>>>(a);
+      fill_long_kernel<uint32_t><<<long_grid(), kBlock, 0, st>>>(a);
+    } else {
+      fill_kernel<uint64_t><<<grid, kBlock, 0, st>>>(a);
+      fill_long_kernel<uint64_t><<<long_grid(), kBlock, 0, st>>>(a);
+    }
     PSELL_CHECK_LAUNCH(err, "fill");
   }
   BuildStats hs;
