@@ -55,6 +55,16 @@ CONFIGS = {
 }
 
 
+def dtype_label(cfg, impl: str) -> str:
+    """The arithmetic the path computes in: x / y storage type and accumulator.  Ours
+    accumulates with FP32 FMA (FP64 for f64 x); the reference (packed.py:268) rounds
+    every product and sum in x's dtype."""
+    x = {"float16": "f16", "float32": "f32", "float64": "f64"}[cfg["xdt"]]
+    if impl == "reference":
+        return f"{x} x/y, {x} accumulate"
+    return f"{x} x/y, {'f64' if x == 'f64' else 'f32'} FMA accumulate"
+
+
 def stencil_k_left(kind: str, nx: int) -> int:
     """Lower bandwidth of the generated matrices (checked against the device in tests)."""
     if kind == "stencil27":
@@ -162,7 +172,39 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU side
-def _cpu_worker(conn, cfg, r0, r1, k_left, seed):
+def _digest(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8)).hexdigest()
+
+
+def _slab_parity(O, M, A, vals, x, expect):
+    """Compare the oracle slab with the GPU's production matrix over the same rows.
+
+    `expect` holds the GPU side: sha256 of the pack words / rebased offsets / perm
+    of the slab's slices in the full device build, and the device REF_ORDER and
+    FMA SpMV outputs on those rows for the same x (SURVEY §8c parity rules 1-3)."""
+    f16 = x.dtype == np.float16
+    y_ref = O.spmv(M, x)
+    y_wide = O.spmv(M, x.astype(np.float32)) if f16 else y_ref
+    q = np.abs(O.quantize(M.fmt, vals))
+    anorm = float(np.max(np.add.reduceat(q, A.row_ptr[:-1]))) if A.nnz else 0.0
+    lmax = int(np.diff(M.offset).max() // M.c)
+    e = float(np.abs(expect["y_fma"].astype(np.float64) - y_wide.astype(np.float64)).max()) / max(
+        anorm * float(np.abs(x.astype(np.float64)).max()), 1e-300)
+    bound = (2.0 ** -11 if f16 else 0.0) + 2 * lmax * 2.0 ** -24
+    res = {"pack": _digest(M.pack) == expect["pack_sha"],
+           "offset": _digest(M.offset) == expect["offset_sha"],
+           "perm": _digest(M.perm) == expect["perm_sha"],
+           "k_left": M.k_left == expect["k_left"],
+           "spmv_ref_order_bitwise": bool(np.array_equal(y_ref.view(np.uint8), expect["y_ref"].view(np.uint8))),
+           "spmv_fma_e_rel": e, "spmv_fma_bound": bound}
+    ok = all(res[k] for k in ("pack", "offset", "perm", "k_left", "spmv_ref_order_bitwise")) and e <= bound
+    res["status"] = "bitwise" if ok else "MISMATCH"
+    res["words_compared"] = int(M.offset[-1])
+    return res
+
+
+def _cpu_worker(conn, cfg, r0, r1, k_left, seed, expect=None):
     os.environ["OMP_NUM_THREADS"] = "1"
     import oracle as O
     from paper_2604_13433_b200.stencil import stencil_rows
@@ -183,7 +225,8 @@ def _cpu_worker(conn, cfg, r0, r1, k_left, seed):
     touched = int(A.col_idx.max()) - int(A.col_idx.min()) + 1 if A.nnz else 0
     nbytes = O.spmv_bytes(M, xsz, xsz) - xsz * A.n_cols + xsz * touched
     x = np.random.default_rng(seed).uniform(-1, 1, A.n_cols).astype(cfg["xdt"])
-    conn.send(("ready", nbytes, A.nnz))
+    parity = None if expect is None else _slab_parity(O, M, A, vals, x, expect)
+    conn.send(("ready", nbytes, A.nnz, parity))
     while True:
         msg = conn.recv()
         if msg == "stop":
@@ -193,8 +236,11 @@ def _cpu_worker(conn, cfg, r0, r1, k_left, seed):
         conn.send(time.perf_counter() - t0)
 
 
-def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: int):
-    """Oracle port of packsell_spmv on `workers` host cores, disjoint slab samples."""
+def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: int, expect=None):
+    """Oracle port of packsell_spmv on `workers` host cores, disjoint slab samples.
+
+    With `expect` (one worker, rows 0..rows_per_worker), the worker also checks the
+    GPU's production matrix and SpMV outputs over its slab against its own build."""
     import multiprocessing as mp
     ctx = mp.get_context("fork")
     n = cfg_rows(cfg)
@@ -206,15 +252,17 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
     for w in range(workers):
         a, b = mp.Pipe()
         r0 = w * stride
-        p = ctx.Process(target=_cpu_worker, args=(b, cfg, r0, min(n, r0 + rows_per_worker), kl, 7 + w))
+        p = ctx.Process(target=_cpu_worker, args=(b, cfg, r0, min(n, r0 + rows_per_worker), kl, 7 + w,
+                                                  expect if w == 0 else None))
         p.start()
         procs.append(p)
         conns.append(a)
-    tot_bytes, tot_nnz = 0, 0
+    tot_bytes, tot_nnz, parity = 0, 0, None
     for c in conns:
-        _, nb, nz = c.recv()
+        _, nb, nz, par = c.recv()
         tot_bytes += nb
         tot_nnz += nz
+        parity = parity or par
     times = []
     for it in range(warmup + steps):
         t0 = time.perf_counter()
@@ -230,7 +278,7 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
         p.join()
     t = float(np.mean(times))
     return dict(gbs=tot_bytes / t / 1e9, gflops=2 * tot_nnz / t / 1e9, sec_per_step=t, workers=workers,
-                rows=rows_per_worker, bytes=tot_bytes, nnz=tot_nnz)
+                rows=rows_per_worker, bytes=tot_bytes, nnz=tot_nnz, parity=parity)
 
 
 def run_reference(args, cfg):
@@ -244,7 +292,7 @@ def run_reference(args, cfg):
     line = {
         "metric": METRIC, "value": r["gbs"], "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["sec_per_step"] * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16" if cfg["xdt"] == "float16" else "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_label(cfg, "reference"),
         "data": "synthetic", "config": {"workload": cfg["workload"], "cpu_sample": sample},
         "gflops": r["gflops"],
         "cpu_baseline": {"value": r["gbs"], "unit": "GB/s", "cores": r["workers"], "kind": "port",
@@ -362,6 +410,25 @@ def run_pcg(args, world, rank, comm, peak):
 
 
 # ----------------------------------------------------------------------------- GPU side
+def gpu_slab_expect(M, cfg, rows, seed):
+    """GPU side of the bench-line parity block: digests of the production matrix over
+    storage rows 0..rows-1 and the device SpMV outputs on those rows for the CPU
+    sample's x (generated identically on the host)."""
+    import torch
+    from paper_2604_13433_b200 import _dev
+    import paper_2604_13433_b200 as P
+    s1 = rows // M.c
+    off = M.offset
+    x = np.random.default_rng(seed).uniform(-1, 1, M.n_cols).astype(cfg["xdt"])
+    xd = torch.from_numpy(x).cuda()
+    y_ref = P.packsell_spmv(M, xd, ref_order=True)[:rows].cpu().numpy()
+    y_fma = P.packsell_spmv(M, xd)[:rows].cpu().numpy()
+    return {"pack_sha": _digest(_dev.download(M.d_pack[:off[s1]], M.fmt.word_dtype)),
+            "offset_sha": _digest(off[:s1 + 1]),
+            "perm_sha": _digest(M.perm[:rows]),
+            "k_left": M.k_left, "y_ref": y_ref, "y_fma": y_fma}
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -575,9 +642,15 @@ def run_ours(args, cfg):
     achieved = bytes_local / (ms_local * 1e-3) / 1e9
     clocks = sampler.summary()
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference(cfg, 1, args.cpu_rows, 3, 1)
+        rows = max(sig, args.cpu_rows // sig * sig)
+        expect = gpu_slab_expect(M, cfg, rows, 7)
+        r = cpu_reference(cfg, 1, args.cpu_rows, 3, 1, expect=expect)
+        parity = r["parity"]
+        parity["sample"] = (f"rows 0..{rows - 1} of the benchmarked matrix: the GPU production build's words / "
+                            f"offsets / perm over those slices and its SpMV outputs on those rows vs the oracle "
+                            f"slab (global k_left)")
         cpu = {"value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": "port",
                "sample": f"{r['rows']} rows (rows 0..{r['rows'] - 1}, {r['nnz']} nnz) of the same matrix, "
                          f"global k_left; oracle port of packsell_spmv, numpy single thread; "
@@ -598,7 +671,7 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": dtype_label(cfg, "ours"), "data": "synthetic",
             "config": {"workload": cfg["workload"], "n": n, "nnz": int(nnz_all),
                        "n_stored_rank0": m_info[0], "counts_rank0": m_info[1], "k_left": kl,
                        "partition": "sigma-aligned row slabs, x replicated (no collective in the step)",
@@ -616,6 +689,7 @@ def run_ours(args, cfg):
                          "kernel": f"{kernel_name} ({launches_per_step} launch(es) per step; traffic = ncu "
                                    "DRAM bytes per launch of the SpMV kernel)"},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": h2d_b,
                     "d2h_bytes_per_step": d2h_b,
