@@ -290,7 +290,8 @@ def run_reference(args, cfg):
     sample = (f"{r['workers']} worker processes x {r['rows']} rows ({r['nnz']} nnz total) of the same matrix, "
               f"sigma-aligned slabs, global k_left; oracle port of packsell_spmv (numpy, 1 thread each)")
     line = {
-        "metric": METRIC, "value": r["gbs"], "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+        "metric": METRIC, "value": r["gbs"], "unit": "GB/s", "impl": "reference",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["sec_per_step"] * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_label(cfg, "reference"),
         "data": "synthetic", "config": {"workload": cfg["workload"], "cpu_sample": sample},
@@ -387,8 +388,12 @@ def run_pcg(args, world, rank, comm, peak):
         "speedup_iocg_vs_fp32_sell_iocg": None if t_32 is None else t_32 / t_io,
         "build_s": t_build,
         "collectives": "none" if world == 1 else (
-            "NCCL point-to-point halo exchange of p (f32 inner, f64 outer; K7 pack/unpack, "
-            "dist.Halo) + all-gather of the FP64 per-rank dot sums (rank-ordered)"),
+            "peer-memory transport (K8, csrc/peer.cu): one kernel per exchange pushes the halo of p (f32 inner, "
+            "f64 outer) into the peers' vectors over NVLink and all-gathers the FP64 per-rank dot sums "
+            "(rank-ordered sums); the distributed inner iteration is one CUDA graph per outer step"
+            if comm.peer(n) is not None else
+            "torch.distributed: point-to-point halo exchange of p (K7 pack/unpack, dist.Halo) + all-gather of the "
+            "FP64 per-rank dot sums (rank-ordered), eager"),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
@@ -714,6 +719,16 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def spawn_ranks(n: int) -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -731,6 +746,10 @@ def main():
     ap.add_argument("--pcg-m-in", type=int, default=50)
     ap.add_argument("--pcg-cpu-nx", type=int, default=32)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: one process per GPU, launched here the way the
+        # driver launches N > 1 (torch.distributed.run, rendezvous on 127.0.0.1)
+        sys.exit(spawn_ranks(args.gpus))
     cfg = dict(CONFIGS[args.config])
     if args.sigma:
         cfg["sigma"] = args.sigma

@@ -377,6 +377,34 @@ PSELL_API int psell_halo_pack(int64_t n, const void* src, const int32_t* idx, vo
 PSELL_API int psell_halo_unpack(int64_t n, const void* src, const int64_t* idx, void* dst, int32_t elem_bytes,
                                 void* stream);
 
+/* ---- K8 peer-memory exchange: the distributed PCG's halo
+ * exchange and FP64 dot all-gather as ONE kernel over NVLink peer memory, so the
+ * distributed inner iteration is CUDA-graph capturable (csrc/peer.cu).  The
+ * reference is single-process (solvers.py:278-308 runs on one vector); this
+ * replaces the NCCL all-gather / all-reduce north_star names for those steps.
+ * Every rank allocates one arena (psell_peer_alloc), exports its IPC handle,
+ * maps the others' (psell_peer_open) and passes the G arena bases as a device
+ * array `peers` (peers[rank] = its own).  Arena layout: see csrc/peer.cu. */
+#define PSELL_PEER_HDR_BYTES 12288
+#define PSELL_PEER_HANDLE_BYTES 64
+PSELL_API size_t psell_peer_arena_bytes(int64_t n_cols);
+/* byte offset of the full-length f32 (elem_bytes 4) or f64 (8) vector inside an arena */
+PSELL_API int64_t psell_peer_vec_offset(int64_t n_cols, int32_t elem_bytes);
+PSELL_API int psell_peer_alloc(size_t bytes, void** out_ptr, void* out_handle /* 64 B */);
+PSELL_API int psell_peer_open(const void* handle, void** out_ptr);
+PSELL_API int psell_peer_close(void* ptr);
+PSELL_API int psell_peer_free(void* ptr);
+/* Push local[send_local[i]] to peer send_dst[i]'s vector at global row0 + send_local[i]
+ * (elem_bytes 4 | 8, vector at vec_off in every arena), push loc[0..n_loc) (n_loc <= 8)
+ * to every rank, signal, wait for every rank (timeout_ns), then
+ * out[q*8 + k] = rank q's loc[k] (rank order).  Stream ordered, no host sync. */
+PSELL_API int psell_peer_exchange(int32_t G, int32_t rank, const uint64_t* peers, int64_t n_send,
+                                  const int32_t* send_dst, const int32_t* send_local, int64_t row0,
+                                  const void* local, int32_t elem_bytes, int64_t vec_off, const double* loc,
+                                  int32_t n_loc, double* out, int64_t timeout_ns, void* stream);
+/* *out_host <- the arena's error word (nonzero: a wait timed out). Synchronous. */
+PSELL_API int psell_peer_error(const void* arena, int32_t* out_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,15 @@ _SIGS = {
     "psell_csr_spmv_dot": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _E]),
     "psell_halo_pack": (c_int32, [c_int64, _P, _P, _P, c_int32, _P]),
     "psell_halo_unpack": (c_int32, [c_int64, _P, _P, _P, c_int32, _P]),
+    "psell_peer_arena_bytes": (c_size_t, [c_int64]),
+    "psell_peer_vec_offset": (c_int64, [c_int64, c_int32]),
+    "psell_peer_alloc": (c_int32, [c_size_t, POINTER(c_void_p), _P]),
+    "psell_peer_open": (c_int32, [_P, POINTER(c_void_p)]),
+    "psell_peer_close": (c_int32, [_P]),
+    "psell_peer_free": (c_int32, [_P]),
+    "psell_peer_exchange": (c_int32, [c_int32, c_int32, _P, c_int64, _P, _P, c_int64, _P, c_int32, c_int64, _P,
+                                      c_int32, _P, c_int64, _P]),
+    "psell_peer_error": (c_int32, [_P, POINTER(c_int32)]),
     "psell_backward_error": (c_int32, [c_int64, c_int64, _P, _P, _P, _P, c_int32, _P, c_int32, _P, _P, _E]),
     "psell_sum_partials": (c_int32, [_P, c_int64, c_int32, _P, _P, _P]),
     "psell_sum_strided": (c_int32, [_P, c_int32, c_int32, c_int32, _P, _P]),

@@ -70,6 +70,154 @@ class Comm:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def slabs(self, row0: int, n: int) -> List[Tuple[int, int]]:
+        """Every rank's (row0, row1), in rank order (host all-gather, setup only)."""
+        out = [None] * self.world
+        self.dist.all_gather_object(out, (int(row0), int(row0) + int(n)), group=self.group)
+        return [tuple(map(int, s)) for s in out]
+
+    def peer(self, n_cols: int):
+        """The peer-memory transport for vectors of n_cols entries, or None.
+
+        Used when the ranks share a node and CUDA IPC works: by default on NCCL
+        process groups, and on any group with PSELL_XPORT=peer (several ranks
+        sharing one GPU over gloo, the tests); PSELL_XPORT=nccl keeps the NCCL
+        collectives (A/B)."""
+        import os
+        mode = os.environ.get("PSELL_XPORT", "auto")
+        if mode == "nccl" or (mode == "auto" and not self.nccl):
+            return None
+        cache = self.__dict__.setdefault("_peers", {})
+        if n_cols not in cache:
+            cache[n_cols] = PeerTransport(self, n_cols)
+        return cache[n_cols]
+
+    def close(self):
+        """Release the peer arenas (collective)."""
+        for t in self.__dict__.pop("_peers", {}).values():
+            t.close()
+
+
+class _CudaView:
+    """__cuda_array_interface__ over raw device memory (arena views as torch tensors)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerTransport:
+    """One-kernel collectives over NVLink peer memory (csrc/peer.cu, K8).
+
+    Each rank allocates an arena holding the exchange flags, the FP64 dot
+    slots and the full-length f32 / f64 vectors, exports it through a CUDA IPC
+    handle and maps every peer's.  `exchange` then pushes this rank's halo
+    entries straight into the peers' full vectors and its local dot sums into
+    their dot slots, signals, waits, and leaves the rank-ordered dot sums in
+    `out` — one stream-ordered kernel, so the distributed inner PCG iteration
+    is a kernel chain captured in one CUDA graph (no NCCL call, no host wait).
+    """
+
+    def __init__(self, comm: "Comm", n_cols: int):
+        import ctypes
+        import os
+
+        import torch
+        from . import _lib
+        self.comm, self.n_cols = comm, int(n_cols)
+        self.lib = lib = _lib.lib()
+        self.G, self.rank = comm.world, comm.rank
+        self.timeout_ns = int(float(os.environ.get("PSELL_PEER_TIMEOUT_S", "60")) * 1e9)
+        nbytes = lib.psell_peer_arena_bytes(self.n_cols)
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        if lib.psell_peer_alloc(nbytes, ctypes.byref(ptr), handle):
+            raise _lib.LibpsellError("psell_peer_alloc failed (cudaMalloc / cudaIpcGetMemHandle)")
+        self.arena = int(ptr.value)
+        handles = [None] * self.G
+        comm.dist.all_gather_object(handles, bytes(handle), group=comm.group)
+        bases, self._opened = [], []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                bases.append(self.arena)
+                continue
+            p = ctypes.c_void_p()
+            hb = (ctypes.c_char * 64).from_buffer_copy(h)
+            if lib.psell_peer_open(hb, ctypes.byref(p)):
+                raise _lib.LibpsellError(f"psell_peer_open of rank {r}'s arena failed (CUDA IPC)")
+            bases.append(int(p.value))
+            self._opened.append(int(p.value))
+        self.d_peers = torch.tensor(bases, dtype=torch.int64, device="cuda")
+        off32 = lib.psell_peer_vec_offset(self.n_cols, 4)
+        off64 = lib.psell_peer_vec_offset(self.n_cols, 8)
+        self.vec_off = {4: off32, 8: off64}
+        self.full32 = torch.as_tensor(_CudaView(self.arena + off32, self.n_cols, "<f4"), device="cuda")
+        self.full64 = torch.as_tensor(_CudaView(self.arena + off64, self.n_cols, "<f8"), device="cuda")
+        self._plans = {}
+        torch.cuda.synchronize()
+        comm.barrier()
+
+    def full(self, dtype):
+        """The arena's full-length vector of `dtype` (f32 inner / f64 outer)."""
+        import torch
+        return self.full32 if dtype == torch.float32 else self.full64
+
+    def plan(self, halo: "Halo", row0: int, n_local: int):
+        """Device (dst rank, local index) lists of the entries this rank pushes: the halo
+        plan's send lists, or its whole slab to every peer when the plan falls back to
+        the all-gather (irregular matrices)."""
+        key = None if halo is None else id(halo)
+        if key not in self._plans:
+            import torch
+            if halo is not None and not halo.use_allgather:
+                dst = np.concatenate([np.full(len(v), s, np.int32) for s, v in enumerate(halo.send_lists)]
+                                     + [np.zeros(0, np.int32)])
+                loc = halo.send_idx.astype(np.int32)
+            else:
+                peers = [s for s in range(self.G) if s != self.rank]
+                dst = np.repeat(np.asarray(peers, np.int32), n_local)
+                loc = np.tile(np.arange(n_local, dtype=np.int32), len(peers))
+            self._plans[key] = (torch.as_tensor(dst).cuda(), torch.as_tensor(loc).cuda(), int(row0), len(dst))
+        return self._plans[key]
+
+    def exchange(self, local=None, plan=None, loc=None, n_loc: int = 0, out=None):
+        """Push `local`'s planned entries and loc[:n_loc], wait for all ranks, out <- dot sums."""
+        from . import _lib
+        if plan is not None:
+            dst, li, row0, n_send = plan
+            es = local.element_size()
+            rc = self.lib.psell_peer_exchange(self.G, self.rank, self.d_peers.data_ptr(), n_send, dst.data_ptr(),
+                                              li.data_ptr(), row0, local.data_ptr(), es, self.vec_off[es],
+                                              None if loc is None else loc.data_ptr(), n_loc,
+                                              None if out is None else out.data_ptr(), self.timeout_ns,
+                                              _lib.stream_handle())
+        else:
+            rc = self.lib.psell_peer_exchange(self.G, self.rank, self.d_peers.data_ptr(), 0, None, None, 0, None,
+                                              8, 0, loc.data_ptr(), n_loc, out.data_ptr(), self.timeout_ns,
+                                              _lib.stream_handle())
+        if rc:
+            raise _lib.LibpsellError(f"psell_peer_exchange failed ({rc})")
+
+    def check(self):
+        """Raise if any exchange of this rank timed out waiting for a peer."""
+        import ctypes
+        from . import _lib
+        v = ctypes.c_int32(0)
+        if self.lib.psell_peer_error(self.arena, ctypes.byref(v)) or v.value:
+            raise _lib.LibpsellError("peer exchange timed out waiting for a rank (PSELL_PEER_TIMEOUT_S)")
+
+    def close(self):
+        import torch
+        torch.cuda.synchronize()
+        self.comm.barrier()
+        for p in self._opened:
+            self.lib.psell_peer_close(p)
+        self._opened = []
+        self.comm.barrier()
+        if self.arena:
+            self.lib.psell_peer_free(self.arena)
+            self.arena = 0
+
 
 class Halo:
     """Point-to-point halo plan of one row-partitioned operator (built once, collectively).
@@ -85,7 +233,7 @@ class Halo:
     solvers keep the all-gather.
     """
 
-    def __init__(self, comm: "Comm", row0: int, row1: int, needed, max_frac: float = 0.5):
+    def __init__(self, comm: "Comm", row0: int, row1: int, needed, max_frac: float = 0.5, n_cols: int = None):
         self.comm = comm
         self.row0, self.row1 = int(row0), int(row1)
         needed = np.unique(np.asarray(needed, dtype=np.int64))
@@ -108,6 +256,12 @@ class Halo:
         self.use_allgather = max(tot) > max_frac * max(n_remote, 1)
         self.send_idx = np.concatenate(self.send_lists + [np.zeros(0, np.int64)]) - self.row0
         self.recv_idx = np.concatenate(self.recv_lists + [np.zeros(0, np.int64)])
+        # every index lands inside the full-length vector and the own slab
+        n_full = n_glob if n_cols is None else int(n_cols)
+        if self.recv_idx.size and (self.recv_idx.min() < 0 or self.recv_idx.max() >= n_full):
+            raise ValueError(f"halo column outside [0, {n_full}): the slabs do not cover the columns read")
+        if self.send_idx.size and (self.send_idx.min() < 0 or self.send_idx.max() >= self.row1 - self.row0):
+            raise ValueError("a peer requested a column outside this rank's slab")
         self._dev = None
 
     @property
@@ -221,4 +375,4 @@ def rank_order_sum(parts: np.ndarray) -> float:
     return s
 
 
-__all__ = ["Comm", "Halo", "equal_row_slabs", "check_equal", "word_balanced_slabs", "rank_order_sum"]
+__all__ = ["Comm", "PeerTransport", "Halo", "equal_row_slabs", "check_equal", "word_balanced_slabs", "rank_order_sum"]

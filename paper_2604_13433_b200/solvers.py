@@ -182,6 +182,7 @@ class _Dev:
         self.L = _lib
         self.comm = comm
         self.G = 1 if comm is None else comm.world
+        self.peer = None  # dist.PeerTransport: gathers become one peer-memory kernel
         np_ = max(int(n_partials), 2 * _lib.RED_BLOCKS)
         self.partials = torch.zeros(np_ + -(-np_ // 32) + 8, dtype=torch.float64, device="cuda")
         self.loc = torch.zeros(8, dtype=torch.float64, device="cuda")
@@ -202,7 +203,10 @@ class _Dev:
         """(pointer base, stride) of every rank's loc[] in rank order."""
         if self.G == 1:
             return self.loc, 8
-        self.comm.all_gather_into(self.glob, self.loc)
+        if self.peer is not None:
+            self.peer.exchange(loc=self.loc, n_loc=8, out=self.glob)
+        else:
+            self.comm.all_gather_into(self.glob, self.loc)
         return self.glob, 8
 
     def reduce(self, k0: int, n_out: int, dst: int):
@@ -231,13 +235,18 @@ class _Dev:
         return float(np.sqrt(float(self.scal[slot].item())))
 
 
-def _gather_full(comm, local, full, halo=None):
+def _gather_full(comm, local, full, halo=None, peer=None, row0: int = 0):
     """Entries of `full` the slab's rows read <- their owners' values.
 
-    With a halo plan (dist.Halo): point-to-point exchange of the
-    boundary columns only; otherwise the in-place all-gather of equal slabs."""
+    With the peer transport, `full` is its arena vector and every rank pushes the
+    entries its peers read straight into theirs (one kernel, K8).  Otherwise, with
+    a halo plan (dist.Halo): NCCL point-to-point exchange of the
+    boundary columns only; else the in-place all-gather of equal slabs."""
     if comm is None or comm.world == 1:
         return local
+    if peer is not None:
+        peer.exchange(local, peer.plan(halo, row0, local.numel()))
+        return full
     if halo is not None and not halo.use_allgather:
         return halo.exchange(full, local)
     comm.all_gather_vec(full, local)
@@ -255,8 +264,20 @@ def _halo_for(comm, src):
         import torch
         from .dist import Halo
         needed = torch.unique(D.col_idx).cpu().numpy() if D.nnz else np.zeros(0, np.int64)
-        cache[id(comm)] = Halo(comm, D.row0, D.row0 + D.n_rows, needed)
+        cache[id(comm)] = Halo(comm, D.row0, D.row0 + D.n_rows, needed, n_cols=D.n_cols)
     return cache[id(comm)]
+
+
+def _check_slabs(comm, row0: int, n: int, halo, peer):
+    """The NCCL all-gather path places rank r's chunk at r * n: it needs equal, rank-ordered
+    slabs.  The halo exchanges and the peer transport address entries by
+    global index and take any sigma-aligned partition."""
+    if comm is None or comm.world == 1 or peer is not None or (halo is not None and not halo.use_allgather):
+        return
+    slabs = comm.slabs(row0, n)
+    if any(s != (r * n, (r + 1) * n) for r, s in enumerate(slabs)):
+        raise ValueError(f"the all-gather transport needs equal rank-ordered row slabs, got {slabs}; use the "
+                         "halo exchange or the peer transport for other partitions")
 
 
 # ----------------------------------------------------------------------------
@@ -280,6 +301,8 @@ class _InnerPCG:
         self.M = M
         self.n = M.n_rows
         self.row0 = M.row0
+        self.peer = None if comm is None or comm.world == 1 else comm.peer(M.n_cols)
+        _check_slabs(comm, self.row0, self.n, self.halo, self.peer)
         self.inv = inv_diag
         f32 = torch.float32
         self.x = torch.zeros(self.n, dtype=f32, device="cuda")
@@ -291,15 +314,18 @@ class _InnerPCG:
             self.p_full = torch.zeros(self.n, dtype=f32, device="cuda")
             self.p = self.p_full
         else:
-            self.p_full = torch.zeros(comm.padded_len(M.n_cols), dtype=f32, device="cuda")
+            self.p_full = self.peer.full32 if self.peer is not None else \
+                torch.zeros(M.n_cols, dtype=f32, device="cuda")
             self.p = self.p_full[self.row0:self.row0 + self.n]
         lib = _lib.lib()
         self.desc = M.desc()
         self.npart = lib.psell_spmv_dot_partials(self.desc, M.spmv_flags())
         self.d = _Dev(max(self.npart, _lib.RED_BLOCKS), comm)
+        self.d.peer = self.peer
         self.graph = None
         self.graph_in = None
-        self.use_graph = use_graph and G == 1
+        # one GPU, or ranks joined by the peer transport: the inner loop is kernels only
+        self.use_graph = use_graph and (G == 1 or self.peer is not None)
         self._io = None
         # outer-loop gate (fcg look-ahead): nonzero turns the whole inner solve into a no-op
         self.gate = torch.zeros(2, dtype=torch.int32, device="cuda")
@@ -341,7 +367,7 @@ class _InnerPCG:
             lib.psell_ipcg_end(self.n, self.x.data_ptr(), z64.data_ptr(), st)
             return
         for _ in range(self.m_in):
-            _gather_full(self.comm, self.p, self.p_full, self.halo)
+            _gather_full(self.comm, self.p, self.p_full, self.halo, self.peer, self.row0)
             rc = lib.psell_spmv_dot(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
                                     self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
                                     d.p(d.partials), d.p(d.flags), M.spmv_flags(), st, err)
@@ -550,8 +576,15 @@ class _Outer:
         self.d = _Dev(_lib.RED_BLOCKS, comm)
         self.lib = self.d.lib
         f64 = torch.float64
-        self.n_glob = self.n * self.G
-        self.full = torch.zeros(self.n_glob, dtype=f64, device="cuda") if self.G > 1 else None
+        self.n_glob = src.n_cols
+        self.peer = comm.peer(self.n_glob) if self.G > 1 else None
+        self.d.peer = self.peer
+        _check_slabs(comm, self.row0, self.n, self.halo, self.peer)
+        if self.G == 1:
+            self.full = None
+        else:
+            self.full = self.peer.full64 if self.peer is not None else \
+                torch.zeros(self.n_glob, dtype=f64, device="cuda")
 
     def vec(self):
         return self.torch.zeros(self.n, dtype=self.torch.float64, device="cuda")
@@ -564,7 +597,7 @@ class _Outer:
         if self.G == 1:
             return self.backend.apply_into(v, out)
         self.slab_of_full().copy_(v)
-        _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
+        _gather_full(self.comm, self.slab_of_full(), self.full, self.halo, self.peer, self.row0)
         return self.backend.apply_into(self.full, out)
 
     def apply_pq(self, p, q, slot: int) -> bool:
@@ -576,7 +609,7 @@ class _Outer:
         x = p
         if self.G > 1:
             self.slab_of_full().copy_(p)
-            x = _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
+            x = _gather_full(self.comm, self.slab_of_full(), self.full, self.halo, self.peer, self.row0)
         L, d = self.d.L, self.d
         err = L.PsellError()
         rc = self.lib.psell_csr_spmv_dot(D.n_rows, L.ptr(D.row_ptr), L.ptr(D.col_idx), L.ptr(D.values),
@@ -597,11 +630,13 @@ class _Outer:
             csr_spmv(src, x, np.float64, out=ax)
         else:
             self.slab_of_full().copy_(x)
-            _gather_full(self.comm, self.slab_of_full(), self.full, self.halo)
+            _gather_full(self.comm, self.slab_of_full(), self.full, self.halo, self.peer, self.row0)
             csr_spmv(src, self.full, np.float64, out=ax)
         self.lib.psell_resid(self.n, self.b.data_ptr(), ax.data_ptr(), d.p(d.partials), d.p(d.loc, 6), d.st())
         d.reduce(6, 1, 14)
         report.final_true_relres = float(np.sqrt(float(d.scal[14].item()))) / bnorm
+        if self.peer is not None:
+            self.peer.check()
         if report.converged and not report.final_true_relres < 10.0 * tol:
             report.converged = False
             msg = f"true residual {report.final_true_relres:.3e} exceeds 10x tolerance"

@@ -91,3 +91,86 @@ def test_distributed_iocg_matches_single_gpu(world):
         xp[r0:r1] = pxs
     assert np.abs(x - ref.x).max() / np.abs(ref.x).max() < 1e-6
     assert np.abs(xp - refp.x).max() / np.abs(refp.x).max() < 1e-9
+
+
+def _rank_peer(rank, world, port, nx, slabs, q):
+    """Same solves over the peer-memory transport (K8: CUDA IPC arenas, one exchange
+    kernel, graph-captured inner loop) next to the gloo-staged collectives."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["PSELL_PEER_TIMEOUT_S"] = "120"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_13433_b200 as P
+        from paper_2604_13433_b200 import dist as D
+        from paper_2604_13433_b200 import solvers as S
+        from paper_2604_13433_b200.packed import lower_bandwidth
+        torch.cuda.set_device(0)
+        comm = D.Comm()
+        n = nx ** 3
+        r0, r1 = slabs[rank]
+        b, _ = S.make_rhs_and_x0(n, 42)
+        cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200)
+        out = {}
+        for xport in ("nccl", "peer"):   # "nccl" = the torch.distributed collectives (gloo here)
+            os.environ["PSELL_XPORT"] = xport
+            A = P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1)
+            kl = comm.allreduce_max(lower_bandwidth(A))
+            be = S.make_backend(A, "packsell-e8m14", k_left=kl)
+            rep = S.iocg(A, b[r0:r1], cfg, backend=be, comm=comm)
+            inner = next(iter(be._inner_cache.values()))
+            rep2 = S.iocg(A, b[r0:r1], cfg, backend=be, comm=comm)  # graph replay
+            pc = S.pcg(P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1), b[r0:r1],
+                       S.SolveConfig(tol=1e-9, max_outer=2000), comm=comm)
+            out[xport] = (rep.converged, rep.outer_iters, rep.total_inner_iters, rep.final_true_relres, rep.x,
+                          rep2.x, pc.converged, pc.outer_iters, pc.x, inner.use_graph, inner.peer is not None)
+        comm.close()
+        q.put((rank, r0, r1, out))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("split", ["equal", "unequal"])
+def test_peer_transport_matches_collectives_and_single_gpu(split):
+    """2 ranks on one GPU: the peer-memory path (graph-captured distributed inner loop)
+    gives the same x bit for bit as the collective path, on equal and unequal slabs."""
+    import torch.multiprocessing as mp
+    import paper_2604_13433_b200 as P
+    from paper_2604_13433_b200 import solvers as S
+    nx, world = 16, 2
+    n = nx ** 3
+    slabs = [(0, n // 2), (n // 2, n)] if split == "equal" else [(0, 1280), (1280, n)]
+    A = P.sym_diag_scale(P.poisson3d(nx))
+    b, _ = S.make_rhs_and_x0(n, 42)
+    ref = S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200))
+    refp = S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=2000))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_rank_peer, args=(r, world, port, nx, slabs, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=900) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+    assert all(len(r) == 4 for r in res), res
+    x, xp = np.zeros(n), np.zeros(n)
+    for rank, r0, r1, out in res:
+        cg = out["nccl"]
+        pe = out["peer"]
+        assert pe[9] and pe[10], "peer transport + CUDA graph not used"
+        assert not cg[10]
+        assert pe[0] and pe[1] == cg[1] and pe[2] == cg[2] and pe[3] < 1e-9
+        assert np.array_equal(pe[4], cg[4]) and np.array_equal(pe[5], pe[4])
+        assert pe[6] and pe[7] == cg[7] and np.array_equal(pe[8], cg[8])
+        assert abs(pe[1] - ref.outer_iters) <= 1
+        x[r0:r1] = pe[4]
+        xp[r0:r1] = pe[8]
+    assert np.abs(x - ref.x).max() / np.abs(ref.x).max() < 1e-6
+    assert np.abs(xp - refp.x).max() / np.abs(refp.x).max() < 1e-9
