@@ -189,6 +189,11 @@ PSELL_API size_t psell_to_csr_workspace_bytes(const psell_desc* desc);
 PSELL_API int psell_to_csr_plan(const psell_desc* desc, const void* pack, const int64_t* offset,
                       const void* perm, void* workspace, size_t ws_bytes, int64_t* row_ptr,
                       int64_t* nnz_host, void* stream, psell_error* err);
+/* Largest column a real (flag = 1) word addresses, walking every storage row from the
+ * SpMV's clamped start (packed.py:257); 0 when there is none.  ws8: 8 bytes of device
+ * scratch.  Synchronises.  read_psell rejects containers whose streams reach n_cols. */
+PSELL_API int psell_max_column(const psell_desc* desc, const void* pack, const int64_t* offset, const void* perm,
+                               int64_t* out_host, void* ws8, void* stream, psell_error* err);
 PSELL_API int psell_to_csr_fill(const psell_desc* desc, const void* pack, const int64_t* offset,
                       const void* perm, const int64_t* row_ptr, int32_t* col_idx, double* values,
                       void* stream, psell_error* err);

@@ -66,6 +66,7 @@ _SIGS = {
     "psell_to_csr_workspace_bytes": (c_size_t, [_D]),
     "psell_to_csr_plan": (c_int32, [_D, _P, _P, _P, _P, c_size_t, _P, POINTER(c_int64), _P, _E]),
     "psell_to_csr_fill": (c_int32, [_D, _P, _P, _P, _P, _P, _P, _P, _E]),
+    "psell_max_column": (c_int32, [_D, _P, _P, _P, POINTER(c_int64), _P, _P, _E]),
     "psell_encode": (c_int32, [_D, _P, c_int64, _P, _P, _P, _E]),
     "psell_decode": (c_int32, [_D, _P, c_int64, _P, _P, _E]),
     "psell_pack_words": (c_int32, [_D, _P, _P, _P, c_int64, _P, _P, _E]),

@@ -147,6 +147,7 @@ def read_psell(source: Union[str, Path, BinaryIO]) -> PackSellMatrix:
             pdt = perm_dtype(sigma)
             perm_raw = _read_exact(f, pdt.itemsize * n_rows, "perm array", into=_pinned(pdt.itemsize * n_rows))
         n_words = int(offset[-1]) if len(offset) else 0
+        _check_device_safe(fmt, c, sigma, mode, n_rows, n_cols, k_left, n_slices, offset, perm_raw)
         wdt = fmt.word_dtype
         pack_raw = _read_exact(f, wdt.itemsize * n_words, "pack array", into=_pinned(wdt.itemsize * n_words))
         if nnz + n_dummy + n_pad != n_words:
@@ -155,8 +156,50 @@ def read_psell(source: Union[str, Path, BinaryIO]) -> PackSellMatrix:
     finally:
         if own:
             f.close()
-    return _upload(n_rows, n_cols, c, sigma, mode, fmt, pack_raw, offset, perm_raw, k_left,
-                   StorageCounts(nnz, n_dummy, n_pad))
+    M = _upload(n_rows, n_cols, c, sigma, mode, fmt, pack_raw, offset, perm_raw, k_left,
+                StorageCounts(nnz, n_dummy, n_pad))
+    _check_stream_columns(M)
+    return M
+
+
+def _check_device_safe(fmt, c, sigma, mode, n_rows, n_cols, k_left, n_slices, offset, perm_raw):
+    """Layout facts the reference's builder guarantees and the device kernels rely on.
+
+    The reference reader checks only the counts (container.py:96-98) and its numpy
+    SpMV would raise IndexError on a corrupt perm or column; on the device the same
+    file would read or write out of bounds, so it is rejected here."""
+    if fmt.codec == "fp16" and fmt.w != 32:
+        raise ContainerError("fp16 values need 32-bit words on the device")
+    if c < 1 or n_rows < 0 or n_cols < 0 or k_left < 0:
+        raise ContainerError("header has a negative size or slice height")
+    if n_rows >= 2 ** 31 or n_cols >= 2 ** 31:
+        raise ContainerError(f"matrix of {n_rows} x {n_cols} exceeds 32-bit row / column indexing")
+    if n_slices != -(-n_rows // c):
+        raise ContainerError(f"header has {n_slices} slices, {n_rows} rows need {-(-n_rows // c)} of height {c}")
+    if len(offset) and np.any(offset % c):
+        raise ContainerError(f"offset array holds a slice start that is not a multiple of C = {c}")
+    if perm_raw is not None and n_rows:
+        perm = np.frombuffer(perm_raw, dtype=perm_dtype(sigma)).astype(np.int64)
+        lim = np.minimum(sigma, n_rows - (np.arange(n_rows) // sigma) * sigma)
+        bad = np.nonzero(perm >= lim)[0]
+        if bad.size:
+            raise ContainerError(f"perm[{bad[0]}] = {perm[bad[0]]} points outside its sigma-block")
+
+
+def _check_stream_columns(M):
+    """Every real word's column < n_cols (one device pass, psell_max_column)."""
+    import ctypes
+    from . import _dev, _lib
+    if M.n_stored == 0:
+        return
+    ws = _dev.workspace(8)
+    out = ctypes.c_int64(0)
+    err = _lib.PsellError()
+    rc = _lib.lib().psell_max_column(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                                     ctypes.byref(out), _lib.ptr(ws), _lib.stream_handle(), err)
+    _lib.check(rc, err, M.fmt)
+    if M.counts.nnz_real and out.value >= M.n_cols:
+        raise ContainerError(f"packed stream addresses column {out.value}, beyond n_cols = {M.n_cols}")
 
 
 def _upload(n_rows, n_cols, c, sigma, mode, fmt, pack_raw, offset, perm_raw, k_left, counts):

@@ -596,6 +596,7 @@ static int check_desc(const psell_desc* d, psell_error* err) {
   if (!d) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null descriptor");
   if (!fmt_valid(fmt_of(d)))
     return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid PackFormat");
+  if (!fmt_device_ok(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, PSELL_FP16_W64_MSG);
   if (d->mode < PSELL_MODE_NONE || d->mode > PSELL_MODE_IMPLICIT)
     return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid mode");
   if (d->c < 1) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "slice size must be >= 1");

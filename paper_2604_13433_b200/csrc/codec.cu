@@ -130,6 +130,7 @@ int psell_pack_words(const psell_desc* d, const void* patterns, const int64_t* d
 int psell_unpack_words(const psell_desc* d, const void* words, int64_t n, void* values,
                        uint64_t* deltas, uint8_t* flags, void* stream, psell_error* err) {
   if (!d || !fmt_valid(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid PackFormat");
+  if (!fmt_device_ok(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, PSELL_FP16_W64_MSG);
   if (n > 0) {
     if (d->w == 32)
       unpack_words_kernel<uint32_t><<<grid_for(n), kBlock, 0, as_stream(stream)>>>(

@@ -76,6 +76,13 @@ inline bool fmt_valid(const Fmt& f) {
   return false;
 }
 
+// The device build / SpMV / decode read fp16 words as 32-bit words (D = 15).
+// PackFormat(64, 47, "fp16") passes codec.py:45-62, but its reference decode
+// takes the value from bits 16..31 of the 64-bit word (codec.py:242), i.e. from
+// delta bits: it is rejected here instead of being reproduced.
+inline bool fmt_device_ok(const Fmt& f) { return fmt_valid(f) && !(f.codec == PSELL_FP16 && f.w != 32); }
+#define PSELL_FP16_W64_MSG "fp16 values need 32-bit words on the device (PackFormat(64, 47, 'fp16') is not supported)"
+
 // ---------------------------------------------------------------- encode
 // Error codes of the per-value encoders.
 enum { ENC_OK = 0, ENC_NONFINITE = 1, ENC_OVERFLOW = 2 };
@@ -189,6 +196,15 @@ __device__ __forceinline__ __half ld_keep(const __half* p, uint64_t pol) {
 }
 
 // ---------------------------------------------------------------- reductions
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

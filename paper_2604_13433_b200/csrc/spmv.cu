@@ -1446,6 +1446,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
                      const void* perm, SpmvArgs& a, psell_error* err, bool need_perm = true) {
   if (!d) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null descriptor");
   if (!fmt_valid(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid PackFormat");
+  if (!fmt_device_ok(fmt_of(d))) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, PSELL_FP16_W64_MSG);
   if (d->c < 1) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "invalid C");
   if (need_perm && d->mode == PSELL_MODE_IMPLICIT && d->n_rows > 0 && (!perm || d->sigma < 1))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "implicit mode needs perm");
@@ -1532,11 +1533,69 @@ __global__ void to_csr_fill_kernel(const SpmvArgs a, const int64_t* __restrict__
   }
 }
 
+// Largest column a real word of the stream addresses, over every storage row the
+// SpMV walks (padding rows of the last slice included), starting from the SpMV's
+// clamped cursor (packed.py:257).  A container whose deltas run past n_cols would
+// make the SpMV gather out of bounds: read_psell rejects it with this value.
+template <int CODEC>
+__global__ void max_column_kernel(const SpmvArgs a, long long n_storage, unsigned long long* __restrict__ out) {
+  using W = typename WordOf<CODEC>::T;
+  const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
+  long long m = -1;
+  if (s < n_storage) {
+    const long long k = s / a.c, lane = s - k * a.c;
+    const long long o0 = a.offset[k];
+    const long long width = (a.offset[k + 1] - o0) / a.c;
+    const W* p = static_cast<const W*>(a.pack) + o0 + lane;
+    const int dbits = word_dbits<CODEC>(a.d);
+    long long cursor = raw_base(a.row0 + s, a.se, a.k_left);
+    cursor = a.n_cols > 0 ? (cursor < a.n_cols - 1 ? cursor : a.n_cols - 1) : 0;
+    for (long long q = 0; q < width; ++q) {
+      const W w = p[q * a.c];
+      const unsigned long long dl = (unsigned long long)unpack_delta<W>(w, dbits);
+      // saturate instead of wrapping on absurd deltas
+      cursor = dl > (unsigned long long)(LLONG_MAX / 2) || cursor > LLONG_MAX / 2 ? LLONG_MAX / 2
+                                                                                  : cursor + (long long)dl;
+      if ((w & W(1)) && cursor > m) m = cursor;
+    }
+  }
+  m = warp_max_ll(m);
+  if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(out, (unsigned long long)m);
+}
+
 }  // namespace psell
 
 using namespace psell;
 
 extern "C" {
+
+int psell_max_column(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
+                     int64_t* out_host, void* ws8, void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  if (!ws8 || !out_host) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "missing workspace");
+  cudaStream_t st = as_stream(stream);
+  unsigned long long* dm = static_cast<unsigned long long*>(ws8);
+  PSELL_CUDA(cudaMemsetAsync(dm, 0, 8, st), err);
+  const long long n_storage = a.n_slices * a.c;
+  unsigned long long any = 0;
+  if (n_storage > 0) {
+    const unsigned grid = (unsigned)ceil_div(n_storage, kBlock);
+    switch (d->codec) {
+      case PSELL_FP16: max_column_kernel<PSELL_FP16><<<grid, kBlock, 0, st>>>(a, n_storage, dm); break;
+      case PSELL_E8MY: max_column_kernel<PSELL_E8MY><<<grid, kBlock, 0, st>>>(a, n_storage, dm); break;
+      default: max_column_kernel<PSELL_FP32EMBED><<<grid, kBlock, 0, st>>>(a, n_storage, dm); break;
+    }
+    PSELL_CHECK_LAUNCH(err, "max_column");
+  }
+  // 0 is both "no real word" and "column 0": one more pass would tell them apart, but
+  // column 0 is in range whenever n_cols > 0, which is all the caller checks
+  PSELL_CUDA(cudaMemcpyAsync(&any, dm, 8, cudaMemcpyDeviceToHost, st), err);
+  PSELL_CUDA(cudaStreamSynchronize(st), err);
+  *out_host = (int64_t)any;
+  return ok(err);
+}
+
 
 int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
                const void* x, int32_t x_dtype, void* y, int32_t flags, void* stream,

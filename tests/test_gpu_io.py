@@ -262,3 +262,47 @@ def test_host_device_staging_round_trip():
         assert _dev.upload(a, out=out) is out and torch.equal(out, t)
     with pytest.raises(ValueError):
         _dev.upload(np.zeros(5_000_000), out=torch.empty(10, dtype=torch.float64, device="cuda"))
+
+
+def _corrupt(M, *, pack=None, perm=None):
+    """A .psell byte string of M with its pack / perm replaced (header and offsets kept)."""
+    buf = io.BytesIO()
+    P.write_psell(M, buf)
+    raw = bytearray(buf.getvalue())
+    hdr = len(P.container.header_bytes(M)) + 8 * (M.n_slices + 1)
+    if perm is not None:
+        pb = np.ascontiguousarray(perm).tobytes()
+        raw[hdr:hdr + len(pb)] = pb
+    if pack is not None:
+        start = hdr + (M.perm.dtype.itemsize * M.n_rows if M.mode == "implicit" else 0)
+        pk = np.ascontiguousarray(pack).tobytes()
+        raw[start:start + len(pk)] = pk
+    return io.BytesIO(bytes(raw))
+
+
+def test_container_rejects_streams_the_device_cannot_run(rng):
+    """a container whose perm leaves its sigma-block or whose deltas run past
+    n_cols is rejected with ContainerError instead of reaching the kernels."""
+    from conftest import random_csr_arrays
+    rp, ci, v = random_csr_arrays(rng, 300, 280, 0.05)
+    A = P.CsrMatrix(300, 280, rp, ci, v)
+    M = P.build_packsell(A, 32, 64, P.parse_format("fp16"), "implicit")
+    assert _equal(P.read_psell(_corrupt(M)), M)  # untouched bytes read back
+    bad_perm = M.perm.copy()
+    bad_perm[-1] = 200  # last sigma-block holds 300 - 256 = 44 rows
+    with pytest.raises(P.ContainerError, match="perm"):
+        P.read_psell(_corrupt(M, perm=bad_perm))
+    pack = M.pack.copy()
+    real = np.nonzero(pack & 1)[0][0]
+    pack[real] |= np.uint32(0x7FFF) << np.uint32(1)  # delta 32767: far past n_cols
+    with pytest.raises(P.ContainerError, match="beyond n_cols"):
+        P.read_psell(_corrupt(M, pack=pack))
+
+
+def test_fp16_with_64bit_words_rejected_on_device():
+    """PackFormat(64, 47, 'fp16') is a valid reference format whose reference decode reads
+    its values from delta bits (codec.py:242); the device path refuses it loudly."""
+    A = P.poisson2d(8)
+    fmt = P.PackFormat(64, 47, "fp16")
+    with pytest.raises(ValueError, match="32-bit words"):
+        P.build_packsell(A, 32, 64, fmt, "implicit")
