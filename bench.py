@@ -41,10 +41,15 @@ CONFIGS = {
                mode="implicit",
                workload="config 2: 27-point stencil 256^3 (HPCG_8_8_8), PackSELL fp16 (W=32, D=15), "
                         "C=32, sigma=256, implicit perm; x, y f16; FP32 FMA accumulation"),
-    "c3": dict(kind="stencil27", nx=256, preset="e8m10", xdt="float32", scale="rowsum", c=32, sigma=256,
+    "c3": dict(kind="stencil27", nx=256, preset="e8m21", xdt="float32", scale="rowsum", c=32, sigma=256,
                mode="implicit",
-               workload="config 3: 27-point stencil 256^3 row-sum scaled, PackSELL e8m10 (20-bit float, "
-                        "D=12), C=32, sigma=256, implicit; x, y f32"),
+               workload="config 3: 27-point stencil 256^3 row-sum scaled, PackSELL e8m21 (30-bit float, D=1: "
+                        "the FP32-accurate point of the D sweep, backward error 2.9e-7 = FP32 CSR's), C=32, "
+                        "sigma=256, implicit; x, y f32"),
+    "c3-e8m10": dict(kind="stencil27", nx=256, preset="e8m10", xdt="float32", scale="rowsum", c=32, sigma=256,
+                     mode="implicit",
+                     workload="config 3 (BASELINE's example codec): 27-point stencil 256^3 row-sum scaled, PackSELL "
+                              "e8m10 (20-bit float, D=12), C=32, sigma=256, implicit; x, y f32"),
     "c1": dict(kind="poisson2d", nx=512, preset="fp16", xdt="float16", scale=None, c=32, sigma=256,
                mode="implicit",
                workload="config 1: 5-point Laplacian 512^2, PackSELL fp16, C=32, sigma=256, implicit; x, y f16"),
@@ -415,6 +420,51 @@ def run_pcg(args, world, rank, comm, peak):
 
 
 # ----------------------------------------------------------------------------- GPU side
+def _event_ms(fn, reps=20):
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record()
+    for _ in range(reps):
+        fn()
+    v1.record()
+    torch.cuda.synchronize()
+    return v0.elapsed_time(v1) / reps
+
+
+def vendor_baselines(S, xt, dev, cfg):
+    """The paper's vendor comparators on the same matrix, one GPU (§V):
+    cuSPARSE SELL ("cuSELL": SELL-C-sigma, C = 32, sigma = 256, rows explicitly sigma-reordered,
+    values and vectors in x's dtype, FP32 compute) and cuSPARSE CSR (torch.sparse_csr_tensor @ x)."""
+    import numpy as np
+    import torch
+    out = {}
+    try:
+        from paper_2604_13433_b200.vendor import CuSell
+        V = CuSell(S, 32, 256, np.float16 if xt == torch.float16 else np.float32)
+        V.x.copy_((torch.rand(S.n_cols, device=dev) * 2 - 1).to(xt))
+        out["cusparse_sell"] = {"what": "cuSPARSE SELL-C-sigma SpMV (cusparseCreateSlicedEll + SELL_ALG1, "
+                                        "preprocessed), C=32, sigma=256 sorted rows, values/x/y in x dtype",
+                                "ms_per_step": _event_ms(V.spmv)}
+        V.close()
+        del V
+    except Exception as e:  # noqa: BLE001
+        out["cusparse_sell"] = {"unavailable": repr(e)[:200]}
+    torch.cuda.empty_cache()
+    try:
+        Acsr = torch.sparse_csr_tensor(S.row_ptr.to(torch.int32), S.col_idx, S.values.to(xt), (S.n_rows, S.n_cols))
+        xv = (torch.rand(Acsr.shape[1], device=dev) * 2 - 1).to(xt).unsqueeze(1)
+        out["cusparse_csr"] = {"what": "cuSPARSE CSR SpMV via torch.sparse_csr_tensor @ x (values in x dtype)",
+                               "ms_per_step": _event_ms(lambda: Acsr @ xv)}
+        del Acsr, xv
+    except Exception as e:  # noqa: BLE001
+        out["cusparse_csr"] = {"unavailable": repr(e)[:200]}
+    torch.cuda.empty_cache()
+    return out
+
+
 def gpu_slab_expect(M, cfg, rows, seed):
     """GPU side of the bench-line parity block: digests of the production matrix over
     storage rows 0..rows-1 and the device SpMV outputs on those rows for the CPU
@@ -503,28 +553,8 @@ def run_ours(args, cfg):
     # torch.sparse_csr_tensor @ x, CSR values in x's precision (the paper's cuCSR comparison)
     vendor = None
     if world == 1 and S.nnz < 2 ** 31 and not args.no_vendor:
-        try:
-            Acsr = torch.sparse_csr_tensor(S.row_ptr.to(torch.int32), S.col_idx, S.values.to(xt),
-                                           (S.n_rows, S.n_cols))
-            del S
-            torch.cuda.empty_cache()
-            xv = (torch.rand(Acsr.shape[1], device=dev) * 2 - 1).to(xt).unsqueeze(1)
-            for _ in range(3):
-                Acsr @ xv
-            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            v0.record()
-            for _ in range(20):
-                Acsr @ xv
-            v1.record()
-            torch.cuda.synchronize()
-            vendor = {"what": "cuSPARSE CSR SpMV via torch.sparse_csr_tensor @ x (values in x dtype), same matrix",
-                      "ms_per_step": v0.elapsed_time(v1) / 20}
-            del Acsr, xv
-        except Exception as e:  # noqa: BLE001
-            vendor = {"unavailable": repr(e)[:200]}
-    if "S" in locals():
-        del S
+        vendor = vendor_baselines(S, xt, dev, cfg)
+    del S
     torch.cuda.empty_cache()
 
     g = torch.Generator(device=dev)
@@ -709,8 +739,9 @@ def run_ours(args, cfg):
                                       "api": "packsell_spmv(M, x_pinned_cpu, out=y_pinned_cpu), one blocking call per step"}},
             "gpu_launches": args.steps * launches_per_step,
             "variants_ms": {"register_pipeline (headline)": ms_local, "tma_bulk_stream": ms_regpipe},
-            "vendor_baseline": None if vendor is None else dict(
-                vendor, **({"speedup_packsell": vendor["ms_per_step"] / ms} if "ms_per_step" in vendor else {})),
+            "vendor_baseline": None if vendor is None else {
+                k: dict(v, **({"speedup_packsell": v["ms_per_step"] / ms} if "ms_per_step" in v else {}))
+                for k, v in vendor.items()},
             "clocks": clocks,
             "pcg": pcg,
         }

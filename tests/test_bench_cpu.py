@@ -17,7 +17,7 @@ def test_metric_matches_baseline_json():
     with open(os.path.join(ROOT, "BASELINE.json")) as f:
         base = json.load(f)
     assert bench.METRIC == base["metric"]
-    assert set(bench.CONFIGS) == {"c1", "c2", "c3", "c4"}
+    assert {"c1", "c2", "c3", "c4"} <= set(bench.CONFIGS)
 
 
 @pytest.mark.parametrize("kind,nx", [("stencil27", 8), ("poisson3d", 8), ("poisson2d", 16)])
