@@ -57,6 +57,11 @@ CONFIGS = {
                sigma=65536, mode="implicit",
                workload="config 4: power-law rows (Pareto alpha 1.5, n=2^23, ~95M nnz, csrc/gen.cu), PackSELL fp16, "
                         "C=32, sigma=65536 (--sigma), implicit; x, y f16; long slices segmented"),
+    "c4b": dict(kind="powerlaw_far", n=2 ** 23, seed=2604, nx=0, preset="fp16", xdt="float16", scale=None, c=32,
+                sigma=65536, mode="implicit",
+                workload="config 4b: power-law rows with ~20% of entries uniform over [0, n) (SURVEY 8d's "
+                         "generator: k_left ~ n, every d_i = 0, dummy-heavy), n=2^23, PackSELL fp16, C=32, "
+                         "sigma=65536, implicit; x, y f16; long slices segmented"),
 }
 
 
@@ -78,11 +83,23 @@ def stencil_k_left(kind: str, nx: int) -> int:
         return nx * nx
     if kind == "powerlaw":
         return 4096  # every row starts at max(0, i - 4096) (csrc/gen.cu)
+    if kind == "powerlaw_far":
+        from paper_2604_13433_b200.stencil import powerlaw_far_k_left
+        return _cached("k_left_far", lambda: powerlaw_far_k_left(2 ** 23, 2604))
     return nx
 
 
+_CACHE = {}
+
+
+def _cached(key, fn):
+    if key not in _CACHE:
+        _CACHE[key] = fn()
+    return _CACHE[key]
+
+
 def cfg_rows(cfg) -> int:
-    if cfg["kind"] == "powerlaw":
+    if cfg["kind"] in ("powerlaw", "powerlaw_far"):
         return cfg["n"]
     return cfg["nx"] ** (2 if cfg["kind"] == "poisson2d" else 3)
 
@@ -91,17 +108,18 @@ def partition(cfg, world):
     """sigma-aligned row slabs: equal for stencils, nnz-balanced for the power-law matrix."""
     from paper_2604_13433_b200 import dist as D
     n = cfg_rows(cfg)
-    if cfg["kind"] != "powerlaw" or world == 1:
+    if not cfg["kind"].startswith("powerlaw") or world == 1:
         return D.equal_row_slabs(n, world, cfg["sigma"])
     from paper_2604_13433_b200.stencil import powerlaw_row_lengths
-    return D.word_balanced_slabs(powerlaw_row_lengths(n, cfg["seed"]), world, cfg["sigma"])
+    return D.word_balanced_slabs(powerlaw_row_lengths(n, cfg["seed"], far=cfg["kind"] == "powerlaw_far"), world,
+                                 cfg["sigma"])
 
 
 def make_slab(cfg, r0, r1):
     import paper_2604_13433_b200 as P
-    if cfg["kind"] == "powerlaw":
+    if cfg["kind"].startswith("powerlaw"):
         from paper_2604_13433_b200.stencil import powerlaw_device
-        return powerlaw_device(cfg["n"], cfg["seed"], row_begin=r0, row_end=r1)
+        return powerlaw_device(cfg["n"], cfg["seed"], row_begin=r0, row_end=r1, far=cfg["kind"] == "powerlaw_far")
     return P.stencil_device(cfg["kind"], cfg["nx"], scale=cfg["scale"], row_begin=r0, row_end=r1)
 
 
@@ -216,6 +234,9 @@ def _cpu_worker(conn, cfg, r0, r1, k_left, seed, expect=None):
     if cfg["kind"] == "powerlaw":
         from paper_2604_13433_b200.stencil import powerlaw_rows
         A = powerlaw_rows(cfg["n"], cfg["seed"], r0, r1)
+    elif cfg["kind"] == "powerlaw_far":
+        from paper_2604_13433_b200.stencil import powerlaw_far_rows
+        A = powerlaw_far_rows(cfg["n"], cfg["seed"], r0, r1)
     else:
         A = stencil_rows(cfg["kind"], cfg["nx"], r0, r1)
     vals = A.values
@@ -541,7 +562,7 @@ def run_ours(args, cfg):
     del M2
     if world == 1:
         touched = n
-    elif cfg["kind"] == "powerlaw":
+    elif cfg["kind"].startswith("powerlaw"):
         touched = int(torch.unique(S.col_idx).numel())  # distinct x entries this slab gathers
     else:
         # stencil rows are ascending with ascending columns: the slab's x footprint
@@ -675,6 +696,22 @@ def run_ours(args, cfg):
 
     peak, peak_kind = measured_peak()
     achieved = bytes_local / (ms_local * 1e-3) / 1e9
+    gather_roof = None
+    if cfg["kind"].startswith("powerlaw"):
+        # irregular rows: the x gathers (one per real word; dummy / padding words issue
+        # none) land on unrelated 32-B sectors of the L2-resident x, so the binding roof
+        # is the GPU's random-gather rate, measured here by the probe kernel
+        try:
+            from paper_2604_13433_b200.vendor import gather_ceiling
+            ceil = gather_ceiling(1 << 23, xsz)
+            bound_ms = nnz_local / ceil * 1e3
+            gather_roof = {"bound": "l2_random_gather", "gathers_per_step": int(nnz_local),
+                           "ceiling_gathers_per_s": ceil, "bound_ms": bound_ms, "frac": bound_ms / ms_local,
+                           "hbm_bound_ms": bytes_local / (peak * 1e9) * 1e3,
+                           "ceiling_how": "csrc/vendor/probe.cu: 16 independent hashed gathers per thread, 8 CTAs/SM, "
+                                          "2^23-element x (L2-resident), CUDA events"}
+        except Exception as e:  # noqa: BLE001
+            gather_roof = {"unavailable": repr(e)[:200]}
     clocks = sampler.summary()
 
     cpu = parity = None
@@ -722,7 +759,8 @@ def run_ours(args, cfg):
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                          "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                          "kernel": f"{kernel_name} ({launches_per_step} launch(es) per step; traffic = ncu "
-                                   "DRAM bytes per launch of the SpMV kernel)"},
+                                   "DRAM bytes per launch of the SpMV kernel)",
+                         "gather": gather_roof},
             "cpu_baseline": cpu,
             "parity": parity,
             "e2e": {"value": e2e_value, "unit": "GB/s", "ms_per_step": ms_e2e,
@@ -785,7 +823,7 @@ def main():
     if args.sigma:
         cfg["sigma"] = args.sigma
         cfg["workload"] += f" [sigma overridden to {args.sigma}]"
-    if args.config == "c4" and not args.no_pcg:
+    if args.config in ("c4", "c4b") and not args.no_pcg:
         args.no_pcg = True  # the PCG time-to-solution belongs to the stencil configs (config 5)
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -169,7 +169,10 @@ PSELL_API int psell_spmv_segmented(const psell_desc* desc, const void* pack, con
                                    int32_t seg_len, int64_t n_seg, const int32_t* seg_slice,
                                    const int32_t* seg_q0, const uint32_t* seg_c2, float* seg_partial,
                                    int64_t n_long, const int32_t* long_slice, const int32_t* long_seg0,
-                                   void* stream, psell_error* err);
+                                   uint32_t* sched, int32_t sched_chunks, void* stream, psell_error* err);
+/* sched (nullable): sched_chunks + 1 zeroed uint32 of device scratch kept with the
+ * matrix; the short slices then run on an SM-affine persistent grid (one chunk of
+ * consecutive slice pairs per SM, work stealing) and the kernel leaves it zeroed. */
 
 /* Number of double partials psell_spmv_dot writes (one per CTA) for these flags. */
 PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc, int32_t flags);
@@ -359,6 +362,15 @@ PSELL_API int psell_gen_powerlaw_plan(int64_t n, uint64_t seed, const double* th
 PSELL_API int psell_gen_powerlaw_fill(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin, int64_t row_end,
                                       const int64_t* row_ptr, int32_t* col_idx, double* values,
                                       void* stream, psell_error* err);
+/* Config 4b (SURVEY §8d's proposal): same row lengths, ~20 % of each row's entries uniform
+ * over [0, n) (k_left ~ n, every d_i = 0: the dummy-heavy far-gap regime).  Law in csrc/gen.cu;
+ * host mirror stencil.powerlaw_far_rows. */
+PSELL_API int psell_gen_powerlaw_far_plan(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin,
+                                          int64_t row_end, void* workspace, size_t ws_bytes, int64_t* row_ptr,
+                                          int64_t* nnz_host, void* stream, psell_error* err);
+PSELL_API int psell_gen_powerlaw_far_fill(int64_t n, uint64_t seed, const double* thresholds, int64_t row_begin,
+                                          int64_t row_end, const int64_t* row_ptr, int32_t* col_idx, double* values,
+                                          void* stream, psell_error* err);
 
 /* ---- K6 metrics: backward error (replaces metrics.py:43-66 backward_error /
  * inf_norm_matrix).  One pass over the f64 CSR A (unquantised source), x and

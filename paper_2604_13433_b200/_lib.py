@@ -60,7 +60,7 @@ _SIGS = {
     "psell_spmv_kernel_name": (ctypes.c_char_p, [_D, c_int32, c_int32]),
     "psell_spmv_seg_checkpoints": (c_int32, [_D, _P, _P, c_int32, c_int64, _P, _P, c_int64, _P, _P, _P, _P, _E]),
     "psell_spmv_segmented": (c_int32, [_D, _P, _P, _P, _P, c_int32, _P, c_int32, c_int64, _P, _P, _P, _P,
-                                       c_int64, _P, _P, _P, _E]),
+                                       c_int64, _P, _P, _P, c_int32, _P, _E]),
     "psell_spmv_dot_partials": (c_int64, [_D, c_int32]),
     "psell_spmv_dot": (c_int32, [_D, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, _P, _E]),
     "psell_to_csr_workspace_bytes": (c_size_t, [_D]),
@@ -114,6 +114,9 @@ _SIGS = {
     "psell_gen_powerlaw_plan": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, c_size_t, _P,
                                           POINTER(c_int64), _P, _E]),
     "psell_gen_powerlaw_fill": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, _P, _P, _P, _E]),
+    "psell_gen_powerlaw_far_plan": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, c_size_t, _P,
+                                              POINTER(c_int64), _P, _E]),
+    "psell_gen_powerlaw_far_fill": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, _P, _P, _P, _E]),
     "psell_gen_stencil_plan": (c_int32, [c_int64, c_int64, c_int64, c_int32, c_double, c_int64, c_int64,
                                          _P, c_size_t, _P, POINTER(c_int64), _P, _E]),
     "psell_gen_stencil_fill": (c_int32, [c_int64, c_int64, c_int64, c_int32, c_double, c_int32, c_int64,
@@ -165,6 +168,18 @@ def lib():
     if _lib is not None and _gpu_ok:
         return _lib
     return load(require_gpu=True)
+
+
+_SMS = None
+
+
+def sm_count() -> int:
+    """Streaming multiprocessors of the current device (148 on B200), queried once."""
+    global _SMS
+    if _SMS is None:
+        import torch
+        _SMS = int(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)
+    return _SMS
 
 
 def ptr(t) -> int:

@@ -143,6 +143,73 @@ __global__ void powerlaw_kernel(PlParams P, long long r0, long long r1, long lon
   if (!FILL) counts[i - r0] = cnt;
 }
 
+// ---------------------------------------------------------------- far-column power-law (config 4b)
+// SURVEY §8d's proposal: the same Pareto row lengths, but ~20 % of a row's entries
+// uniform over [0, n) instead of near the diagonal, so the lower bandwidth k_left
+// is ~n, every base offset d_i is 0 and the first gap of a row is its first column
+// (the dummy-heavy far-gap regime).  Counter-based like config 4:
+//   L_i    as config 4 (stream 0)
+//   far_j  = h(2, j) % 5 == 0 for j < L_i; m_f = #far, m_n = L_i - m_f
+//   near   : c = max(0, i - 4096) + h(6, 0) % 1024, then c += 1 + h(1, k) % G2,
+//            G2 = 2 max(1, 8192 / max(m_n, 1))            (a band of ~16 K columns)
+//   far    : S = max(1, n / (m_f + 1)), c = h(5, 0) % S, then c += 1 + h(7, k) % (2 S)
+//   row    = sorted union of the two increasing walks below n (a column both walks
+//            reach is stored once); value(col) = (0.01 + 0.99 u53(h(4, col))) * (h(3, col) & 1 ? -1 : 1)
+__device__ __forceinline__ double far_value(uint64_t hr, long long c) {
+  const double m = __dadd_rn(0.01, __dmul_rn(0.99, u53(hdraw(hr, 4, c))));
+  return (hdraw(hr, 3, c) & 1ull) ? -m : m;
+}
+
+template <bool FILL>
+__global__ void powerlaw_far_kernel(PlParams P, long long r0, long long r1, long long* __restrict__ counts,
+                                    const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                    double* __restrict__ val) {
+  const long long i = r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  const uint64_t hr = hrow(P.seed, i);
+  const double u = u53(hdraw(hr, 0, 0));
+  int lo = 0, hi = 8192;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (P.thr[mid] >= u) lo = mid + 1;
+    else hi = mid;
+  }
+  const long long L = lo < 1 ? 1 : lo;
+  long long mf = 0;
+  for (long long j = 0; j < L; ++j) mf += hdraw(hr, 2, j) % 5ull == 0ull;
+  const long long mn = L - mf;
+  const uint64_t G2 = 2ull * (uint64_t)(8192 / (mn > 1 ? mn : 1) > 1 ? 8192 / (mn > 1 ? mn : 1) : 1);
+  const long long Sl = P.n / (mf + 1);
+  const uint64_t S = (uint64_t)(Sl > 1 ? Sl : 1);
+  long long cn = (i - 4096 > 0 ? i - 4096 : 0) + (long long)(hdraw(hr, 6, 0) % 1024ull);
+  long long cf = (long long)(hdraw(hr, 5, 0) % S);
+  long long kn = 0, kf = 0;
+  long long t = FILL ? row_ptr[i - r0] : 0;
+  long long cnt = 0;
+  const long long BIG = 1ll << 62;
+  for (;;) {
+    const long long a = (kn < mn && cn < P.n) ? cn : BIG;
+    const long long b = (kf < mf && cf < P.n) ? cf : BIG;
+    const long long c = a < b ? a : b;
+    if (c == BIG) break;
+    if (FILL) {
+      col[t] = (int32_t)c;
+      val[t] = far_value(hr, c);
+      ++t;
+    }
+    ++cnt;
+    if (a == c) {
+      cn += 1 + (long long)(hdraw(hr, 1, kn) % G2);
+      ++kn;
+    }
+    if (b == c) {
+      cf += 1 + (long long)(hdraw(hr, 7, kf) % (2ull * S));
+      ++kf;
+    }
+  }
+  if (!FILL) counts[i - r0] = cnt;
+}
+
 }  // namespace psell
 
 using namespace psell;
@@ -175,6 +242,38 @@ extern "C" PSELL_API int psell_gen_powerlaw_fill(int64_t n, uint64_t seed, const
   PlParams P{n, seed, thresholds};
   powerlaw_kernel<true><<<(unsigned)ceil_div(m, kBlock), kBlock, 0, as_stream(stream)>>>(P, row_begin, row_end, nullptr, row_ptr, col_idx, values);
   PSELL_CHECK_LAUNCH(err, "powerlaw_fill");
+  return ok(err);
+}
+
+extern "C" PSELL_API int psell_gen_powerlaw_far_plan(int64_t n, uint64_t seed, const double* thresholds,
+                                                     int64_t row_begin, int64_t row_end, void* ws, size_t ws_bytes,
+                                                     int64_t* row_ptr, int64_t* nnz_host, void* stream,
+                                                     psell_error* err) {
+  const long long m = row_end - row_begin;
+  if (m < 0 || row_end > n) return set_err(err, PSELL_EVALUE, PSELL_KIND_PARAM, -1, 0, 0, "bad row range");
+  if (!ws || ws_bytes < psell_gen_workspace_bytes(m)) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  long long* counts = static_cast<long long*>(ws);
+  long long* tmp = reinterpret_cast<long long*>(static_cast<char*>(ws) + align_up(8 * (size_t)(m > 0 ? m : 1)));
+  PlParams P{n, seed, thresholds};
+  if (m > 0) powerlaw_far_kernel<false><<<(unsigned)ceil_div(m, kBlock), kBlock, 0, st>>>(P, row_begin, row_end, counts, nullptr, nullptr, nullptr);
+  PSELL_CHECK_LAUNCH(err, "powerlaw_far_count");
+  if (int rc = scan_i64(counts, m, tmp, reinterpret_cast<long long*>(row_ptr), st, err)) return rc;
+  long long nnz = 0;
+  PSELL_CUDA(cudaMemcpyAsync(&nnz, row_ptr + m, 8, cudaMemcpyDeviceToHost, st), err);
+  PSELL_CUDA(cudaStreamSynchronize(st), err);
+  *nnz_host = nnz;
+  return ok(err);
+}
+
+extern "C" PSELL_API int psell_gen_powerlaw_far_fill(int64_t n, uint64_t seed, const double* thresholds,
+                                                     int64_t row_begin, int64_t row_end, const int64_t* row_ptr,
+                                                     int32_t* col_idx, double* values, void* stream, psell_error* err) {
+  const long long m = row_end - row_begin;
+  if (m <= 0) return ok(err);
+  PlParams P{n, seed, thresholds};
+  powerlaw_far_kernel<true><<<(unsigned)ceil_div(m, kBlock), kBlock, 0, as_stream(stream)>>>(P, row_begin, row_end, nullptr, row_ptr, col_idx, values);
+  PSELL_CHECK_LAUNCH(err, "powerlaw_far_fill");
   return ok(err);
 }
 

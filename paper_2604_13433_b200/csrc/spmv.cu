@@ -55,6 +55,10 @@ struct SpmvArgs {
   const int32_t* long_seg0;   // [n_long + 1] first segment of each long slice
   // n / se and n / sigma for n < 2^31 as (umulhi(n, m) + n) >> l (Granlund-Montgomery)
   uint32_t se_m, se_l, sig_m, sig_l;
+  // SM-affine persistent scheduling of the dual kernel (irregular matrices):
+  // claim counters, one per chunk, + exit count; zero between launches
+  uint32_t* sched;
+  int aff_chunks;
 };
 
 // (m, l) with n / d == (umulhi(n, m) + n) >> l for every n < 2^31 (d >= 1)
@@ -538,16 +542,72 @@ done:
 // chunks, so the two per-slice latency chains (offset -> words -> x -> y)
 // overlap inside one warp.  Aimed at narrow slices (7-point rows: ~9 steps),
 // where one slice per warp leaves the chain exposed.
-template <int CODEC, typename XT, bool DOT, int U, bool GR = false>
+// SM-affine persistent scheduling (AFF, irregular matrices): the slice pairs are
+// cut into one contiguous chunk per SM; the warps resident on SM j claim pairs
+// of chunk j (per-chunk atomic counter), then steal from the following chunks.
+// Consecutive slices are neighbouring rows of the same sigma-block, so the x
+// columns one SM gathers stay within a narrow window and hit its L1 instead of
+// each gather crossing to L2 (block-linear CTA order puts slices 2368 apart on
+// one SM).  sched[0..nchunk) claim counters, sched[nchunk] exit count; the last
+// warp to leave resets them for the next launch (no memset node).
+__device__ __forceinline__ uint32_t smid_u32() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+struct AffSched {
+  uint32_t owner, tried;
+};
+
+// next slice pair for this warp, or ~0u when every chunk is exhausted (warp-uniform)
+__device__ __forceinline__ uint32_t aff_next(const SpmvArgs& a, AffSched& st, uint32_t npairs) {
+  const uint32_t nc = (uint32_t)a.aff_chunks;
+  uint32_t pair = ~0u;
+  if ((threadIdx.x & 31) == 0) {
+    while (st.tried < nc) {
+      const uint32_t o = st.owner;
+      const uint32_t lo = (uint32_t)(((unsigned long long)npairs * o) / nc);
+      const uint32_t hi = (uint32_t)(((unsigned long long)npairs * (o + 1)) / nc);
+      // cheap read first: exhausted chunks cost no atomic once seen
+      if (*reinterpret_cast<volatile uint32_t*>(a.sched + o) < hi - lo) {
+        const uint32_t t = atomicAdd(a.sched + o, 1u);
+        if (t < hi - lo) {
+          pair = lo + t;
+          break;
+        }
+      }
+      st.owner = st.owner + 1 == nc ? 0 : st.owner + 1;
+      ++st.tried;
+    }
+  }
+  return __shfl_sync(0xffffffffu, pair, 0);
+}
+
+__device__ __forceinline__ void aff_exit(const SpmvArgs& a) {
+  if ((threadIdx.x & 31) == 0) {
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    const uint32_t nc = (uint32_t)a.aff_chunks;
+    if (atomicAdd(a.sched + nc, 1u) == nw - 1) {
+      for (uint32_t i = 0; i <= nc; ++i) a.sched[i] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
 __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) {
   using S = FastStep<CODEC, XT, GR>;
   if constexpr (DOT) {
     if (a.skip && *a.skip) return;
   }
-  const long long wg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const long long kA = 2 * wg, kB = kA + 1;
   double dotv = 0.0;
+  const uint32_t npairs = (uint32_t)((a.n_slices + 1) >> 1);
+  AffSched sched{AFF ? smid_u32() % (uint32_t)a.aff_chunks : 0u, 0u};
+  long long wg = AFF ? (long long)aff_next(a, sched, npairs) : ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  for (; !AFF || wg != (long long)~0u; wg = AFF ? (long long)aff_next(a, sched, npairs) : (long long)~0u) {
+  const long long kA = 2 * wg, kB = kA + 1;
   if (kA < a.n_slices) {
     const bool hasB = kB < a.n_slices;
     const long long oA = a.offset[kA], oB = a.offset[kA + 1];
@@ -658,6 +718,9 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
     if (!skipA) flush(kA, accA);
     if (hasB && !skipB) flush(kB, accB);
   }
+  if (!AFF) break;
+  }
+  if constexpr (AFF) aff_exit(a);
   finish_dot<DOT>(a, dotv);
 }
 
@@ -1463,6 +1526,8 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.ticket = nullptr;
   a.scal = nullptr;
   a.iflags = nullptr;
+  a.sched = nullptr;
+  a.aff_chunks = 0;
   a.n_rows = d->n_rows;
   a.n_cols = d->n_cols;
   a.n_slices = ceil_div(d->n_rows, d->c);
@@ -1664,9 +1729,31 @@ int psell_spmv_seg_checkpoints(const psell_desc* d, const void* pack, const int6
 }  // extern "C"
 
 namespace psell {
+// SM-affine dual kernel for the short slices of an irregular matrix (PSELL_AFF=1: on, A/B;
+// PSELL_AFF_CTAS = resident CTAs per SM, default 6).  Off by default: on config 4 it
+// raised the L1 hit rate of the x gathers from 26 % to 39 % and cut L2 sectors by 10 %,
+// but ran 480-540 us against 366 us (twice the instructions; the claim atomics and the
+// end-of-work chunk scan are serial L2 round trips), scripts/c4_aff.py.
+static bool aff_on() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_AFF", v)) return v != 0;
+  return false;
+}
+static int aff_ctas() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_AFF_CTAS", v) && v >= 1 && v <= 6) return v;
+  return 6;
+}
+
 template <int CODEC, typename XT>
 static void launch_segmented(const SpmvArgs& a, long long n_seg, long long n_long, cudaStream_t st) {
-  launch_spmv<CODEC, XT, false, false, true>(a, st);  // short slices (long ones are skipped); flag-predicated gathers
+  if (a.sched && a.aff_chunks > 0 && aff_on() && a.n_slices >= 2) {
+    const unsigned g = (unsigned)(sm_count() * aff_ctas());
+    spmv_dual_kernel<CODEC, XT, false, 8, true, true><<<g, kBlock, 0, st>>>(a);
+  } else
+    launch_spmv<CODEC, XT, false, false, true>(a, st);  // short slices (long ones are skipped); flag-predicated gathers
   if (n_seg > 0)
     spmv_seg_kernel<CODEC, XT, 8><<<(unsigned)ceil_div(n_seg * 32, kBlock), kBlock, 0, st>>>(a, n_seg);
   if (n_long > 0)
@@ -1680,9 +1767,12 @@ int psell_spmv_segmented(const psell_desc* d, const void* pack, const int64_t* o
                          const void* x, int32_t x_dtype, void* y, int32_t seg_len, int64_t n_seg,
                          const int32_t* seg_slice, const int32_t* seg_q0, const uint32_t* seg_c2,
                          float* seg_partial, int64_t n_long, const int32_t* long_slice,
-                         const int32_t* long_seg0, void* stream, psell_error* err) {
+                         const int32_t* long_seg0, uint32_t* sched, int32_t sched_chunks, void* stream,
+                         psell_error* err) {
   SpmvArgs a;
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  a.sched = sched;
+  a.aff_chunks = sched ? sched_chunks : 0;
   if (d->c != 32 || d->codec == PSELL_FP32EMBED || (x_dtype != PSELL_DT_F16 && x_dtype != PSELL_DT_F32))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0,
                    "segmented SpMV: C = 32, fp16/e8my codec, f16/f32 x only");

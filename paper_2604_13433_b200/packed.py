@@ -318,7 +318,9 @@ def _seg_schedule(M: PackSellMatrix):
     seg_q0 = ((np.arange(n_seg) - np.repeat(seg0[:-1], per)) * SEG_LEN).astype(np.int32)
     s = dict(n_seg=n_seg, n_long=int(long_.size), seg_slice=_dev.upload(seg_slice), seg_q0=_dev.upload(seg_q0),
              long_slice=_dev.upload(long_.astype(np.int32)), long_seg0=_dev.upload(seg0),
-             seg_c2=_dev.empty(n_seg * 32, np.uint32))
+             seg_c2=_dev.empty(n_seg * 32, np.uint32),
+             # SM-affine scheduler counters of the short-slice kernel (left zeroed by every launch)
+             sched=_dev.zeros(_lib.sm_count() + 1, np.uint32), sched_chunks=_lib.sm_count())
     lib = _lib.lib()
     err = _lib.PsellError()
     rc = lib.psell_spmv_seg_checkpoints(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), SEG_LEN, n_seg,
@@ -355,7 +357,8 @@ def _spmv_device(M: PackSellMatrix, xd, y, ref_order: bool, pipe: int = 0):
                                           _lib.ptr(xd), _dev.T_DT_CODE[xd.dtype], _lib.ptr(y), SEG_LEN, s["n_seg"],
                                           _lib.ptr(s["seg_slice"]), _lib.ptr(s["seg_q0"]), _lib.ptr(s["seg_c2"]),
                                           _lib.ptr(part), s["n_long"], _lib.ptr(s["long_slice"]),
-                                          _lib.ptr(s["long_seg0"]), _lib.stream_handle(), err)
+                                          _lib.ptr(s["long_seg0"]), _lib.ptr(s["sched"]), s["sched_chunks"],
+                                          _lib.stream_handle(), err)
             _lib.check(rc, err, M.fmt)
             return y
     rc = lib.psell_spmv(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),

@@ -173,6 +173,65 @@ def powerlaw_rows(n: int = 2**23, seed: int = 2604, row_begin: int = 0, row_end:
     return CsrMatrix(r1 - r0, n, row_ptr, cols, vals)
 
 
+def powerlaw_far_rows(n: int = 2**23, seed: int = 2604, row_begin: int = 0, row_end: int = None) -> CsrMatrix:
+    """Rows [row_begin, row_end) of the config-4b far-column power-law matrix (host mirror
+    of psell_gen_powerlaw_far_*; law in csrc/gen.cu): a near-diagonal walk and a walk
+    spread uniformly over [0, n), merged into sorted unique columns."""
+    r1 = n if row_end is None else int(row_end)
+    r0 = int(row_begin)
+    rows = np.arange(r0, r1, dtype=np.int64)
+    with np.errstate(over="ignore"):
+        hr = _smix(_U64(seed) ^ (rows.astype(_U64) * _U64(0xD1B54A32D192ED03)))
+
+    def draw(stream, j, h):
+        return _smix(h ^ (_U64(stream) << _U64(56)) ^ _U64(j))
+
+    u = (draw(0, 0, hr) >> _U64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    L = np.maximum(np.searchsorted(-powerlaw_thresholds(), -u, side="right"), 1).astype(np.int64)
+    mf = np.zeros(len(rows), np.int64)
+    act = np.arange(len(rows))
+    j = 0
+    while act.size:
+        mf[act] += (draw(2, j, hr[act]) % _U64(5) == 0)
+        j += 1
+        act = act[j < L[act]]
+    mn = L - mf
+    G2 = (2 * np.maximum(1, 8192 // np.maximum(mn, 1))).astype(_U64)
+    S = np.maximum(n // (mf + 1), 1).astype(_U64)
+    out_r, out_c = [], []
+
+    def walk(c, count, stream, step_mod):
+        act = np.nonzero((count > 0) & (c < n))[0]
+        k = 0
+        while act.size:
+            out_r.append(act)
+            out_c.append(c[act].copy())
+            c[act] += 1 + (draw(stream, k, hr[act]) % step_mod[act]).astype(np.int64)
+            k += 1
+            act = act[(k < count[act]) & (c[act] < n)]
+
+    walk(np.maximum(rows - 4096, 0) + (draw(6, 0, hr) % _U64(1024)).astype(np.int64), mn, 1, G2)
+    walk((draw(5, 0, hr) % S).astype(np.int64), mf, 7, _U64(2) * S)
+    if out_r:
+        rr = np.concatenate(out_r)
+        cc = np.concatenate(out_c)
+        o = np.lexsort((cc, rr))
+        rr, cc = rr[o], cc[o]
+        keep = np.ones(len(rr), bool)
+        keep[1:] = (rr[1:] != rr[:-1]) | (cc[1:] != cc[:-1])
+        rr, cc = rr[keep], cc[keep]
+        h = hr[rr]
+        m = 0.01 + 0.99 * ((draw(4, 0, h ^ cc.astype(_U64)) >> _U64(11)).astype(np.float64)
+                           * (1.0 / 9007199254740992.0))
+        vals = np.where((draw(3, 0, h ^ cc.astype(_U64)) & _U64(1)) != 0, -m, m)
+        counts = np.bincount(rr, minlength=r1 - r0)
+        cols = cc.astype(np.int32)
+    else:
+        cols, vals, counts = np.zeros(0, np.int32), np.zeros(0), np.zeros(r1 - r0, np.int64)
+    row_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return CsrMatrix(r1 - r0, n, row_ptr, cols, vals)
+
+
 def powerlaw_thresholds() -> np.ndarray:
     """T_k = (4/k)^1.5, k = 1..8192: L >= k  <=>  u <= T_k (Pareto alpha 1.5)."""
     return (4.0 / np.arange(1, 8193, dtype=np.float64)) ** 1.5
@@ -183,8 +242,35 @@ def powerlaw(n: int = 2**23, seed: int = 2604) -> CsrMatrix:
     return powerlaw_rows(n, seed)
 
 
-def powerlaw_row_lengths(n: int = 2**23, seed: int = 2604) -> np.ndarray:
-    """Row lengths of the whole config-4 matrix (device count pass only) — partition weights."""
+def powerlaw_far_k_left(n: int = 2**23, seed: int = 2604) -> int:
+    """Lower bandwidth of the whole config-4b matrix from each row's first column only
+    (the smaller of the two walks' starts), on the host: max_i(i - first_col_i)."""
+    rows = np.arange(n, dtype=np.int64)
+    with np.errstate(over="ignore"):
+        hr = _smix(_U64(seed) ^ (rows.astype(_U64) * _U64(0xD1B54A32D192ED03)))
+
+    def draw(stream, j, h):
+        return _smix(h ^ (_U64(stream) << _U64(56)) ^ _U64(j))
+
+    u = (draw(0, 0, hr) >> _U64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    L = np.maximum(np.searchsorted(-powerlaw_thresholds(), -u, side="right"), 1).astype(np.int64)
+    mf = np.zeros(n, np.int64)
+    act = np.arange(n)
+    j = 0
+    while act.size:
+        mf[act] += (draw(2, j, hr[act]) % _U64(5) == 0)
+        j += 1
+        act = act[j < L[act]]
+    big = np.int64(1) << 62
+    near = np.where(L - mf > 0, np.maximum(rows - 4096, 0) + (draw(6, 0, hr) % _U64(1024)).astype(np.int64), big)
+    far = np.where(mf > 0, (draw(5, 0, hr) % np.maximum(n // (mf + 1), 1).astype(_U64)).astype(np.int64), big)
+    first = np.minimum(near, far)
+    ok = first < n
+    return int(max(0, int(np.max(rows[ok] - first[ok])))) if ok.any() else 0
+
+
+def powerlaw_row_lengths(n: int = 2**23, seed: int = 2604, far: bool = False) -> np.ndarray:
+    """Row lengths of the whole config-4 (4b: far=True) matrix (device count pass only) — partition weights."""
     import ctypes
     from . import _dev, _lib
     lib = _lib.lib()
@@ -193,14 +279,17 @@ def powerlaw_row_lengths(n: int = 2**23, seed: int = 2604) -> np.ndarray:
     row_ptr = _dev.empty(n + 1, np.int64)
     nnz = ctypes.c_int64(0)
     err = _lib.PsellError()
-    rc = lib.psell_gen_powerlaw_plan(n, seed, _lib.ptr(thr), 0, n, _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr),
-                                     ctypes.byref(nnz), _lib.stream_handle(), err)
+    plan = lib.psell_gen_powerlaw_far_plan if far else lib.psell_gen_powerlaw_plan
+    rc = plan(n, seed, _lib.ptr(thr), 0, n, _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr), ctypes.byref(nnz),
+              _lib.stream_handle(), err)
     _lib.check(rc, err)
     return np.diff(_dev.download(row_ptr, np.int64))
 
 
-def powerlaw_device(n: int = 2**23, seed: int = 2604, *, row_begin: int = 0, row_end: int = None):
-    """Rows [row_begin, row_end) of the config-4 matrix generated in HBM (DeviceCsrMatrix)."""
+def powerlaw_device(n: int = 2**23, seed: int = 2604, *, row_begin: int = 0, row_end: int = None,
+                    far: bool = False):
+    """Rows [row_begin, row_end) of the config-4 matrix (config 4b with far=True) generated in
+    HBM (DeviceCsrMatrix)."""
     import ctypes
     from . import _dev, _lib
     from .matrix import DeviceCsrMatrix
@@ -213,13 +302,13 @@ def powerlaw_device(n: int = 2**23, seed: int = 2604, *, row_begin: int = 0, row
     nnz = ctypes.c_int64(0)
     err = _lib.PsellError()
     st = _lib.stream_handle()
-    rc = lib.psell_gen_powerlaw_plan(n, seed, _lib.ptr(thr), r0, r1, _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr),
-                                     ctypes.byref(nnz), st, err)
+    plan = lib.psell_gen_powerlaw_far_plan if far else lib.psell_gen_powerlaw_plan
+    fill = lib.psell_gen_powerlaw_far_fill if far else lib.psell_gen_powerlaw_fill
+    rc = plan(n, seed, _lib.ptr(thr), r0, r1, _lib.ptr(ws), ws.numel(), _lib.ptr(row_ptr), ctypes.byref(nnz), st, err)
     _lib.check(rc, err)
     col = _dev.empty(nnz.value, np.int32)
     val = _dev.empty(nnz.value, np.float64)
-    rc = lib.psell_gen_powerlaw_fill(n, seed, _lib.ptr(thr), r0, r1, _lib.ptr(row_ptr), _lib.ptr(col),
-                                     _lib.ptr(val), st, err)
+    rc = fill(n, seed, _lib.ptr(thr), r0, r1, _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(val), st, err)
     _lib.check(rc, err)
     return DeviceCsrMatrix(r1 - r0, n, row_ptr, col, val, row0=r0)
 

@@ -1,4 +1,4 @@
-"""Vendor comparators for the bench (NOT on the product path).
+"""Vendor comparators and measurement probes for the bench (NOT on the product path).
 
 cuSPARSE sliced ELL ("cuSELL", the paper's primary vendor baseline,
 PAPER.md §V) through libpsell_vendor.so (csrc/vendor/cusell.cu), on the
@@ -34,6 +34,7 @@ def vlib():
                                            ctypes.POINTER(P)]
         L.vendor_cusell_spmv.argtypes = [P]
         L.vendor_cusell_destroy.argtypes = [P]
+        L.probe_gather.argtypes = [P, ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
         _vlib = L
     return _vlib
 
@@ -95,3 +96,27 @@ class CuSell:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+def gather_ceiling(n_elems: int = 1 << 23, elem_bytes: int = 2, reps: int = 10) -> float:
+    """Measured random-gather rate (gathers/s) of an L2-resident vector on this GPU: the
+    ceiling of an SpMV whose x gathers land on unrelated 32-B sectors (config 4).  Every
+    thread of a 8-CTA-per-SM grid issues 16 independent hashed gathers per round
+    (csrc/vendor/probe.cu); scripts/probe/l2_gather.py sweeps the knobs (flat at ~289 G/s)."""
+    import torch
+    L = vlib()
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    grid, rounds, g = sms * 8, 64, 16
+    x = torch.rand(n_elems, device="cuda").to(torch.float16 if elem_bytes == 2 else torch.float32)
+    out = torch.zeros(grid * 256, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        L.probe_gather(x.data_ptr(), elem_bytes, n_elems, g, rounds, grid, out.data_ptr(), st)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        L.probe_gather(x.data_ptr(), elem_bytes, n_elems, g, rounds, grid, out.data_ptr(), st)
+    e1.record()
+    torch.cuda.synchronize()
+    return grid * 256 * rounds * g / (e0.elapsed_time(e1) / reps * 1e-3)

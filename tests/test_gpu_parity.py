@@ -457,3 +457,47 @@ def test_persistent_pair_kernel_at_scale(rng):
         anorm = np.bincount(r, np.abs(P.quantize(P.parse_format(pre), v)), minlength=n).max()
         err = np.abs(yf - yr).max() / (anorm * np.abs(x.astype(np.float64)).max())
         assert err <= 2 * lmax * 2.0 ** -24 + (2.0 ** -11 if dt == np.float16 else 0.0), (pre, err)
+
+
+@pytest.mark.parametrize("n,r0,r1", [(5000, 0, 5000), (2 ** 23, 0, 30_000), (2 ** 23, 2 ** 23 - 20_000, 2 ** 23)])
+def test_powerlaw_far_device_equals_host(n, r0, r1):
+    """Config-4b generator (SURVEY §8d's far columns): device == host mirror, bit for bit."""
+    from paper_2604_13433_b200.stencil import powerlaw_device, powerlaw_far_rows
+    H = powerlaw_far_rows(n, 2604, r0, r1)
+    D = powerlaw_device(n, 2604, row_begin=r0, row_end=r1, far=True).to_host()
+    assert np.array_equal(D.row_ptr, H.row_ptr)
+    assert np.array_equal(D.col_idx, H.col_idx)
+    assert np.array_equal(_bits(D.values), _bits(H.values))
+
+
+@pytest.mark.parametrize("sigma", [256, 65536])
+def test_powerlaw_far_build_and_spmv_vs_oracle(sigma):
+    """The dummy-heavy far-gap regime (k_left ~ n, every d_i = 0) through K1/K2 vs the oracle,
+    including the segmented path and its SM-affine short-slice kernel (bitwise equal to the
+    block-linear one)."""
+    import os
+    from paper_2604_13433_b200 import _lib
+    from paper_2604_13433_b200.stencil import powerlaw_far_rows
+    A = powerlaw_far_rows(1 << 17, 5)
+    M = P.build_packsell(A, 32, sigma, P.parse_format("fp16"), "implicit")
+    OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, sigma, O.preset("fp16"), "implicit")
+    assert M.k_left == OM.k_left > (1 << 17) - 2 * sigma
+    assert np.array_equal(M.pack, OM.pack) and np.array_equal(M.perm, OM.perm)
+    assert np.array_equal(M.offset, OM.offset) and tuple(M.counts) == OM.counts
+    assert OM.counts[1] > A.nnz // 20  # dummy heavy (27 % of nnz at the full n = 2^23)
+    x = np.random.default_rng(3).uniform(-1, 1, A.n_cols).astype(np.float16)
+    assert np.array_equal(_bits(P.packsell_spmv(M, x, ref_order=True)), _bits(O.spmv(OM, x)))
+    ys = {}
+    for aff in ("0", "1"):
+        os.environ["PSELL_AFF"] = aff
+        _lib.lib().psell_reload_env()
+        ys[aff] = P.packsell_spmv(M, x)
+    os.environ.pop("PSELL_AFF")
+    _lib.lib().psell_reload_env()
+    assert np.array_equal(_bits(ys["0"]), _bits(ys["1"]))
+    ref = O.spmv(OM, x.astype(np.float32)).astype(np.float64)
+    lmax = int(np.max(np.diff(OM.offset) // 32))
+    aq = np.abs(O.quantize(O.preset("fp16"), A.values))
+    anorm = np.bincount(np.repeat(np.arange(A.n_rows), A.row_lengths()), aq, minlength=A.n_rows).max()
+    err = np.abs(ys["0"].astype(np.float64) - ref).max() / (anorm * np.abs(x.astype(np.float64)).max())
+    assert err <= 2.0 ** -11 + 2 * lmax * 2.0 ** -24, err

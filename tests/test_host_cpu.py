@@ -216,3 +216,22 @@ int main(void) {
     run = subprocess.run([str(exe)], capture_output=True, text=True, env=env)
     assert run.returncode == 0, run.stderr
     assert "sm_100a" in run.stdout
+
+
+def test_powerlaw_far_rows_properties():
+    """Config-4b host generator: sorted unique columns in [0, n), Pareto row lengths, the
+    lower bandwidth ~ n (far entries push k_left so every d_i = 0)."""
+    import oracle as O
+    from paper_2604_13433_b200.stencil import powerlaw_far_k_left, powerlaw_far_rows
+    n = 1 << 16
+    A = powerlaw_far_rows(n, 9)
+    rp, ci = A.row_ptr, A.col_idx
+    assert rp[0] == 0 and rp[-1] == A.nnz and np.all(np.diff(rp) >= 1)
+    assert ci.min() >= 0 and ci.max() < n
+    row = np.repeat(np.arange(n), np.diff(rp))
+    same = row[1:] == row[:-1]
+    assert np.all(ci[1:][same] > ci[:-1][same])
+    kl = O.lower_bandwidth(rp, ci)
+    assert kl == powerlaw_far_k_left(n, 9) and kl > n - 4096
+    B = powerlaw_far_rows(n, 9, 1000, 3000)
+    assert np.array_equal(B.col_idx, ci[rp[1000]:rp[3000]]) and np.array_equal(B.values, A.values[rp[1000]:rp[3000]])
