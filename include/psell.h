@@ -67,6 +67,7 @@ typedef enum psell_dtype { PSELL_DT_F16 = 0, PSELL_DT_F32 = 1, PSELL_DT_F64 = 2 
 #define PSELL_SPMV_TMA_STREAM 2 /* C=32 fast path: persistent TMA bulk-copy stream instead of the default
                                   register-pipelined dual-slice kernel (A/B experiments) */
 #define PSELL_SPMV_NARROW 4     /* mean slice width <= 12 steps (e.g. 7-point rows): 12-step chunks */
+#define PSELL_SPMV_NARROW12 8   /* with NARROW: every slice <= 12 steps, the TMA slot kernel may run */
 
 typedef struct psell_error {
   int32_t code;  /* psell_status */

@@ -38,6 +38,7 @@ struct SpmvArgs {
   int c, se, sigma, mode, d, perm_bytes;
   int variant;  // 0: register-pipelined kernels (default), 2: persistent TMA stream
   int narrow;   // mean slice width <= 12 steps (PSELL_SPMV_NARROW)
+  int narrow12; // every slice <= 12 steps (PSELL_SPMV_NARROW12): the slot kernel applies
   int codec;
   // long-slice segmentation (0 = off): slices wider than seg_len steps run as
   // segments (see spmv_seg_kernel)
@@ -760,10 +761,26 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
       return blk + pp;
     };
     uint32_t oA = sA, oB = sB;
+#ifndef PSELL_PAIR_PERM_EARLY
+    // HOIST: the perm bytes are issued here but added into the output rows only at the
+    // flush (the add right after the load stalled the warp for the load's full latency
+    // before its word stream: the hottest stall of this kernel in ncu)
+    uint32_t ppA = 0u, ppB = 0u;
+    if constexpr (HOIST) {
+      if (impl) {
+        const uint32_t scA = sA < n_rows ? sA : n_rows - 1u, scB = sB < n_rows ? sB : n_rows - 1u;
+        ppA = a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + scA)
+                                : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + scA);
+        ppB = a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + scB)
+                                : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + scB);
+      }
+    }
+#else
     if constexpr (HOIST) {
       oA = out_of(kA, sA);
       oB = out_of(kB, sB);
     }
+#endif
     const long long o0 = a.offset[kA], o1 = a.offset[kA + 1];
     const long long o2 = hasB ? a.offset[kA + 2] : o1;
     const bool skipA = a.seg_len > 0 && (int)((o1 - o0) >> 5) > a.seg_len;  // segment kernels own it
@@ -877,6 +894,14 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
       oA = out_of(kA, sA);
       oB = out_of(kB, sB);
     }
+#ifndef PSELL_PAIR_PERM_EARLY
+    if constexpr (HOIST) {
+      if (impl) {
+        oA = fast_div(kA * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppA;
+        oB = fast_div(kB * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppB;
+      }
+    }
+#endif
     if (!skipA) flush(sA, oA, accA);
     if (hasB && !skipB) flush(sB, oB, accB);
     if (!PERSIST) break;
@@ -1358,6 +1383,183 @@ __global__ void __launch_bounds__(kTileThreads, kTileCtasPerSm) spmv_tile_kernel
   finish_dot<DOT, kTileThreads>(a, dotv);
 }
 
+// ---- slot kernel (narrow slices, C == 32): the persistent pair kernel with the next
+// pair's words in flight during the current pair's gathers.
+// Each warp owns one shared-memory slot (a pair of slices <= 12 steps each: 3 KB)
+// and an mbarrier.  Iteration k: wait for pair k in the slot, copy it into
+// registers, and immediately refill the slot with pair k+1 (ONE cp.async.bulk by
+// lane 0, L2 evict-first), so pair k+1's HBM latency overlaps pair k's x gathers
+// and FMAs instead of following them.  No per-lane global word loads and no word
+// pointers in registers; lane 0 keeps the look-ahead offsets in shared memory and
+// every lane reads the current widths from there.  The same FMAs in the same order
+// as the pair kernel (bitwise equal).  Launched only when every slice is <= 12 steps
+// wide (PSELL_SPMV_NARROW12: 7-point rows are 9).
+constexpr int kSlotWords = 768;
+#ifndef PSELL_SLOT_MINB
+#define PSELL_SLOT_MINB 6  // resident CTAs per SM the slot kernel's register budget is sized for
+#endif
+constexpr int kSlotCtasPerSm = PSELL_SLOT_MINB;
+// per warp: the word slot, its mbarrier, two look-ahead offset triples (cp.async'd
+// 8-byte LDGSTS, so lane 0 never waits on an offset load) and the current widths
+struct SlotMeta {
+  long long off[2][4];
+  uint32_t cur;
+  uint32_t pad[3];
+};
+constexpr size_t kSlotSmemBytes = kWarpsPerCta * (kSlotWords * 4 + 8 + sizeof(SlotMeta));
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int CODEC, typename XT, bool DOT>
+__global__ void __launch_bounds__(kBlock, kSlotCtasPerSm) spmv_slot_kernel(const SpmvArgs a) {
+  using S = FastStep<CODEC, XT>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  extern __shared__ __align__(128) unsigned char slot_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(slot_smem) + warp * kSlotWords;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(slot_smem + kWarpsPerCta * kSlotWords * 4) + warp;
+  SlotMeta* meta = reinterpret_cast<SlotMeta*>(slot_smem + kWarpsPerCta * (kSlotWords * 4 + 8)) + warp;
+  const uint32_t ns = (uint32_t)a.n_slices;
+  const uint32_t npairs = (ns + 1u) >> 1;
+  const uint32_t wstride = gridDim.x * (unsigned)kWarpsPerCta;
+  uint32_t pk = blockIdx.x * (unsigned)kWarpsPerCta + warp;
+  // lanes 0..2: request the offset triple of pair p into look-ahead slot r (async)
+  auto request_offsets = [&](uint32_t p, int r) {
+    if (lane < 3 && p < npairs) {
+      const uint32_t kk = 2u * p + (uint32_t)lane;
+      cp_async8(&meta->off[r][lane], a.offset + (kk <= ns ? kk : ns));
+    }
+    cp_async_commit();
+  };
+  // lane 0: the bulk copy of a pair whose offsets sit in look-ahead slot r; records its widths
+  auto issue_words = [&](int r) {
+    const long long o0 = meta->off[r][0], o1 = meta->off[r][1], o2 = meta->off[r][2];
+    const uint32_t wA = (uint32_t)((o1 - o0) >> 5), wB = (uint32_t)((o2 - o1) >> 5);
+    meta->cur = wA | (wB << 16);
+    const uint32_t bytes = (wA + wB) * 128u;
+    if (bytes == 0) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(slot, static_cast<const uint32_t*>(a.pack) + o0, bytes, bar, policy_evict_first());
+  };
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // prologue: offsets of the first two pairs, words of the first
+  request_offsets(pk, 0);
+  request_offsets(pk + wstride, 1);
+  cp_async_wait_all();
+  __syncwarp();
+  if (lane == 0 && pk < npairs) issue_words(0);
+  __syncwarp();
+  int rnext = 1;  // look-ahead slot holding the offsets of the next pair
+  uint32_t phase = 0;
+  const XT* __restrict__ x = static_cast<const XT*>(a.x);
+  const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+  const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+  double dotv = 0.0;
+  constexpr int U = 12, K = PairK<12>::K;
+  for (; pk < npairs; pk += wstride) {
+    const uint32_t kA = 2u * pk, kB = kA + 1u;
+    const uint32_t n_rows = (uint32_t)a.n_rows;
+    const uint32_t sA = kA * 32u + lane, sB = sA + 32u;
+    // perm bytes issued first, consumed only at the flush: adding them into the output
+    // row right away put a full-latency stall in front of the word decode (ncu: the
+    // hottest stall of the pair kernel)
+    const bool impl = a.mode == PSELL_MODE_IMPLICIT;
+    auto perm_of = [&](uint32_t s) -> uint32_t {
+      if (!impl) return 0u;
+      const uint32_t sc = s < n_rows ? s : n_rows - 1u;
+      return a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc)
+                               : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
+    };
+    const uint32_t ppA = perm_of(sA), ppB = perm_of(sB);
+    auto base2 = [&](uint32_t k) -> uint32_t {
+      const uint32_t kl = (uint32_t)a.k_left;
+      const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+      const uint32_t g = (uint32_t)a.row0 + k * 32u + lane;
+      const uint32_t blk = a.se == 1 ? g : fast_div(g, a.se_m, a.se_l) * (uint32_t)a.se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    uint32_t cA = base2(kA), cB = base2(kB);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const uint32_t wab = meta->cur;
+    const int wA = (int)(wab & 0xFFFFu), wB = (int)(wab >> 16);
+    uint32_t wa[U], wb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      wa[u] = u < wA ? slot[u * 32 + lane] : 0u;
+      wb[u] = u < wB ? slot[(wA + u) * 32 + lane] : 0u;
+    }
+    // the next pair's offsets were requested an iteration ago: refill the slot with its
+    // words now, and request the offsets of the pair after it into the freed slot
+    cp_async_wait_all();
+    __syncwarp();
+    if (lane == 0 && pk + wstride < npairs) issue_words(rnext);
+    __syncwarp();
+    request_offsets(pk + 2u * wstride, rnext ^ 1);
+    rnext ^= 1;
+    float accA = 0.f, accB = 0.f;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      S::run(wa[u], cA, x, accA, m_real, vmask);
+      S::run(wb[u], cB, x, accB, m_real, vmask);
+    }
+    if (wA > K || wB > K) {
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        S::run(wa[u], cA, x, accA, m_real, vmask);
+        S::run(wb[u], cB, x, accB, m_real, vmask);
+      }
+    }
+    auto flush = [&](uint32_t k, uint32_t s, uint32_t pp, float acc) {
+      if (s < n_rows) {
+        const uint32_t o = impl ? fast_div(k * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + pp : s;
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
+      }
+    };
+    flush(kA, sA, ppA, accA);
+    if (kB < ns) flush(kB, sB, ppB, accB);
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
+// slot kernel for narrow slices instead of the persistent pair kernel (PSELL_SLOT=1: on, A/B).
+// Off by default: 7-point 256^3 e8m14 / f32 x 156-160 us at 6 CTAs/SM (40 registers,
+// 52-92 B of spills; ncu: long-scoreboard stalls per issue 13.4 -> 9.7, eligible warps
+// 1.5 -> 2.0, but 21 % more instructions) and 147 us at 5 CTAs/SM (48 registers, no
+// spills in the plain kernel) against the pair kernel's 146 us (scripts/slot_ab.py).
+static bool slot_kernel() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_SLOT", v)) return v != 0;
+  return false;
+}
+
+template <int CODEC, typename XT, bool DOT>
+static void launch_slot(const SpmvArgs& a, cudaStream_t st, unsigned grid) {
+  static bool attr = false;  // idempotent attribute, benign race
+  if (!attr) {
+    cudaFuncSetAttribute(spmv_slot_kernel<CODEC, XT, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSlotSmemBytes);
+    attr = true;
+  }
+  spmv_slot_kernel<CODEC, XT, DOT><<<grid, kBlock, kSlotSmemBytes, st>>>(a);
+}
+
 static int sm_count();
 
 template <int CODEC, typename XT, bool DOT>
@@ -1457,7 +1659,8 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
             const int pn = pair_nt(DOT);
             const unsigned gp = (unsigned)ceil_div(ceil_div(a.n_slices, 2), pn / 32);
             const unsigned gpp = pair_persist_grid(a.n_slices, DOT);
-            if (gpp) spmv_pair_kernel<CODEC, XT, DOT, PSELL_PAIR_U, true, kBlock, true><<<gpp, kBlock, 0, st>>>(a);
+            if (gpp && slot_kernel() && a.narrow12 && a.seg_len == 0) launch_slot<CODEC, XT, DOT>(a, st, gpp);
+            else if (gpp) spmv_pair_kernel<CODEC, XT, DOT, PSELL_PAIR_U, true, kBlock, true><<<gpp, kBlock, 0, st>>>(a);
             else if (pn == 64) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 64><<<gp, 64, 0, st>>>(a);
             else if (pn == 128) spmv_pair_kernel<CODEC, XT, DOT, 12, true, 128><<<gp, 128, 0, st>>>(a);
             else spmv_pair_kernel<CODEC, XT, DOT, 12, true><<<gd, kBlock, 0, st>>>(a);
@@ -1541,6 +1744,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.perm_bytes = d->sigma <= 256 ? 1 : 2;
   a.variant = 0;
   a.narrow = 0;
+  a.narrow12 = 0;
   a.codec = d->codec;
   a.seg_len = 0;
   a.seg_slice = a.seg_q0 = a.long_slice = a.long_seg0 = nullptr;
@@ -1674,6 +1878,7 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
   const bool ref = (flags & PSELL_SPMV_REF_ORDER) != 0;
   a.variant = (flags & PSELL_SPMV_TMA_STREAM) ? 2 : 0;
   a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
+  a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
   int bad = 1;
   switch (d->codec) {
     case PSELL_FP16: bad = dispatch_x<PSELL_FP16>(a, x_dtype, ref, st); break;
@@ -1695,7 +1900,10 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   const long long ns = ceil_div(d->n_rows, d->c);
   if ((flags & PSELL_SPMV_NARROW) && tile_kernel()) return "spmv_tile_kernel (TMA ring)";
   if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel())
-    return pair_persist_grid(ns, false) ? "spmv_pair_kernel<U=12, persistent>" : "spmv_pair_kernel<U=12>";
+    return pair_persist_grid(ns, false) ? (slot_kernel() && (flags & PSELL_SPMV_NARROW12)
+                                               ? "spmv_slot_kernel (TMA slot per warp, persistent)"
+                                                         : "spmv_pair_kernel<U=12, persistent>")
+                                        : "spmv_pair_kernel<U=12>";
   if (dual_slices(ns) && pair_wide()) return "spmv_pair_kernel<U=8>";
   if (dual_slices(ns)) {
     const int du = dual_chunk((flags & PSELL_SPMV_NARROW) != 0);
@@ -1826,6 +2034,7 @@ int psell_spmv_dot(const psell_desc* d, const void* pack, const int64_t* offset,
   SpmvArgs a;
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
   a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
+  a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
   a.x = x;
   a.y = y;
   a.p_own = p_own;
@@ -1852,6 +2061,7 @@ int psell_spmv_dot_alpha(const psell_desc* d, const void* pack, const int64_t* o
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
   if (!ticket || !scal || !iflags) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null scalar state");
   a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
+  a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
   a.x = x;
   a.y = y;
   a.p_own = p_own;

@@ -200,7 +200,17 @@ class PackSellMatrix:
         mean slice width is <= 12 steps (7-point rows), so one 12-step chunk covers a slice."""
         if self.n_slices == 0:
             return 0
-        return 4 if self.n_stored <= 12 * self.c * self.n_slices else 0
+        f = self.__dict__.get("_flags_cache")
+        if f is None:
+            f = 0
+            if self.n_stored <= 12 * self.c * self.n_slices:
+                f = 4  # PSELL_SPMV_NARROW
+                import torch
+                wmax = int(torch.max(self.d_offset[1:] - self.d_offset[:-1]).item()) // self.c
+                if wmax <= 12:
+                    f |= 8  # PSELL_SPMV_NARROW12: every slice fits the slot kernel's 12 steps
+            self.__dict__["_flags_cache"] = f
+        return f
 
     def spmv_bytes(self, x_itemsize: int, y_itemsize: Optional[int] = None, with_perm: bool = True,
                    x_elems: Optional[int] = None) -> int:
