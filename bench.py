@@ -200,36 +200,102 @@ def _digest(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8)).hexdigest()
 
 
-def _slab_parity(O, M, A, vals, x, expect):
-    """Compare the oracle slab with the GPU's production matrix over the same rows.
+def reference_pkg():
+    """The reference package itself (`packsell` 0.1.0, pure Python/numpy), pip-installed from
+    /root/reference into baseline/_ref (git-ignored; it travels to the GPU box with the
+    snapshot; __graft_entry__.build() installs it).  None when absent: the CPU legs then
+    time the oracle port instead (kind "port")."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(p, "packsell")):
+        return None
+    if p not in sys.path:
+        sys.path.append(p)
+    try:
+        import packsell
+        return packsell
+    except Exception:  # noqa: BLE001
+        return None
 
-    `expect` holds the GPU side: sha256 of the pack words / rebased offsets / perm
-    of the slab's slices in the full device build, and the device REF_ORDER and
-    FMA SpMV outputs on those rows for the same x (SURVEY §8c parity rules 1-3)."""
+
+class CpuPath:
+    """One CPU implementation of the path on a row slab [r0, r1) of a config matrix:
+    the reference's own build_packsell / packsell_spmv (kind "reference") or the oracle
+    port (kind "port").  The reference has no row origin, so its slab is a CsrMatrix of
+    r1 rows whose first r0 rows are empty: same base offsets (global rows, global k_left),
+    hence the same words as the production matrix's slices over [r0, r1), at the cost of
+    r0 empty rows (no words)."""
+
+    def __init__(self, cfg, A, vals, r0, k_left, prefer_reference=True):
+        self.ref = reference_pkg() if prefer_reference else None
+        self.kind = "reference" if self.ref is not None else "port"
+        self.r0, self.n = r0, A.n_rows
+        c, sg = cfg["c"], cfg["sigma"]
+        if self.ref is not None:
+            R = self.ref
+            rp = np.concatenate([np.zeros(r0, np.int64), A.row_ptr])
+            Af = R.CsrMatrix(r0 + A.n_rows, A.n_cols, rp, A.col_idx, vals)
+            self.M = R.build_packsell(Af, c, sg, R.parse_format(cfg["preset"]), cfg["mode"], _k_left_override=k_left)
+            s0 = r0 // c
+            off = self.M.offset
+            self.pack = self.M.pack
+            self.offset = off[s0:] - off[s0]
+            self.perm = self.M.perm[r0:] if self.M.perm is not None else None
+            self.k_left = self.M.k_left
+            self.counts = tuple(self.M.counts)
+        else:
+            import oracle as O
+            self.M = O.build(A.row_ptr, A.col_idx, vals, A.n_cols, c, sg, O.preset(cfg["preset"]), cfg["mode"],
+                             k_left=k_left, row0=r0)
+            self.pack, self.offset, self.perm = self.M.pack, self.M.offset, self.M.perm
+            self.k_left, self.counts = self.M.k_left, tuple(self.M.counts)
+
+    def spmv(self, x):
+        """y over the slab's rows (the reference call: packed.py:242)."""
+        if self.ref is not None:
+            return self.ref.packsell_spmv(self.M, x)[self.r0:]
+        import oracle as O
+        return O.spmv(self.M, x)
+
+    def nbytes(self, xsz, touched):
+        """SURVEY §8d bytes of the slab's SpMV (x counted over the columns it touches)."""
+        n_sl = len(self.offset) - 1
+        b = 4 * int(self.pack.size) * (2 if self.pack.dtype.itemsize == 8 else 1) + 8 * (n_sl + 1)
+        b += xsz * touched + xsz * self.n
+        if self.perm is not None:
+            b += self.perm.dtype.itemsize * self.n
+        return b
+
+
+def _slab_parity(P, A, vals, x, expect, preset):
+    """Compare the CPU implementation's slab with the GPU's production matrix over the same rows.
+
+    `expect` holds the GPU side: sha256 of the pack words / rebased offsets / perm of the
+    slab's slices in the full device build, and the device REF_ORDER and FMA SpMV outputs
+    on those rows for the same x (SURVEY §8c parity rules 1-3)."""
+    import oracle as O
     f16 = x.dtype == np.float16
-    y_ref = O.spmv(M, x)
-    y_wide = O.spmv(M, x.astype(np.float32)) if f16 else y_ref
-    q = np.abs(O.quantize(M.fmt, vals))
+    y_ref = P.spmv(x)
+    y_wide = P.spmv(x.astype(np.float32)) if f16 else y_ref
+    q = np.abs(O.quantize(O.preset(preset), vals))
     anorm = float(np.max(np.add.reduceat(q, A.row_ptr[:-1]))) if A.nnz else 0.0
-    lmax = int(np.diff(M.offset).max() // M.c)
+    lmax = int(np.diff(P.offset).max() // 32)
     e = float(np.abs(expect["y_fma"].astype(np.float64) - y_wide.astype(np.float64)).max()) / max(
         anorm * float(np.abs(x.astype(np.float64)).max()), 1e-300)
     bound = (2.0 ** -11 if f16 else 0.0) + 2 * lmax * 2.0 ** -24
-    res = {"pack": _digest(M.pack) == expect["pack_sha"],
-           "offset": _digest(M.offset) == expect["offset_sha"],
-           "perm": _digest(M.perm) == expect["perm_sha"],
-           "k_left": M.k_left == expect["k_left"],
+    res = {"against": P.kind, "pack": _digest(P.pack) == expect["pack_sha"],
+           "offset": _digest(P.offset) == expect["offset_sha"],
+           "perm": _digest(P.perm) == expect["perm_sha"],
+           "k_left": P.k_left == expect["k_left"],
            "spmv_ref_order_bitwise": bool(np.array_equal(y_ref.view(np.uint8), expect["y_ref"].view(np.uint8))),
            "spmv_fma_e_rel": e, "spmv_fma_bound": bound}
     ok = all(res[k] for k in ("pack", "offset", "perm", "k_left", "spmv_ref_order_bitwise")) and e <= bound
     res["status"] = "bitwise" if ok else "MISMATCH"
-    res["words_compared"] = int(M.offset[-1])
+    res["words_compared"] = int(P.offset[-1])
     return res
 
 
-def _cpu_worker(conn, cfg, r0, r1, k_left, seed, expect=None):
-    os.environ["OMP_NUM_THREADS"] = "1"
-    import oracle as O
+def _cpu_slab(cfg, r0, r1):
+    """Host CSR rows [r0, r1) of a config matrix with the reference's scaling (matrix.py:294-316)."""
     from paper_2604_13433_b200.stencil import stencil_rows
     if cfg["kind"] == "powerlaw":
         from paper_2604_13433_b200.stencil import powerlaw_rows
@@ -245,20 +311,27 @@ def _cpu_worker(conn, cfg, r0, r1, k_left, seed, expect=None):
         s = np.zeros(A.n_rows)
         np.add.at(s, rows, np.abs(vals))
         vals = vals / s[rows]
-    M = O.build(A.row_ptr, A.col_idx, vals, A.n_cols, cfg["c"], cfg["sigma"], O.preset(cfg["preset"]),
-                cfg["mode"], k_left=k_left, row0=r0)
+    return A, vals
+
+
+def _cpu_worker(conn, cfg, r0, r1, k_left, seed, expect=None):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    A, vals = _cpu_slab(cfg, r0, r1)
+    t0 = time.perf_counter()
+    P = CpuPath(cfg, A, vals, r0, k_left)
+    t_build = time.perf_counter() - t0
     xsz = np.dtype(cfg["xdt"]).itemsize
     touched = int(A.col_idx.max()) - int(A.col_idx.min()) + 1 if A.nnz else 0
-    nbytes = O.spmv_bytes(M, xsz, xsz) - xsz * A.n_cols + xsz * touched
+    nbytes = P.nbytes(xsz, touched)
     x = np.random.default_rng(seed).uniform(-1, 1, A.n_cols).astype(cfg["xdt"])
-    parity = None if expect is None else _slab_parity(O, M, A, vals, x, expect)
-    conn.send(("ready", nbytes, A.nnz, parity))
+    parity = None if expect is None else _slab_parity(P, A, vals, x, expect, cfg["preset"])
+    conn.send(("ready", nbytes, A.nnz, parity, P.kind, t_build))
     while True:
         msg = conn.recv()
         if msg == "stop":
             break
         t0 = time.perf_counter()
-        O.spmv(M, x)
+        P.spmv(x)
         conn.send(time.perf_counter() - t0)
 
 
@@ -275,6 +348,11 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
     workers = max(1, min(workers, n // rows_per_worker))
     procs, conns = [], []
     stride = (n // workers) // cfg["sigma"] * cfg["sigma"]
+    if reference_pkg() is not None:
+        # the reference has no row origin: a slab at r0 > 0 would carry r0 empty rows whose
+        # per-row work (y, the output index) is not the sample's; every worker runs the
+        # matrix's first rows instead (interior stencil rows are all alike)
+        stride = 0
     for w in range(workers):
         a, b = mp.Pipe()
         r0 = w * stride
@@ -283,12 +361,13 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
         p.start()
         procs.append(p)
         conns.append(a)
-    tot_bytes, tot_nnz, parity = 0, 0, None
+    tot_bytes, tot_nnz, parity, kind, t_build = 0, 0, None, "port", 0.0
     for c in conns:
-        _, nb, nz, par = c.recv()
+        _, nb, nz, par, kind, tb = c.recv()
         tot_bytes += nb
         tot_nnz += nz
         parity = parity or par
+        t_build = max(t_build, tb)
     times = []
     for it in range(warmup + steps):
         t0 = time.perf_counter()
@@ -304,7 +383,8 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
         p.join()
     t = float(np.mean(times))
     return dict(gbs=tot_bytes / t / 1e9, gflops=2 * tot_nnz / t / 1e9, sec_per_step=t, workers=workers,
-                rows=rows_per_worker, bytes=tot_bytes, nnz=tot_nnz, parity=parity)
+                rows=rows_per_worker, bytes=tot_bytes, nnz=tot_nnz, parity=parity, kind=kind, build_s=t_build,
+                sec_min=float(np.min(times)))
 
 
 def run_reference(args, cfg):
@@ -313,8 +393,11 @@ def run_reference(args, cfg):
         return
     cores = os.cpu_count() or 1
     r = cpu_reference(cfg, cores, args.ref_rows, args.steps, args.warmup)
+    what = ("the reference's own packsell.packsell_spmv (baseline/_ref, pure numpy)" if r["kind"] == "reference"
+            else "oracle port of packsell_spmv (numpy)")
+    where = ("each on rows 0..%d" % (r["rows"] - 1)) if r["kind"] == "reference" else "on disjoint sigma-aligned slabs"
     sample = (f"{r['workers']} worker processes x {r['rows']} rows ({r['nnz']} nnz total) of the same matrix, "
-              f"sigma-aligned slabs, global k_left; oracle port of packsell_spmv (numpy, 1 thread each)")
+              f"{where}, global k_left; {what}, 1 thread each; os.cpu_count() = {cores}")
     line = {
         "metric": METRIC, "value": r["gbs"], "unit": "GB/s", "impl": "reference",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
@@ -322,8 +405,8 @@ def run_reference(args, cfg):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_label(cfg, "reference"),
         "data": "synthetic", "config": {"workload": cfg["workload"], "cpu_sample": sample},
         "gflops": r["gflops"],
-        "cpu_baseline": {"value": r["gbs"], "unit": "GB/s", "cores": r["workers"], "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": r["gbs"], "unit": "GB/s", "cores": r["workers"], "kind": r["kind"],
+                         "sample": sample, "ms_per_step_min": r["sec_min"] * 1e3, "build_s_per_worker": r["build_s"]},
         "e2e": {"value": r["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -336,6 +419,117 @@ def pcg_bytes(M, n_local, nnz_local, n_glob_touched):
     csr64 = 8 * (n_local + 1) + 12 * nnz_local + 8 * n_glob_touched + 8 * n_local
     outer = csr64 + 168 * n_local
     return inner, outer
+
+
+def pcg_cpu_baseline(args, nx, rep_io, rep64, t_io, t_64):
+    """Config 5 on the host CPU as BASELINE.md §3 plans it, with the reference's own solvers
+    (baseline/_ref: packsell.iocg / pcg, pure numpy, one core) when installed, else the
+    oracle port: full solves at 64^3 (and 128^3 with --pcg-cpu-full: ~8 min), and at the
+    GPU's grid a fixed window -- 3 inner PCG iterations on the PackSELL e8m14 operator and
+    2 FP64 PCG iterations -- extrapolated by the GPU run's own iteration counts
+    (labelled "extrapolated")."""
+    R = reference_pkg()
+    kind = "reference" if R is not None else "port"
+    from paper_2604_13433_b200 import solvers as S
+
+    def problem(m):
+        if R is not None:
+            return R.sym_diag_scale(R.poisson3d(m))
+        import paper_2604_13433_b200 as P
+        return P.sym_diag_scale(P.poisson3d(m))
+
+    def solve_full(m):
+        A = problem(m)
+        b = S.make_rhs_and_x0(A.n_rows, 42)[0]
+        res = {"grid": f"{m}^3", "n": A.n_rows}
+        if R is not None:
+            t = time.perf_counter()
+            r = R.iocg(A, b, R.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="packsell-e8m14",
+                                           max_outer=400))
+            res["iocg"] = {"solve_s": time.perf_counter() - t, "outer_iters": r.outer_iters,
+                           "inner_iters": r.total_inner_iters, "converged": r.converged,
+                           "true_relres": r.final_true_relres}
+            t = time.perf_counter()
+            r = R.pcg(A, b, R.SolveConfig(tol=1e-9, max_outer=5000))
+            res["fp64_pcg"] = {"solve_s": time.perf_counter() - t, "iters": r.outer_iters, "converged": r.converged,
+                               "true_relres": r.final_true_relres}
+        else:
+            import oracle as O
+            OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, 256, O.preset("e8m14"), "implicit")
+            ap64 = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64)  # noqa: E731
+            t = time.perf_counter()
+            r = O.iocg(ap64, lambda v: O.spmv(OM, v), b, 1e-9, 400, args.pcg_m_in)
+            res["iocg"] = {"solve_s": time.perf_counter() - t, "outer_iters": r["outer_iters"],
+                           "inner_iters": r["total_inner_iters"], "converged": r["converged"]}
+            t = time.perf_counter()
+            r = O.pcg(ap64, b, 1e-9, 5000)
+            res["fp64_pcg"] = {"solve_s": time.perf_counter() - t, "iters": r["outer_iters"],
+                               "converged": r["converged"]}
+        return res
+
+    out = {"kind": kind, "cores": 1, "os_cpu_count": os.cpu_count(),
+           "what": ("the reference's own packsell.iocg / packsell.pcg (baseline/_ref)" if R is not None
+                    else "the oracle port of iocg / pcg"),
+           "full": [solve_full(m) for m in ([64, 128] if args.pcg_cpu_full else [64])]}
+    def window(m, k_in=3, k_pcg=4):
+        """(s per inner PCG iteration, s per FP64 PCG iteration, gen s, build s) at m^3."""
+        t0 = time.perf_counter()
+        A = problem(m)
+        b = S.make_rhs_and_x0(A.n_rows, 42)[0]
+        t_gen = time.perf_counter() - t0
+        ts = []
+        if R is not None:
+            from packsell import solvers as RS
+            t0 = time.perf_counter()
+            be = RS.make_backend(A, "packsell-e8m14")
+            t_build = time.perf_counter() - t0
+            RS._inner_pcg(be.apply, b, 1, lambda r: r, np.float32)  # builds the SpMV plan cache
+            t0 = time.perf_counter()
+            RS._inner_pcg(be.apply, b, k_in, lambda r: r, np.float32)
+            t_in = (time.perf_counter() - t0) / k_in
+            del be
+            for k in (1, 1 + k_pcg):
+                t0 = time.perf_counter()
+                R.pcg(A, b, R.SolveConfig(tol=1e-300, max_outer=k))
+                ts.append(time.perf_counter() - t0)
+        else:
+            import oracle as O
+            t0 = time.perf_counter()
+            OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, 256, O.preset("e8m14"), "implicit")
+            t_build = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            O.inner_pcg(lambda v: O.spmv(OM, v), b, k_in)
+            t_in = (time.perf_counter() - t0) / k_in
+            ap64 = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64)  # noqa: E731
+            for k in (1, 1 + k_pcg):
+                t0 = time.perf_counter()
+                O.pcg(ap64, b, 1e-300, k)
+                ts.append(time.perf_counter() - t0)
+        return t_in, (ts[1] - ts[0]) / k_pcg, t_gen, t_build
+
+    def extrap(t_in, t64, inner, outer, iters64):
+        return inner * t_in + (outer + 1) * t64, iters64 * t64
+
+    # the window model checked against the full 64^3 solves, then applied at the GPU's grid
+    f64 = out["full"][0]
+    w = window(64)
+    e_io, e_64 = extrap(w[0], w[1], f64["iocg"]["inner_iters"], f64["iocg"]["outer_iters"],
+                        f64["fp64_pcg"]["iters"])
+    out["window_model_check_64"] = {"iocg_extrapolated_over_measured": e_io / f64["iocg"]["solve_s"],
+                                    "fp64_pcg_extrapolated_over_measured": e_64 / f64["fp64_pcg"]["solve_s"]}
+    if nx <= 256:
+        t_in, t_it64, t_gen, t_build = window(nx) if nx != 64 else w
+        io_s, p64_s = extrap(t_in, t_it64, rep_io.total_inner_iters, rep_io.outer_iters, rep64.outer_iters)
+        out["window"] = {
+            "grid": f"{nx}^3", "label": "extrapolated",
+            "how": f"3 inner PCG iterations (f32, PackSELL e8m14 operator) and 4 FP64 PCG iterations timed at "
+                   f"{nx}^3; IO-CG = GPU inner iterations x t_inner + (GPU outer iterations + 1) x "
+                   f"t_fp64_iteration; FP64 PCG = GPU iterations x t_fp64_iteration (model checked at 64^3: "
+                   f"window_model_check_64)",
+            "s_per_inner_iter": t_in, "s_per_fp64_iter": t_it64, "gen_s": t_gen, "build_s": t_build,
+            "iocg_solve_s_extrapolated": io_s, "fp64_pcg_solve_s_extrapolated": p64_s,
+            "gpu_speedup_iocg": io_s / t_io, "gpu_speedup_fp64_pcg": p64_s / t_64}
+    return out
 
 
 def run_pcg(args, world, rank, comm, peak):
@@ -422,21 +616,7 @@ def run_pcg(args, world, rank, comm, peak):
             "FP64 per-rank dot sums (rank-ordered), eager"),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle as O
-        m = args.pcg_cpu_nx
-        H = P.sym_diag_scale(P.poisson3d(m))
-        bh = S.make_rhs_and_x0(H.n_rows, 42)[0]
-        OM = O.build(H.row_ptr, H.col_idx, H.values, H.n_cols, 32, 256, O.preset("e8m14"), "implicit")
-        t = time.perf_counter()
-        rr = O.iocg(lambda v: O.csr_spmv(H.row_ptr, H.col_idx, H.values, v, np.float64),
-                    lambda v: O.spmv(OM, v), bh, 1e-9, 400, args.pcg_m_in)
-        dt = time.perf_counter() - t
-        out["cpu_baseline"] = {"kind": "port", "cores": 1, "problem": f"same protocol at {m}^3 (n={m**3})",
-                               "solve_s": dt, "inner_iters": rr["total_inner_iters"],
-                               "ms_per_inner_iter": 1e3 * dt / max(rr["total_inner_iters"], 1),
-                               "gpu_speedup_per_inner_iter_scaled_by_n":
-                                   (dt / max(rr["total_inner_iters"], 1)) * (n / m ** 3)
-                                   / (t_io / max(rep.total_inner_iters, 1))}
+        out["cpu_baseline"] = pcg_cpu_baseline(args, nx, rep, rep64, t_io, t_64)
     return out
 
 
@@ -720,13 +900,15 @@ def run_ours(args, cfg):
         expect = gpu_slab_expect(M, cfg, rows, 7)
         r = cpu_reference(cfg, 1, args.cpu_rows, 3, 1, expect=expect)
         parity = r["parity"]
+        who = "the reference's own build_packsell / packsell_spmv" if r["kind"] == "reference" else "the oracle port"
         parity["sample"] = (f"rows 0..{rows - 1} of the benchmarked matrix: the GPU production build's words / "
-                            f"offsets / perm over those slices and its SpMV outputs on those rows vs the oracle "
-                            f"slab (global k_left)")
-        cpu = {"value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": "port",
+                            f"offsets / perm over those slices and its SpMV outputs on those rows vs {who} on the "
+                            f"same rows (global k_left)")
+        cpu = {"value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": r["kind"],
                "sample": f"{r['rows']} rows (rows 0..{r['rows'] - 1}, {r['nnz']} nnz) of the same matrix, "
-                         f"global k_left; oracle port of packsell_spmv, numpy single thread; "
-                         f"{r['gflops']:.4f} GFLOP/s"}
+                         f"global k_left; {who}, numpy single thread; {r['gflops']:.4f} GFLOP/s; "
+                         f"build {r['build_s']:.2f} s; os.cpu_count() = {os.cpu_count()}",
+               "ms_per_step_min": r["sec_min"] * 1e3}
 
     # every collective runs on all ranks, before the rank-0-only report
     bytes_noperm_all = allreduce(float(bytes_noperm), dist.ReduceOp.SUM if world > 1 else None)
@@ -813,7 +995,8 @@ def main():
     ap.add_argument("--no-vendor", action="store_true", help="skip the cuSPARSE CSR comparison")
     ap.add_argument("--pcg-nx", type=int, default=256)
     ap.add_argument("--pcg-m-in", type=int, default=50)
-    ap.add_argument("--pcg-cpu-nx", type=int, default=32)
+    ap.add_argument("--pcg-cpu-full", action="store_true",
+                    help="also run the full 128^3 CPU solves of the config-5 baseline (~8 min)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N`: one process per GPU, launched here the way the

@@ -38,7 +38,7 @@ def test_partitions_cover_rows():
 
 
 def test_reference_arm_sample_runs(capsys):
-    """The CPU reference arm (oracle port) on a tiny sample prints the contract's JSON line."""
+    """The CPU reference arm on a tiny sample prints the contract's JSON line."""
     cfg = dict(bench.CONFIGS["c1"])
 
     class A:
@@ -49,7 +49,9 @@ def test_reference_arm_sample_runs(capsys):
     bench.run_reference(A, cfg)
     line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    # the reference's own code when baseline/_ref is installed, else the oracle port
+    want = "reference" if bench.reference_pkg() is not None else "port"
+    assert line["cpu_baseline"]["kind"] == want and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["metric"] == bench.METRIC and line["higher_is_better"] is True
 
 
@@ -66,3 +68,21 @@ def test_bench_spawns_ranks_for_gpus_n():
     lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout
     assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+
+
+def test_cpu_path_reference_equals_oracle_on_a_slab():
+    """The reference arm's slab trick (r0 empty rows, global k_left) reproduces the oracle's
+    slab build with a row origin byte for byte, and the same REF SpMV."""
+    import numpy as np
+    if bench.reference_pkg() is None:
+        pytest.skip("reference not installed in baseline/_ref")
+    cfg = dict(bench.CONFIGS["c2"], nx=16)
+    A, vals = bench._cpu_slab(cfg, 256, 1024)
+    kl = bench.stencil_k_left("stencil27", 16)
+    Pr = bench.CpuPath(cfg, A, vals, 256, kl)
+    Po = bench.CpuPath(cfg, A, vals, 256, kl, prefer_reference=False)
+    assert Pr.kind == "reference" and Po.kind == "port"
+    assert np.array_equal(Pr.pack, Po.pack) and np.array_equal(Pr.offset, Po.offset)
+    assert np.array_equal(Pr.perm, Po.perm) and Pr.counts == Po.counts
+    x = np.random.default_rng(0).uniform(-1, 1, A.n_cols).astype(np.float16)
+    assert np.array_equal(Pr.spmv(x).view(np.uint16), Po.spmv(x).view(np.uint16))
