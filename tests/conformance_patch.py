@@ -6,3 +6,8 @@ import packsell
 from paper_2604_13433_b200.integration import patch_reference
 
 PATCHED = patch_reference(packsell)
+
+
+def pytest_report_header(config):
+    return [f"b200-conformance: patched {len(PATCHED)} reference names "
+            f"(e.g. {', '.join(sorted(PATCHED)[:3])})"]
