@@ -169,14 +169,7 @@ class PeerTransport:
         key = None if halo is None else id(halo)
         if key not in self._plans:
             import torch
-            if halo is not None and not halo.use_allgather:
-                dst = np.concatenate([np.full(len(v), s, np.int32) for s, v in enumerate(halo.send_lists)]
-                                     + [np.zeros(0, np.int32)])
-                loc = halo.send_idx.astype(np.int32)
-            else:
-                peers = [s for s in range(self.G) if s != self.rank]
-                dst = np.repeat(np.asarray(peers, np.int32), n_local)
-                loc = np.tile(np.arange(n_local, dtype=np.int32), len(peers))
+            dst, loc = push_lists(halo, self.rank, self.G, n_local)
             self._plans[key] = (torch.as_tensor(dst).cuda(), torch.as_tensor(loc).cuda(), int(row0), len(dst))
         return self._plans[key]
 
@@ -323,6 +316,20 @@ class Halo:
         return full
 
 
+def push_lists(halo, rank: int, world: int, n_local: int):
+    """(destination rank, local row) of every entry this rank pushes per exchange over peer
+    memory: the halo plan's send lists (each peer gets the columns its slab reads from this
+    rank), or the whole slab to every other rank when the plan falls back to the
+    all-gather (halo None or use_allgather).  Host side of PeerTransport.plan."""
+    if halo is not None and not halo.use_allgather:
+        dst = np.concatenate([np.full(len(v), s, np.int32) for s, v in enumerate(halo.send_lists)]
+                             + [np.zeros(0, np.int32)])
+        return dst, halo.send_idx.astype(np.int32)
+    peers = [s for s in range(world) if s != rank]
+    return (np.repeat(np.asarray(peers, np.int32), n_local),
+            np.tile(np.arange(n_local, dtype=np.int32), len(peers)))
+
+
 def equal_row_slabs(n: int, world: int, sigma: int) -> List[Tuple[int, int]]:
     """sigma-aligned contiguous row slabs, as equal as the sigma granularity allows.
 
@@ -375,4 +382,4 @@ def rank_order_sum(parts: np.ndarray) -> float:
     return s
 
 
-__all__ = ["Comm", "PeerTransport", "Halo", "equal_row_slabs", "check_equal", "word_balanced_slabs", "rank_order_sum"]
+__all__ = ["Comm", "PeerTransport", "push_lists", "Halo", "equal_row_slabs", "check_equal", "word_balanced_slabs", "rank_order_sum"]

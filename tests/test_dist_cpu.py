@@ -148,3 +148,54 @@ def test_gloo_world2_halo_exchange():
         assert not h_ag and g_ag
     # what rank 0 receives from rank 1 is what rank 1 sends to rank 0, and vice versa
     assert res[0][5][1] == res[1][6][0] and res[1][5][0] == res[0][6][1]
+
+
+def _push_worker(rank, world, port, slabs, use_halo, q):
+    """Simulate the peer transport's pushes: every rank contributes its push lists; the
+    entries pushed to rank s are applied to rank s's full vector; the columns rank s's
+    rows read must then hold their owners' values (equal or unequal slabs)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = D.Comm()
+        nx = 8
+        n = nx ** 3
+        r0, r1 = slabs[rank]
+        A = stencil.poisson3d(nx)
+        cols = A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]]
+        h = D.Halo(comm, r0, r1, cols, n_cols=n) if use_halo else None
+        dst, loc = D.push_lists(h, rank, world, r1 - r0)
+        vals = (r0 + loc.astype(np.int64)) * 0.25 + 3.0   # the owner's p at those global rows
+        pushed = [None] * world
+        dist.all_gather_object(pushed, (dst, r0 + loc.astype(np.int64), vals))
+        full = np.zeros(n)
+        full[r0:r1] = np.arange(r0, r1) * 0.25 + 3.0
+        for d_, g_, v_ in pushed:
+            sel = d_ == rank
+            full[g_[sel]] = v_[sel]
+        need = np.unique(cols)
+        ok = bool(np.array_equal(full[need], need * 0.25 + 3.0))
+        q.put((rank, ok, int(len(dst)), None if h is None else h.volume))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,slabs,use_halo", [
+    (2, [(0, 256), (256, 512)], True),
+    (3, [(0, 96), (96, 352), (352, 512)], True),     # unequal slabs: addressed by global index
+    (3, [(0, 96), (96, 352), (352, 512)], False),    # all-gather fallback over peer memory
+])
+def test_peer_push_lists_cover_every_read_column(world, slabs, use_halo):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_push_worker, args=(r, world, port, slabs, use_halo, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _, _ in res), res
+    if not use_halo:
+        assert [k for _, _, k, _ in res] == [(b - a) * (world - 1) for a, b in slabs]
