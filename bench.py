@@ -349,7 +349,7 @@ def cpu_reference(cfg, workers: int, rows_per_worker: int, steps: int, warmup: i
     ctx = mp.get_context("fork")
     n = cfg_rows(cfg)
     kl = stencil_k_left(cfg["kind"], cfg["nx"])
-    rows_per_worker = max(cfg["sigma"], rows_per_worker // cfg["sigma"] * cfg["sigma"])
+    rows_per_worker = max(cfg["sigma"], min(rows_per_worker, n) // cfg["sigma"] * cfg["sigma"])
     workers = max(1, min(workers, n // rows_per_worker))
     procs, conns = [], []
     stride = (n // workers) // cfg["sigma"] * cfg["sigma"]
@@ -906,7 +906,7 @@ def run_ours(args, cfg):
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows = max(sig, args.cpu_rows // sig * sig)
+        rows = max(sig, min(args.cpu_rows, M.n_rows) // sig * sig)
         expect = gpu_slab_expect(M, cfg, rows, 7)
         r = cpu_reference(cfg, 1, args.cpu_rows, 3, 1, expect=expect)
         parity = r["parity"]
