@@ -929,7 +929,21 @@ def run_ours(args, cfg):
         from paper_2604_13433_b200 import dist as D
         del M, x, y, xh, yh
         torch.cuda.empty_cache()
-        pcg = run_pcg(args, world, rank, D.Comm() if world > 1 else None, peak)
+        comm = D.Comm() if world > 1 else None
+        try:
+            pcg = run_pcg(args, world, rank, comm, peak)
+        except Exception as e:  # noqa: BLE001
+            if comm is None or os.environ.get("PSELL_XPORT") == "nccl":
+                raise
+            # the peer-memory transport failed on this node (IPC mapping refused, or a wait
+            # timed out on every rank alike): rerun the solves over torch.distributed
+            comm.close()
+            os.environ["PSELL_XPORT"] = "nccl"
+            comm = D.Comm()
+            pcg = run_pcg(args, world, rank, comm, peak)
+            pcg["transport_fallback"] = f"peer transport failed ({repr(e)[:160]}); solved over torch.distributed"
+        if comm is not None:
+            comm.close()
 
     if rank == 0:
         line = {
