@@ -417,7 +417,11 @@ template <bool GR> struct FastStep<PSELL_E8MY, float, GR> {
                              uint32_t vmask) {
     const uint32_t f = w & 1u;
     c2 += w & (f ? m_real : 0xFFFFFFFEu);
+#ifdef PSELL_DEBUG_NOGATHER  // measurement-only build: the word stream without the x gathers
+    const float xv = __uint_as_float(c2 & 0x3F800000u);
+#else
     const float xv = gather_f32<GR>(xbyte(x, c2), f);
+#endif
     const float v = __uint_as_float(w & vmask);
     asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
         : "+f"(acc) : "r"(f), "f"(v), "f"(xv));
