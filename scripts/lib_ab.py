@@ -13,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2604_13433_b200 as P  # noqa: E402
 
-cfg = dict(bench.CONFIGS[sys.argv[1]])
+C5 = dict(kind="poisson3d", nx=256, preset="e8m14", xdt="float32", scale="sym", c=32, sigma=256, mode="implicit")
+cfg = dict(C5) if sys.argv[1] == "c5" else dict(bench.CONFIGS[sys.argv[1]])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 S = bench.make_slab(cfg, 0, bench.cfg_rows(cfg))
 M = P.build_packsell(S, cfg["c"], cfg["sigma"], P.parse_format(cfg["preset"]), cfg["mode"])
