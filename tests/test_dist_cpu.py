@@ -199,3 +199,43 @@ def test_peer_push_lists_cover_every_read_column(world, slabs, use_halo):
     assert all(ok for _, ok, _, _ in res), res
     if not use_halo:
         assert [k for _, _, k, _ in res] == [(b - a) * (world - 1) for a, b in slabs]
+
+
+def _slab_check_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_13433_b200 import solvers as S
+        comm = D.Comm()
+        out = []
+        # equal, rank-ordered slabs pass the all-gather check
+        S._check_slabs(comm, rank * 512, 512, None, None)
+        out.append("equal ok")
+        # unequal slabs: refused for the all-gather transport ...
+        r0, n = (0, 256) if rank == 0 else (256, 768)
+        try:
+            S._check_slabs(comm, r0, n, None, None)
+            out.append("unequal accepted")
+        except ValueError:
+            out.append("unequal refused")
+        # ... accepted with the peer transport (global indices)
+        S._check_slabs(comm, r0, n, None, object())
+        out.append("peer ok")
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allgather_transport_refuses_unequal_slabs():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_slab_check_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for _, out in res:
+        assert out == ["equal ok", "unequal refused", "peer ok"], out
