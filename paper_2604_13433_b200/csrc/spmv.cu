@@ -285,6 +285,26 @@ static unsigned pair_persist_grid(long long n_slices, bool dot) {
   return (unsigned)(full < cap ? full : cap);
 }
 
+// narrow kernel for slices of <= 12 steps (PSELL_NARROW=0: the persistent pair kernel, A/B)
+// and its resident CTAs per SM (PSELL_NARROW_MINB = 4 | 5: 64 / 48 registers)
+static bool narrow_on() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_NARROW", v)) return v != 0;
+  return true;
+}
+static int narrow_minb() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_NARROW_MINB", v) && (v == 4 || v == 5)) return v;
+  return 4;
+}
+static unsigned narrow_grid(long long n_slices) {
+  const long long full = ceil_div(ceil_div(n_slices, 2), kWarpsPerCta);
+  const long long cap = (long long)sm_count() * narrow_minb();
+  return (unsigned)(full < cap ? full : cap);
+}
+
 // pair kernel for wide slices too (PSELL_PAIR_WIDE=1, A/B; default: dual kernel)
 static bool pair_wide() {
   static EnvCache c;
@@ -911,6 +931,210 @@ __global__ void __launch_bounds__(NT, PSELL_PAIR_MINB * kBlock / NT) spmv_pair_k
     if (!PERSIST) break;
   }
   finish_dot<DOT, NT>(a, dotv);
+}
+
+// ---- narrow kernel (C == 32, every slice <= 12 steps, no segmentation: 7-point rows,
+// the PCG inner operator).  The pair kernel's slice pairing and FMA order (outputs are
+// bitwise equal to it), with the per-pair bookkeeping cut to what such slices need
+// (71.7 M instead of 94.6 M warp instructions on 7-point 256^3 e8m14, ncu) and the
+// memory round trips of a pair taken off its critical path:
+//  * the next pair's offsets and perm bytes load while this pair runs (software
+//    pipelined, no select on a loaded value: a select on the prefetched offset stalled
+//    on it and made the prefetch synchronous -- 12 % of the stall samples, 145.5 -> 137.3 us);
+//  * decode runs in two passes (cursor prefix and gathers, then the FMAs), so ptxas
+//    issues the gathers of a pair in ~3 batches instead of one per few words;
+//  * the p_own load of the fused dot issues between the gather and FMA passes;
+//  * perm width, mode and the tail split are compile-time; offsets in 32-bit arithmetic.
+// Steps [0, K) are decoded for every pair, [K, 12) only when a slice reaches them.
+// 4 CTAs x 8 warps per SM (64 registers, no spills; PSELL_NARROW_MINB=5: 48 registers).
+// Measured and dropped (profiles/r02/narrow_ab*.txt): the next pair's words in registers
+// (3 CTAs/SM, 140.2 us, fused dot 159.7 us), a bulk L2 prefetch of the next pair
+// (147.9 us), a __syncwarp fence forcing every gather before the first FMA (ptxas then
+// parks the flag predicates in a register: 144.2 us), a 64-bit byte-pointer cursor
+// (ptxas splits the mad.wide into LEA + LEA.HI.X: 168.8 us), 6 CTAs/SM (spills).
+#ifndef PSELL_NARROW_K
+#define PSELL_NARROW_K 9
+#endif
+
+// cursor step (c2 = 2 * column), the flag test fused into the AND (LOP3 with a predicate
+// output): the C form of this loses the fusion once the flag is tested again in the FMA pass
+__device__ __forceinline__ void narrow_cursor(uint32_t w, uint32_t& c2, uint32_t m_real) {
+  asm("{\n .reg .pred p;\n .reg .b32 t, m;\n and.b32 t, %1, 1;\n setp.ne.b32 p, t, 0;\n"
+      " selp.b32 m, %2, 0xFFFFFFFE, p;\n and.b32 t, %1, m;\n add.u32 %0, %0, t;\n}"
+      : "+r"(c2) : "r"(w), "r"(m_real));
+}
+template <int CODEC, typename XT> struct NarrowStep;
+template <> struct NarrowStep<PSELL_E8MY, float> {
+  __device__ static uint32_t gather(uint32_t w, uint32_t& c2, const float* x, uint32_t m_real) {
+    narrow_cursor(w, c2, m_real);
+    return __float_as_uint(__ldg(reinterpret_cast<const float*>(xbyte(x, c2))));
+  }
+  __device__ static void fma(uint32_t w, uint32_t xr, float& acc, uint32_t vmask) {
+    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
+        : "+f"(acc) : "r"(w & 1u), "f"(__uint_as_float(w & vmask)), "f"(__uint_as_float(xr)));
+  }
+};
+template <> struct NarrowStep<PSELL_E8MY, __half> {
+  __device__ static uint32_t gather(uint32_t w, uint32_t& c2, const __half* x, uint32_t m_real) {
+    narrow_cursor(w, c2, m_real);
+    return (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(xbyte(x, c2)));
+  }
+  __device__ static void fma(uint32_t w, uint32_t xr, float& acc, uint32_t vmask) {
+    const float xv = __half2float(__ushort_as_half((unsigned short)xr));
+    asm("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p fma.rn.f32 %0, %2, %3, %0;\n}"
+        : "+f"(acc) : "r"(w & 1u), "f"(__uint_as_float(w & vmask)), "f"(xv));
+  }
+};
+template <> struct NarrowStep<PSELL_FP16, __half> {
+  __device__ static uint32_t gather(uint32_t w, uint32_t& c2, const __half* x, uint32_t) {
+    narrow_cursor(w, c2, 0xFFFEu);
+    return (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(xbyte(x, c2)));
+  }
+  __device__ static void fma(uint32_t w, uint32_t xr, float& acc, uint32_t) {
+    asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
+        " @p fma.rn.f32.f16 %0, hi, %3, %0;\n}" : "+f"(acc) : "r"(w & 1u), "r"(w), "h"((unsigned short)xr));
+  }
+};
+template <> struct NarrowStep<PSELL_FP16, float> {
+  __device__ static uint32_t gather(uint32_t w, uint32_t& c2, const float* x, uint32_t) {
+    narrow_cursor(w, c2, 0xFFFEu);
+    return __float_as_uint(__ldg(reinterpret_cast<const float*>(xbyte(x, c2))));
+  }
+  __device__ static void fma(uint32_t w, uint32_t xr, float& acc, uint32_t) {
+    asm("{\n .reg .pred p;\n .reg .b16 lo, hi;\n .reg .f32 v;\n setp.ne.b32 p, %1, 0;\n mov.b32 {lo, hi}, %2;\n"
+        " cvt.f32.f16 v, hi;\n @p fma.rn.f32 %0, v, %3, %0;\n}"
+        : "+f"(acc) : "r"(w & 1u), "r"(w), "f"(__uint_as_float(xr)));
+  }
+};
+
+template <int CODEC, typename XT, bool DOT, int PB, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) spmv_narrow_kernel(const SpmvArgs a) {
+  using S = NarrowStep<CODEC, XT>;
+  constexpr int U = 12, K = PSELL_NARROW_K;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t ns = (uint32_t)a.n_slices, np = (ns + 1u) >> 1;
+  const uint32_t n_rows = (uint32_t)a.n_rows;
+  const uint32_t wstride = gridDim.x * (unsigned)kWarpsPerCta;
+  const XT* __restrict__ x = static_cast<const XT*>(a.x);
+  const uint32_t* __restrict__ pack = static_cast<const uint32_t*>(a.pack);
+  const int64_t* __restrict__ off = a.offset;
+  const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+  const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+  const uint32_t kl = (uint32_t)a.k_left, row0 = (uint32_t)a.row0, se = (uint32_t)a.se;
+  const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+  auto perm_of = [&](uint32_t s) -> uint32_t {
+    const uint32_t sc = s < n_rows ? s : n_rows - 1u;  // rows past n_rows are never stored
+    if constexpr (PB == 1) return (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc);
+    else return (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
+  };
+  double dotv = 0.0;
+  uint32_t wg = (blockIdx.x * (unsigned)kBlock + threadIdx.x) >> 5;
+  // pipelined per-pair metadata: offsets (o0 64-bit, o1 / o2 low words) and perm bytes
+  long long n_o0 = 0;
+  uint32_t n_o1 = 0u, n_o2 = 0u, n_ppA = 0u, n_ppB = 0u;
+  auto fetch = [&](uint32_t g) {
+    if (g < np) {
+      const uint32_t k = 2u * g;
+      // no select on a loaded value: a lone last slice reads off[ns] == off[k + 1]
+      // (the select waited for the load, which made this prefetch synchronous)
+      n_o0 = __ldg(off + k);
+      n_o1 = (uint32_t)__ldg(off + k + 1);
+      n_o2 = (uint32_t)__ldg(off + (k + 2u < ns ? k + 2u : ns));
+      if constexpr (PB != 0) {
+        n_ppA = perm_of(k * 32u + lane);
+        n_ppB = perm_of(k * 32u + 32u + lane);
+      }
+    }
+  };
+  fetch(wg);
+  for (; wg < np; wg += wstride) {
+    const uint32_t kA = 2u * wg;
+    const bool hasB = kA + 1u < ns;
+    const long long o0 = n_o0;
+    const uint32_t wA = (n_o1 - (uint32_t)o0) >> 5, wB = (n_o2 - n_o1) >> 5;
+    const uint32_t ppA = n_ppA, ppB = n_ppB;
+    fetch(wg + wstride);
+    const uint32_t* pA = pack + o0 + lane;
+    const uint32_t* pB = pA + wA * 32u;
+    auto base2 = [&](uint32_t k) -> uint32_t {
+      const uint32_t g = row0 + k * 32u + lane;
+      const uint32_t blk = se == 1u ? g : fast_div(g, a.se_m, a.se_l) * se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    uint32_t cA = base2(kA), cB = base2(kA + 1u);
+    uint32_t wa[U], wb[U], xa[U], xb[U];
+    if (wA >= (uint32_t)K && wB >= (uint32_t)K) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        wa[u] = __ldcs(pA + u * 32);
+        wb[u] = __ldcs(pB + u * 32);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        wa[u] = (uint32_t)u < wA ? __ldcs(pA + u * 32) : 0u;
+        wb[u] = (uint32_t)u < wB ? __ldcs(pB + u * 32) : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      xa[u] = S::gather(wa[u], cA, x, m_real);
+      xb[u] = S::gather(wb[u], cB, x, m_real);
+    }
+    const uint32_t sA = kA * 32u + lane, sB = sA + 32u;
+    uint32_t oA = sA, oB = sB;
+    if constexpr (PB != 0) {
+      oA = fast_div(kA * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppA;
+      oB = fast_div(kA * 32u + 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppB;
+    }
+    const bool stA = sA < n_rows, stB = hasB && sB < n_rows;
+    float pvA = 0.f, pvB = 0.f;
+    if constexpr (DOT) {  // in flight under the FMA pass
+      if (stA) pvA = __ldg(a.p_own + oA);
+      if (stB) pvB = __ldg(a.p_own + oB);
+    }
+    float accA = 0.f, accB = 0.f;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      S::fma(wa[u], xa[u], accA, vmask);
+      S::fma(wb[u], xb[u], accB, vmask);
+    }
+    // steps [K, 12): rare (boundary slices), after the main pass so they hold no
+    // registers across it
+    if (wA > (uint32_t)K || wB > (uint32_t)K) {
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        wa[u] = (uint32_t)u < wA ? __ldcs(pA + u * 32) : 0u;
+        wb[u] = (uint32_t)u < wB ? __ldcs(pB + u * 32) : 0u;
+      }
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        xa[u] = S::gather(wa[u], cA, x, m_real);
+        xb[u] = S::gather(wb[u], cB, x, m_real);
+      }
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        S::fma(wa[u], xa[u], accA, vmask);
+        S::fma(wb[u], xb[u], accB, vmask);
+      }
+    }
+    auto flush = [&](bool st, uint32_t o, float acc, float pv) {
+      if (st) {
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)pv * (double)to_f<XT>(yv);
+      }
+    };
+    flush(stA, oA, accA, pvA);
+    flush(stB, oB, accB, pvB);
+  }
+  finish_dot<DOT>(a, dotv);
 }
 
 // ---- long slices (power-law rows): segments of seg_len steps per warp.
@@ -1644,6 +1868,22 @@ __global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const SpmvArgs a) 
   finish_dot<DOT>(a, dotv);
 }
 
+template <int CODEC, typename XT, bool DOT, int PB>
+static void launch_narrow_pb(const SpmvArgs& a, cudaStream_t st) {
+  const unsigned g = narrow_grid(a.n_slices);
+  switch (narrow_minb()) {
+    case 5: spmv_narrow_kernel<CODEC, XT, DOT, PB, 5><<<g, kBlock, 0, st>>>(a); break;
+    default: spmv_narrow_kernel<CODEC, XT, DOT, PB, 4><<<g, kBlock, 0, st>>>(a); break;
+  }
+}
+template <int CODEC, typename XT, bool DOT>
+static void launch_narrow(const SpmvArgs& a, cudaStream_t st) {
+  if constexpr (CODEC == PSELL_FP32EMBED) return;
+  else if (a.mode != PSELL_MODE_IMPLICIT) launch_narrow_pb<CODEC, XT, DOT, 0>(a, st);
+  else if (a.perm_bytes == 1) launch_narrow_pb<CODEC, XT, DOT, 1>(a, st);
+  else launch_narrow_pb<CODEC, XT, DOT, 2>(a, st);
+}
+
 template <int CODEC, typename XT, bool REF, bool DOT, bool GR = false>
 static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
   if (a.c == 32) {
@@ -1659,6 +1899,8 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
           const int du = dual_chunk(a.narrow);
           if (a.narrow && tile_kernel()) {
             launch_tile<CODEC, XT, DOT>(a, st);
+          } else if (a.narrow12 && a.seg_len == 0 && narrow_on()) {
+            launch_narrow<CODEC, XT, DOT>(a, st);
           } else if (dual_slices(a.n_slices) && a.narrow && pair_kernel()) {
             const int pn = pair_nt(DOT);
             const unsigned gp = (unsigned)ceil_div(ceil_div(a.n_slices, 2), pn / 32);
@@ -1903,6 +2145,8 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   if (flags & PSELL_SPMV_TMA_STREAM) return "spmv_stream_kernel";
   const long long ns = ceil_div(d->n_rows, d->c);
   if ((flags & PSELL_SPMV_NARROW) && tile_kernel()) return "spmv_tile_kernel (TMA ring)";
+  if ((flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_NARROW12) && narrow_on())
+    return "spmv_narrow_kernel (pipelined pair metadata, two-pass decode, persistent)";
   if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel())
     return pair_persist_grid(ns, false) ? (slot_kernel() && (flags & PSELL_SPMV_NARROW12)
                                                ? "spmv_slot_kernel (TMA slot per warp, persistent)"
@@ -2021,6 +2265,8 @@ int64_t psell_spmv_dot_partials(const psell_desc* d, int32_t flags) {
       const long long cap = (long long)sm_count() * kTileCtasPerSm;
       return n_tiles < cap ? n_tiles : cap;
     }
+    if (d->codec != PSELL_FP32EMBED && (flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_NARROW12) && narrow_on())
+      return narrow_grid(ns);
     if (d->codec != PSELL_FP32EMBED && dual_slices(ns) && pair_kernel() && (flags & PSELL_SPMV_NARROW)) {
       if (const unsigned g = pair_persist_grid(ns, true)) return g;
       return ceil_div(ceil_div(ns, 2), pair_nt(true) / 32);

@@ -389,7 +389,7 @@ def test_tile_tma_kernel_equals_pair_kernel(monkeypatch, kind, nx):
         lib.psell_reload_env()  # the launchers cache their knobs
         from paper_2604_13433_b200 import _dev
         assert lib.psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode().startswith(
-            "spmv_tile" if tile == "1" else "spmv_pair")
+            "spmv_tile" if tile == "1" else ("spmv_pair", "spmv_narrow"))
         y = P.packsell_spmv(M, x)
         npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
         part = torch.zeros(npart, dtype=torch.float64, device="cuda")
@@ -501,3 +501,62 @@ def test_powerlaw_far_build_and_spmv_vs_oracle(sigma):
     anorm = np.bincount(np.repeat(np.arange(A.n_rows), A.row_lengths()), aq, minlength=A.n_rows).max()
     err = np.abs(ys["0"].astype(np.float64) - ref).max() / (anorm * np.abs(x.astype(np.float64)).max())
     assert err <= 2.0 ** -11 + 2 * lmax * 2.0 ** -24, err
+
+
+def _narrow_csr(rng, n, lmin, lmax, spread):
+    lens = rng.integers(lmin, lmax + 1, n)
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.clip(rows + rng.integers(-spread, spread + 1, rows.size), 0, n - 1)
+    order = np.lexsort((cols, rows))
+    r, c = rows[order], cols[order]
+    keep = np.ones(r.size, bool)
+    keep[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+    r, c = r[keep], c[keep]
+    v = rng.uniform(0.01, 1, r.size) * rng.choice([-1.0, 1.0], r.size)
+    rp = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n))]).astype(np.int64)
+    return P.CsrMatrix(n, n, rp, c.astype(np.int32), v)
+
+
+@pytest.mark.parametrize("matrix", ["poisson3d-37", "ragged-narrow"])
+@pytest.mark.parametrize("sigma,mode", [(256, "implicit"), (512, "implicit"), (256, "explicit"), (1, "none")])
+def test_narrow_kernel_equals_pair_kernel(monkeypatch, rng, matrix, sigma, mode):
+    """The narrow kernel (default for slices <= 12 steps) gives the persistent pair kernel's
+    bits (same FMAs in the same order): plain SpMV for every codec / x dtype it serves and the
+    fused SpMV + p.q, with u8 / u16 / no perm, tail steps past 9 and a ragged last slice pair."""
+    import torch
+    from paper_2604_13433_b200 import _dev, _lib
+    if matrix == "poisson3d-37":
+        A = P.sym_diag_scale(P.poisson3d(37))                 # 50653 rows: odd slice count, ragged last slice
+    else:
+        A = _narrow_csr(rng, 200_003, 3, 11, 100)             # widths up to 12: the [9, 12) tail path
+    lib = _lib.lib()
+    for pre, dt in (("e8m14", torch.float32), ("fp16", torch.float16), ("fp16", torch.float32),
+                    ("e8m14", torch.float16)):
+        M = P.build_packsell(A, 32, sigma, P.parse_format(pre), mode)
+        assert M.spmv_flags() & 12 == 12, "expected narrow slices of <= 12 steps"
+        x = (torch.rand(M.n_cols, device="cuda") * 2 - 1).to(dt)
+        res = {}
+        for nar in ("0", "1"):
+            monkeypatch.setenv("PSELL_NARROW", nar)
+            lib.psell_reload_env()
+            name = lib.psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
+            assert name.startswith("spmv_narrow" if nar == "1" else "spmv_pair"), name
+            y = P.packsell_spmv(M, x)
+            out = [y.clone()]
+            if dt == torch.float32:
+                npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
+                part = torch.zeros(npart, dtype=torch.float64, device="cuda")
+                q = torch.empty_like(x)
+                err = _lib.PsellError()
+                rc = lib.psell_spmv_dot(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                                        x.data_ptr(), q.data_ptr(), x.data_ptr(), part.data_ptr(), None,
+                                        M.spmv_flags(), _lib.stream_handle(), err)
+                _lib.check(rc, err)
+                out += [q.clone(), float(part.sum())]
+            res[nar] = out
+        monkeypatch.delenv("PSELL_NARROW")
+        lib.psell_reload_env()
+        assert torch.equal(res["0"][0], res["1"][0]), (matrix, pre, dt)
+        if dt == torch.float32:
+            assert torch.equal(res["0"][1], res["1"][1]), (matrix, pre)
+            assert res["1"][2] == pytest.approx(res["0"][2], rel=1e-12)
