@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kBlock) ipcg_direction_x_kernel(long long n, f
                                                                   const float* __restrict__ z,
                                                                   float* __restrict__ x,
                                                                   const double* __restrict__ scal,
-                                                                  const int32_t* __restrict__ iflags) {
+                                                                  const int32_t* __restrict__ iflags,
+                                                                  bool rev = false) {
   if (iflags[0]) return;
   const float al = __double2float_rn(scal[2]);
   const float b = __double2float_rn(scal[3]);
@@ -142,7 +143,8 @@ __global__ void __launch_bounds__(kBlock) ipcg_direction_x_kernel(long long n, f
                      reinterpret_cast<uintptr_t>(x)) & 15) == 0;
   if (vec) {
     const long long n4 = n >> 2;
-    for (long long i4 = gt; i4 < n4; i4 += gs) {
+    for (long long k4 = gt; k4 < n4; k4 += gs) {
+      const long long i4 = rev ? n4 - 1 - k4 : k4;  // rev: descending rows (see ipcg_update_kernel)
       float4 pv = reinterpret_cast<float4*>(p)[i4];
       float4 xv = reinterpret_cast<float4*>(x)[i4];
       const float4 zv = reinterpret_cast<const float4*>(z)[i4];
@@ -172,7 +174,8 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
                                                              const float* __restrict__ q,
                                                              const float* __restrict__ inv,
                                                              double* scal, int32_t* iflags,
-                                                             double* __restrict__ parts, unsigned* ticket) {
+                                                             double* __restrict__ parts, unsigned* ticket,
+                                                             bool rev = false) {
   if (iflags[0]) return;
   __shared__ double sh[kBlock / 32];
   const float a = __double2float_rn(scal[2]);
@@ -182,8 +185,12 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
   long long done = 0;
   if (VEC) {
     const long long n4 = n >> 2;
+    // rev: rows in descending order (the SpMV before this pass wrote q ascending, so the
+    // most recently written -- still L2-resident -- part of q is read first)
+    auto at = [&](long long i4) { return rev ? n4 - 1 - i4 : i4; };
     auto step = [&](long long i4, float4 rv, const float4 qv) {
       float4 zv;
+      i4 = at(i4);
       const long long i = i4 * 4;
       if (x) {
         float4 xv = reinterpret_cast<float4*>(x)[i4];
@@ -211,15 +218,15 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
     // per-thread order of the dot sum as one element per trip)
 #ifndef PSELL_UPD_U1
     for (; i4 + gs < n4; i4 += 2 * gs) {
-      const float4 r0 = reinterpret_cast<float4*>(r)[i4];
-      const float4 q0 = reinterpret_cast<const float4*>(q)[i4];
-      const float4 r1 = reinterpret_cast<float4*>(r)[i4 + gs];
-      const float4 q1 = reinterpret_cast<const float4*>(q)[i4 + gs];
+      const float4 r0 = reinterpret_cast<float4*>(r)[at(i4)];
+      const float4 q0 = reinterpret_cast<const float4*>(q)[at(i4)];
+      const float4 r1 = reinterpret_cast<float4*>(r)[at(i4 + gs)];
+      const float4 q1 = reinterpret_cast<const float4*>(q)[at(i4 + gs)];
       step(i4, r0, q0);
       step(i4 + gs, r1, q1);
     }
 #endif
-    for (; i4 < n4; i4 += gs) step(i4, reinterpret_cast<float4*>(r)[i4], reinterpret_cast<const float4*>(q)[i4]);
+    for (; i4 < n4; i4 += gs) step(i4, reinterpret_cast<float4*>(r)[at(i4)], reinterpret_cast<const float4*>(q)[at(i4)]);
     done = n4 * 4;
   }
   for (long long i = done + gt; i < n; i += gs) {
@@ -462,6 +469,21 @@ __global__ void sum_strided_kernel(const double* parts, int np, int stride, int 
   out[j] = s;
 }
 
+// traversal order of the inner PCG's vector passes (A/B knobs, read once per process):
+// PSELL_UPD_REV / PSELL_DIR_REV = 1 walk the update / direction pass in descending rows
+static bool env_flag(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e ? atoi(e) : dflt) != 0;
+}
+static bool upd_rev() {
+  static const bool v = env_flag("PSELL_UPD_REV", 0);
+  return v;
+}
+static bool dir_rev() {
+  static const bool v = env_flag("PSELL_DIR_REV", 1);
+  return v;
+}
+
 static unsigned vgrid(long long n) {
   long long g = ceil_div(n, kBlock);
   if (g > kRB) g = kRB;
@@ -533,7 +555,7 @@ int psell_ipcg_update(int64_t n, float* x, float* r, float* z, const float* p, c
                      reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
   double* sc = const_cast<double*>(scal);
   int32_t* fl = const_cast<int32_t*>(iflags);
-  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, sc, fl, partials, nullptr);
+  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, sc, fl, partials, nullptr, upd_rev());
   else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, sc, fl, partials, nullptr);
   finalize(partials, kRB, 1, local_out, iflags, st);
   return LAUNCH_OK();
@@ -546,7 +568,7 @@ int psell_ipcg_update_beta(int64_t n, float* x, float* r, float* z, const float*
   cudaStream_t st = as_stream(stream);
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(z) |
                      reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
-  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket);
+  if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket, upd_rev());
   else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket);
   return LAUNCH_OK();
 }
@@ -564,7 +586,7 @@ int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal
 
 int psell_ipcg_direction_x(int64_t n, float* p, const float* z, float* x, const double* scal,
                            const int32_t* iflags, void* stream) {
-  ipcg_direction_x_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, x, scal, iflags);
+  ipcg_direction_x_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, x, scal, iflags, dir_rev());
   return LAUNCH_OK();
 }
 

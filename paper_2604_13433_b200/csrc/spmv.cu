@@ -299,9 +299,10 @@ static int narrow_minb() {
   if (env_int(c, "PSELL_NARROW_MINB", v) && (v == 4 || v == 5)) return v;
   return 4;
 }
+static bool narrow_tma();
 static unsigned narrow_grid(long long n_slices) {
   const long long full = ceil_div(ceil_div(n_slices, 2), kWarpsPerCta);
-  const long long cap = (long long)sm_count() * narrow_minb();
+  const long long cap = (long long)sm_count() * (narrow_tma() ? 4 : narrow_minb());
   return (unsigned)(full < cap ? full : cap);
 }
 
@@ -1641,6 +1642,7 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int CODEC, typename XT, bool DOT>
 __global__ void __launch_bounds__(kBlock, kSlotCtasPerSm) spmv_slot_kernel(const SpmvArgs a) {
@@ -1765,11 +1767,214 @@ __global__ void __launch_bounds__(kBlock, kSlotCtasPerSm) spmv_slot_kernel(const
   finish_dot<DOT>(a, dotv);
 }
 
+// ---- narrow TMA kernel (PSELL_NARROW_TMA=1): the narrow kernel with each warp's
+// slice-pair words staged through two shared-memory slots by cp.async.bulk (one bulk copy
+// per pair, issued by lane 0 about one pair ahead), so a pair's words are resident when the
+// warp reaches it instead of costing an HBM round trip per pair (29 % of the narrow
+// kernel's stall samples wait on its first word).  The offsets of the pairs ahead travel
+// through a 4-entry shared ring by cp.async (a register rotation of prefetched offsets
+// waits on the loads).  Same decode, FMAs and order as the narrow kernel.  (Per-lane
+// 16-byte cp.async.cg staging instead of the bulk copy: 130.5 us, fused dot 162 us.)
+constexpr int kNtSlotWords = 24 * 32;  // a pair of slices of <= 12 steps
+struct NtMeta {
+  long long off[4][4];  // ring of {o0, o1, o2, pad} for the pairs ahead
+};
+constexpr size_t kNtSmemBytes = kWarpsPerCta * (2 * kNtSlotWords * 4 + 2 * 8 + sizeof(NtMeta));
+template <int CODEC, typename XT, bool DOT, int PB>
+__global__ void __launch_bounds__(kBlock, 4) spmv_narrow_tma_kernel(const SpmvArgs a) {
+  using S = NarrowStep<CODEC, XT>;
+  constexpr int U = 12, K = PSELL_NARROW_K;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  extern __shared__ __align__(128) unsigned char nt_smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint32_t* slots = reinterpret_cast<uint32_t*>(nt_smem) + warp * 2 * kNtSlotWords;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(nt_smem + kWarpsPerCta * 2 * kNtSlotWords * 4) + warp * 2;
+  NtMeta* meta = reinterpret_cast<NtMeta*>(nt_smem + kWarpsPerCta * (2 * kNtSlotWords * 4 + 16)) + warp;
+  const uint32_t ns = (uint32_t)a.n_slices, np = (ns + 1u) >> 1;
+  const uint32_t n_rows = (uint32_t)a.n_rows;
+  const uint32_t ws = gridDim.x * (unsigned)kWarpsPerCta;
+  const XT* __restrict__ x = static_cast<const XT*>(a.x);
+  const uint32_t* __restrict__ pack = static_cast<const uint32_t*>(a.pack);
+  const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+  const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+  const uint32_t kl = (uint32_t)a.k_left, row0 = (uint32_t)a.row0, se = (uint32_t)a.se;
+  const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+  auto perm_of = [&](uint32_t s) -> uint32_t {
+    const uint32_t sc = s < n_rows ? s : n_rows - 1u;
+    if constexpr (PB == 1) return (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc);
+    else return (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
+  };
+  // lanes 0..2: the offset triple of pair g into ring entry r (async; one commit group per call)
+  auto request = [&](uint32_t g, uint32_t r) {
+    if (lane < 3u && g < np) {
+      const uint32_t k = 2u * g + lane;
+      cp_async8(&meta->off[r][lane], a.offset + (k <= ns ? k : ns));
+    }
+    cp_async_commit();
+  };
+  // the whole warp: the bulk copy of the pair in ring entry r into slot sl, issued by one
+  // elected lane (operands warp-uniform: no divergent lane-0 path for ptxas to serialise);
+  // an empty pair just arrives on the barrier
+  auto issue = [&](uint32_t sl, uint32_t r) {
+    const long long o0 = meta->off[r][0], o2 = meta->off[r][2];
+    const uint32_t bytes = (uint32_t)(o2 - o0) * 4u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile(
+        "{\n .reg .pred e, z;\n elect.sync _|e, 0xffffffff;\n setp.eq.u32 z, %2, 0;\n"
+        " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n"
+        " @!z and.pred e, e, !z;\n"
+        " @e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%3], %2, [%1], %4;\n}"
+        ::"r"(smem_u32(slots + sl * kNtSlotWords)), "r"(smem_u32(bars + sl)), "r"(bytes), "l"(pack + o0),
+        "l"(policy_evict_first())
+        : "memory");
+  };
+  uint32_t wg = blockIdx.x * (unsigned)kWarpsPerCta + warp;
+  if (lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  request(wg, 0);
+  request(wg + ws, 1);
+  request(wg + 2u * ws, 2);
+  cp_async_wait_all();
+  __syncwarp();
+  if (wg < np) issue(0, 0);
+  if (wg + ws < np) issue(1, 1);
+  uint32_t n_ppA = 0u, n_ppB = 0u;
+  if constexpr (PB != 0) {
+    n_ppA = perm_of(2u * wg * 32u + lane);
+    n_ppB = perm_of(2u * wg * 32u + 32u + lane);
+  }
+  double dotv = 0.0;
+  for (uint32_t it = 0; wg < np; wg += ws, ++it) {
+    const uint32_t sl = it & 1u, r = it & 3u;
+    request(wg + 3u * ws, (it + 3u) & 3u);
+    const uint32_t* slot = slots + sl * kNtSlotWords;
+    const uint32_t kA = 2u * wg;
+    const bool hasB = kA + 1u < ns;
+    const uint32_t q0 = (uint32_t)meta->off[r][0], q1 = (uint32_t)meta->off[r][1], q2 = (uint32_t)meta->off[r][2];
+    const uint32_t wA = (q1 - q0) >> 5, wB = (q2 - q1) >> 5;
+    const uint32_t ppA = n_ppA, ppB = n_ppB;
+    if constexpr (PB != 0) {
+      if (wg + ws < np) {
+        n_ppA = perm_of(2u * (wg + ws) * 32u + lane);
+        n_ppB = perm_of(2u * (wg + ws) * 32u + 32u + lane);
+      }
+    }
+    auto base2 = [&](uint32_t k) -> uint32_t {
+      const uint32_t g = row0 + k * 32u + lane;
+      const uint32_t blk = se == 1u ? g : fast_div(g, a.se_m, a.se_l) * se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    uint32_t cA = base2(kA), cB = base2(kA + 1u);
+    mbar_wait(bars + sl, (it >> 1) & 1u);
+    const uint32_t* sA = slot + lane;
+    const uint32_t* sB = sA + wA * 32u;
+    uint32_t wa[U], wb[U], xa[U], xb[U];
+    if (wA >= (uint32_t)K && wB >= (uint32_t)K) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        wa[u] = sA[u * 32];
+        wb[u] = sB[u * 32];
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        wa[u] = (uint32_t)u < wA ? sA[u * 32] : 0u;
+        wb[u] = (uint32_t)u < wB ? sB[u * 32] : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      xa[u] = S::gather(wa[u], cA, x, m_real);
+      xb[u] = S::gather(wb[u], cB, x, m_real);
+    }
+    const uint32_t rA = kA * 32u + lane, rB = rA + 32u;
+    uint32_t oA = rA, oB = rB;
+    if constexpr (PB != 0) {
+      oA = fast_div(kA * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppA;
+      oB = fast_div(kA * 32u + 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppB;
+    }
+    const bool stA = rA < n_rows, stB = hasB && rB < n_rows;
+    float pvA = 0.f, pvB = 0.f;
+    if constexpr (DOT) {  // unpredicated: rows past n_rows read a valid row, their product is dropped
+      pvA = __ldg(a.p_own + (oA < n_rows ? oA : n_rows - 1u));
+      pvB = __ldg(a.p_own + (oB < n_rows ? oB : n_rows - 1u));
+    }
+    float accA = 0.f, accB = 0.f;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      S::fma(wa[u], xa[u], accA, vmask);
+      S::fma(wb[u], xb[u], accB, vmask);
+    }
+    if (wA > (uint32_t)K || wB > (uint32_t)K) {
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        wa[u] = (uint32_t)u < wA ? sA[u * 32] : 0u;
+        wb[u] = (uint32_t)u < wB ? sB[u * 32] : 0u;
+      }
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        xa[u] = S::gather(wa[u], cA, x, m_real);
+        xb[u] = S::gather(wb[u], cB, x, m_real);
+      }
+#pragma unroll
+      for (int u = K; u < U; ++u) {
+        S::fma(wa[u], xa[u], accA, vmask);
+        S::fma(wb[u], xb[u], accB, vmask);
+      }
+    }
+    // every lane has read the slot and the offsets of pair +2 (requested two pairs ago)
+    // have landed: refill the slot with that pair
+    cp_async_wait_group1();
+    __syncwarp();
+    if (wg + 2u * ws < np) issue(sl, (it + 2u) & 3u);
+    auto flush = [&](bool st, uint32_t o, float acc, float pv) {
+      if (st) {
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)pv * (double)to_f<XT>(yv);
+      }
+    };
+    flush(stA, oA, accA, pvA);
+    flush(stB, oB, accB, pvB);
+  }
+  cp_async_wait_all();
+  finish_dot<DOT>(a, dotv);
+}
+
+// word staging of the narrow kernel (PSELL_NARROW_TMA=0: words loaded per lane from global
+// memory, A/B).  7-point 256^3 e8m14 / f32 x: 124.9 vs 137.3 us; fp16 / f16 x 116.1 vs
+// 128.9 us; fused p.q 134.5 vs 139.5 us (profiles/r02/narrow_tma_ab.txt)
+static bool narrow_tma() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_NARROW_TMA", v)) return v != 0;
+  return true;
+}
+
 // slot kernel for narrow slices instead of the persistent pair kernel (PSELL_SLOT=1: on, A/B).
 // Off by default: 7-point 256^3 e8m14 / f32 x 156-160 us at 6 CTAs/SM (40 registers,
 // 52-92 B of spills; ncu: long-scoreboard stalls per issue 13.4 -> 9.7, eligible warps
 // 1.5 -> 2.0, but 21 % more instructions) and 147 us at 5 CTAs/SM (48 registers, no
 // spills in the plain kernel) against the pair kernel's 146 us (scripts/slot_ab.py).
+template <int CODEC, typename XT, bool DOT, int PB>
+static void launch_narrow_tma(const SpmvArgs& a, cudaStream_t st, unsigned g) {
+  static bool attr = false;  // idempotent attribute, benign race
+  if (!attr) {
+    cudaFuncSetAttribute(spmv_narrow_tma_kernel<CODEC, XT, DOT, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kNtSmemBytes);
+    attr = true;
+  }
+  spmv_narrow_tma_kernel<CODEC, XT, DOT, PB><<<g, kBlock, kNtSmemBytes, st>>>(a);
+}
+
 static bool slot_kernel() {
   static EnvCache c;
   int v;
@@ -1869,8 +2074,14 @@ __global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const SpmvArgs a) 
 }
 
 template <int CODEC, typename XT, bool DOT, int PB>
+static void launch_narrow_tma(const SpmvArgs& a, cudaStream_t st, unsigned g);
+template <int CODEC, typename XT, bool DOT, int PB>
 static void launch_narrow_pb(const SpmvArgs& a, cudaStream_t st) {
   const unsigned g = narrow_grid(a.n_slices);
+  if (narrow_tma()) {
+    launch_narrow_tma<CODEC, XT, DOT, PB>(a, st, g);
+    return;
+  }
   switch (narrow_minb()) {
     case 5: spmv_narrow_kernel<CODEC, XT, DOT, PB, 5><<<g, kBlock, 0, st>>>(a); break;
     default: spmv_narrow_kernel<CODEC, XT, DOT, PB, 4><<<g, kBlock, 0, st>>>(a); break;
@@ -2146,7 +2357,8 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   const long long ns = ceil_div(d->n_rows, d->c);
   if ((flags & PSELL_SPMV_NARROW) && tile_kernel()) return "spmv_tile_kernel (TMA ring)";
   if ((flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_NARROW12) && narrow_on())
-    return "spmv_narrow_kernel (pipelined pair metadata, two-pass decode, persistent)";
+    return narrow_tma() ? "spmv_narrow_tma_kernel (pair words staged by cp.async.bulk, two-pass decode, persistent)"
+                        : "spmv_narrow_kernel (pipelined pair metadata, two-pass decode, persistent)";
   if (dual_slices(ns) && (flags & PSELL_SPMV_NARROW) && pair_kernel())
     return pair_persist_grid(ns, false) ? (slot_kernel() && (flags & PSELL_SPMV_NARROW12)
                                                ? "spmv_slot_kernel (TMA slot per warp, persistent)"

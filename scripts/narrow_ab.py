@@ -15,7 +15,7 @@ from pair_sweep import timed  # noqa: E402
 
 lib = _lib.lib()
 nx = int(os.environ.get("NX", "256"))
-variants = [tuple(v.split(":")) for v in os.environ.get("VARIANTS", "0:6:0,1:4:0,1:5:0,1:6:0,1:3:1").split(",")]
+variants = os.environ.get("VARIANTS", "PSELL_NARROW=0;PSELL_NARROW=1").split(";")
 cases = [("e8m14", torch.float32), ("fp16", torch.float32), ("fp16", torch.float16)]
 if os.environ.get("QUICK"):
     cases = cases[:1]
@@ -28,16 +28,19 @@ for pre, dt in cases:
     y = torch.empty(M.n_rows, dtype=dt, device="cuda")
     nb = M.spmv_bytes(x.element_size())
     outs, dots = {}, {}
-    for nar, minb, pipe in variants:
-        os.environ["PSELL_NARROW"] = nar
-        os.environ["PSELL_NARROW_MINB"] = minb
-        os.environ["PSELL_NARROW_PIPE"] = pipe
+    knobs = sorted({kv.split("=")[0] for v in variants for kv in v.split(",")})
+    for var in variants:
+        for k in knobs:
+            os.environ.pop(k, None)
+        for kv in var.split(","):
+            k, v = kv.split("=")
+            os.environ[k] = v
         lib.psell_reload_env()
         kname = lib.psell_spmv_kernel_name(M.desc(), 0 if dt == torch.float16 else 1, M.spmv_flags()).decode()
         ms = min(timed(lambda: P.packsell_spmv(M, x, out=y), reps=100) for _ in range(3))
-        key = nar + minb + pipe
+        key = var
         outs[key] = y.clone()
-        line = f"7pt {nx}^3 {pre:6s} {str(dt)[6:]:8s} NARROW={nar} MINB={minb} PIPE={pipe} {kname[:20]:20s} {ms * 1e3:8.1f} us {nb / ms / 1e6:8.1f} GB/s"
+        line = f"7pt {nx}^3 {pre:6s} {str(dt)[6:]:8s} {var:36s} {kname[:20]:20s} {ms * 1e3:8.1f} us {nb / ms / 1e6:8.1f} GB/s"
         if dt == torch.float32:
             npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
             part = torch.zeros(max(npart, 1), dtype=torch.float64, device="cuda")
@@ -51,8 +54,8 @@ for pre, dt in cases:
             dots[key] = (q.clone(), float(part[:npart].sum().item()))
             line += f" | spmv_dot {ms2 * 1e3:8.1f} us"
         print(line, flush=True)
-    for k in ("NARROW_MINB", "NARROW", "NARROW_PIPE"):
-        os.environ.pop("PSELL_" + k)
+    for k in knobs:
+        os.environ.pop(k, None)
     lib.psell_reload_env()
     k0 = next(iter(outs))
     ref = outs[k0]

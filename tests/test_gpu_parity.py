@@ -520,9 +520,11 @@ def _narrow_csr(rng, n, lmin, lmax, spread):
 @pytest.mark.parametrize("matrix", ["poisson3d-37", "ragged-narrow"])
 @pytest.mark.parametrize("sigma,mode", [(256, "implicit"), (512, "implicit"), (256, "explicit"), (1, "none")])
 def test_narrow_kernel_equals_pair_kernel(monkeypatch, rng, matrix, sigma, mode):
-    """The narrow kernel (default for slices <= 12 steps) gives the persistent pair kernel's
-    bits (same FMAs in the same order): plain SpMV for every codec / x dtype it serves and the
-    fused SpMV + p.q, with u8 / u16 / no perm, tail steps past 9 and a ragged last slice pair."""
+    """The narrow kernels (default for slices <= 12 steps: words staged through shared memory
+    by cp.async.bulk; PSELL_NARROW_TMA=0: words loaded per lane) give the persistent pair
+    kernel's bits (same FMAs in the same order): plain SpMV for every codec / x dtype they
+    serve and the fused SpMV + p.q, with u8 / u16 / no perm, tail steps past 9 and a ragged
+    last slice pair."""
     import torch
     from paper_2604_13433_b200 import _dev, _lib
     if matrix == "poisson3d-37":
@@ -530,17 +532,20 @@ def test_narrow_kernel_equals_pair_kernel(monkeypatch, rng, matrix, sigma, mode)
     else:
         A = _narrow_csr(rng, 200_003, 3, 11, 100)             # widths up to 12: the [9, 12) tail path
     lib = _lib.lib()
+    variants = {"pair": ("0", "0", "spmv_pair"), "narrow": ("1", "0", "spmv_narrow_kernel"),
+                "narrow_tma": ("1", "1", "spmv_narrow_tma")}
     for pre, dt in (("e8m14", torch.float32), ("fp16", torch.float16), ("fp16", torch.float32),
                     ("e8m14", torch.float16)):
         M = P.build_packsell(A, 32, sigma, P.parse_format(pre), mode)
         assert M.spmv_flags() & 12 == 12, "expected narrow slices of <= 12 steps"
         x = (torch.rand(M.n_cols, device="cuda") * 2 - 1).to(dt)
         res = {}
-        for nar in ("0", "1"):
+        for key, (nar, tma, kname) in variants.items():
             monkeypatch.setenv("PSELL_NARROW", nar)
+            monkeypatch.setenv("PSELL_NARROW_TMA", tma)
             lib.psell_reload_env()
             name = lib.psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
-            assert name.startswith("spmv_narrow" if nar == "1" else "spmv_pair"), name
+            assert name.startswith(kname), name
             y = P.packsell_spmv(M, x)
             out = [y.clone()]
             if dt == torch.float32:
@@ -553,10 +558,12 @@ def test_narrow_kernel_equals_pair_kernel(monkeypatch, rng, matrix, sigma, mode)
                                         M.spmv_flags(), _lib.stream_handle(), err)
                 _lib.check(rc, err)
                 out += [q.clone(), float(part.sum())]
-            res[nar] = out
+            res[key] = out
         monkeypatch.delenv("PSELL_NARROW")
+        monkeypatch.delenv("PSELL_NARROW_TMA")
         lib.psell_reload_env()
-        assert torch.equal(res["0"][0], res["1"][0]), (matrix, pre, dt)
-        if dt == torch.float32:
-            assert torch.equal(res["0"][1], res["1"][1]), (matrix, pre)
-            assert res["1"][2] == pytest.approx(res["0"][2], rel=1e-12)
+        for key in ("narrow", "narrow_tma"):
+            assert torch.equal(res["pair"][0], res[key][0]), (matrix, pre, dt, key)
+            if dt == torch.float32:
+                assert torch.equal(res["pair"][1], res[key][1]), (matrix, pre, key)
+                assert res[key][2] == pytest.approx(res["pair"][2], rel=1e-12)
