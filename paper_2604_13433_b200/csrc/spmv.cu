@@ -1780,7 +1780,7 @@ struct NtMeta {
   long long off[4][4];  // ring of {o0, o1, o2, pad} for the pairs ahead
 };
 constexpr size_t kNtSmemBytes = kWarpsPerCta * (2 * kNtSlotWords * 4 + 2 * 8 + sizeof(NtMeta));
-template <int CODEC, typename XT, bool DOT, int PB>
+template <int CODEC, typename XT, bool DOT, int PB, bool P2>
 __global__ void __launch_bounds__(kBlock, 4) spmv_narrow_tma_kernel(const SpmvArgs a) {
   using S = NarrowStep<CODEC, XT>;
   constexpr int U = 12, K = PSELL_NARROW_K;
@@ -1866,7 +1866,7 @@ __global__ void __launch_bounds__(kBlock, 4) spmv_narrow_tma_kernel(const SpmvAr
     }
     auto base2 = [&](uint32_t k) -> uint32_t {
       const uint32_t g = row0 + k * 32u + lane;
-      const uint32_t blk = se == 1u ? g : fast_div(g, a.se_m, a.se_l) * se;
+      const uint32_t blk = P2 ? g & ~(se - 1u) : se == 1u ? g : fast_div(g, a.se_m, a.se_l) * se;
       const uint32_t d = blk > kl ? blk - kl : 0u;
       return 2u * (d < cmax ? d : cmax);
     };
@@ -1896,8 +1896,14 @@ __global__ void __launch_bounds__(kBlock, 4) spmv_narrow_tma_kernel(const SpmvAr
     const uint32_t rA = kA * 32u + lane, rB = rA + 32u;
     uint32_t oA = rA, oB = rB;
     if constexpr (PB != 0) {
-      oA = fast_div(kA * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppA;
-      oB = fast_div(kA * 32u + 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppB;
+      if constexpr (P2) {  // power-of-two sigma: block starts by mask
+        const uint32_t sm = ~((uint32_t)a.sigma - 1u);
+        oA = ((kA * 32u) & sm) + ppA;
+        oB = ((kA * 32u + 32u) & sm) + ppB;
+      } else {
+        oA = fast_div(kA * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppA;
+        oB = fast_div(kA * 32u + 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + ppB;
+      }
     }
     const bool stA = rA < n_rows, stB = hasB && rB < n_rows;
     float pvA = 0.f, pvB = 0.f;
@@ -1966,13 +1972,17 @@ static bool narrow_tma() {
 // spills in the plain kernel) against the pair kernel's 146 us (scripts/slot_ab.py).
 template <int CODEC, typename XT, bool DOT, int PB>
 static void launch_narrow_tma(const SpmvArgs& a, cudaStream_t st, unsigned g) {
-  static bool attr = false;  // idempotent attribute, benign race
+  static bool attr = false;  // idempotent attributes, benign race
   if (!attr) {
-    cudaFuncSetAttribute(spmv_narrow_tma_kernel<CODEC, XT, DOT, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(spmv_narrow_tma_kernel<CODEC, XT, DOT, PB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kNtSmemBytes);
+    cudaFuncSetAttribute(spmv_narrow_tma_kernel<CODEC, XT, DOT, PB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kNtSmemBytes);
     attr = true;
   }
-  spmv_narrow_tma_kernel<CODEC, XT, DOT, PB><<<g, kBlock, kNtSmemBytes, st>>>(a);
+  const bool p2 = (a.se & (a.se - 1)) == 0 && (a.sigma & (a.sigma - 1)) == 0;  // power-of-two blocks
+  if (p2) spmv_narrow_tma_kernel<CODEC, XT, DOT, PB, true><<<g, kBlock, kNtSmemBytes, st>>>(a);
+  else spmv_narrow_tma_kernel<CODEC, XT, DOT, PB, false><<<g, kBlock, kNtSmemBytes, st>>>(a);
 }
 
 static bool slot_kernel() {

@@ -518,13 +518,14 @@ def _narrow_csr(rng, n, lmin, lmax, spread):
 
 
 @pytest.mark.parametrize("matrix", ["poisson3d-37", "ragged-narrow"])
-@pytest.mark.parametrize("sigma,mode", [(256, "implicit"), (512, "implicit"), (256, "explicit"), (1, "none")])
+@pytest.mark.parametrize("sigma,mode", [(256, "implicit"), (512, "implicit"), (96, "implicit"), (256, "explicit"),
+                                        (1, "none")])
 def test_narrow_kernel_equals_pair_kernel(monkeypatch, rng, matrix, sigma, mode):
     """The narrow kernels (default for slices <= 12 steps: words staged through shared memory
     by cp.async.bulk; PSELL_NARROW_TMA=0: words loaded per lane) give the persistent pair
     kernel's bits (same FMAs in the same order): plain SpMV for every codec / x dtype they
-    serve and the fused SpMV + p.q, with u8 / u16 / no perm, tail steps past 9 and a ragged
-    last slice pair."""
+    serve and the fused SpMV + p.q, with u8 / u16 / no perm, power-of-two and other sigma, tail
+    steps past 9 and a ragged last slice pair."""
     import torch
     from paper_2604_13433_b200 import _dev, _lib
     if matrix == "poisson3d-37":
