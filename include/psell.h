@@ -318,6 +318,25 @@ PSELL_API int psell_scalar_div(const double* num_parts, const double* den_parts,
                      int32_t stride, double* dst, int32_t* flag, int32_t check_curvature,
                      void* stream);
 
+/* Fused FP64 PCG iteration (identity preconditioner, one GPU; reference solvers.py:183-209,
+ * the loop body of pcg): three launches per iteration instead of eleven.
+ *   psell_csr_spmv_dot_alpha: q = A p (bitwise psell_csr_spmv), pq = p.q, and in the last CTA
+ *     scal[1] = scal[10] = pq, gate[0] = 1 on non-positive / non-finite curvature, else
+ *     scal[0] = alpha = scal[4] / pq.  A no-op when gate[0] != 0.
+ *   psell_pcg_update_status: x += alpha p; r -= alpha q; scal[12] = rr = r.r (fixed order);
+ *     out[3] = psell_pcg_status's {breakdown, pq, sqrt(rr) / bnorm} (gate[0] = 2 below tol);
+ *     scal[2] = beta = rr / scal[4]; scal[4] = rr.
+ *   then psell_xpby_checked(n, p, r, scal + 2, gate): p = r + beta p.
+ * partials >= 2 * PSELL_RED_BLOCKS doubles; ticket: two zeroed regions of
+ * 1 + PSELL_RED_BLOCKS / 32 counters (one per kernel), left zero. */
+PSELL_API int psell_csr_spmv_dot_alpha(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                                       const double* values, const double* x, double* y, const double* p_own,
+                                       double* partials, double* scal, int32_t* gate, unsigned* ticket,
+                                       void* stream, psell_error* err);
+PSELL_API int psell_pcg_update_status(int64_t n, double* x, double* r, const double* p, const double* q,
+                                      double* scal, int32_t* gate, double bnorm, double tol, double* out,
+                                      double* partials, unsigned* ticket, void* stream);
+
 /* FP64 PCG convergence gate (solvers.py:183-207): gate[2] int32 (0 running,
  * 1 breakdown -- pass gate as psell_scalar_div's flag and psell_axpy2's skip
  * flag -- 2 converged; gate[1] = breakdown reported).  out[3] = {breakdown,

@@ -108,6 +108,8 @@ _SIGS = {
     "psell_precond_dot": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P]),
     "psell_scalar_div": (c_int32, [_P, _P, c_int32, c_int32, _P, _P, c_int32, _P]),
     "psell_pcg_status": (c_int32, [_P, _P, _P, c_double, c_double, _P, _P]),
+    "psell_csr_spmv_dot_alpha": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _E]),
+    "psell_pcg_update_status": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, c_double, c_double, _P, _P, _P, _P]),
     "psell_sell_fill": (c_int32, [_D, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, _E]),
     "psell_sell_spmv": (c_int32, [_D, _P, c_int32, _P, _P, _P, _P, c_int32, _P, _P, _E]),
     "psell_gen_workspace_bytes": (c_size_t, [c_int64]),

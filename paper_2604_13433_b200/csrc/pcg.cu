@@ -379,6 +379,75 @@ __global__ void __launch_bounds__(kBlock) axpy2_kernel(long long n, double* __re
   if (threadIdx.x == 0) parts[blockIdx.x] = v;
 }
 
+// FP64 PCG iteration tail, identity preconditioner (solvers.py:201-209), one launch after
+// psell_csr_spmv_dot_alpha: x += alpha p; r -= alpha q (axpy2's ops); rr = r.r in a fixed
+// order (the last CTA); the status {breakdown, pq, sqrt(rr) / bnorm} the host appends to
+// the history (psell_pcg_status's semantics, gate closed at convergence); beta = rr / rz;
+// rz = rr.  With the gate already closed only the status is written.
+__global__ void __launch_bounds__(kBlock) pcg_update_status_kernel(long long n, double* __restrict__ x,
+                                                                   double* __restrict__ r,
+                                                                   const double* __restrict__ p,
+                                                                   const double* __restrict__ q,
+                                                                   double* scal, int32_t* gate, double bnorm,
+                                                                   double tol, double* out,
+                                                                   double* __restrict__ parts, unsigned* ticket) {
+  __shared__ double sh[kBlock / 32];
+  const int g0 = gate[0];  // changed only by this kernel's last CTA, after every CTA read it
+  if (g0 != 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (g0 == 2 || gate[1]) {
+        out[0] = -1.0;
+      } else {  // breakdown found by this iteration's alpha step: report it once
+        out[0] = 1.0;
+        out[1] = scal[10];
+        out[2] = __ddiv_rn(__dsqrt_rn(scal[12]), bnorm);
+        gate[1] = 1;
+      }
+    }
+    return;
+  }
+  const double a = scal[0];
+  double v = 0.0;
+  const long long gs = (long long)gridDim.x * kBlock;
+  long long i = (long long)blockIdx.x * kBlock + threadIdx.x;
+  for (; i + 3 * gs < n; i += 4 * gs) {
+    double xv[4], rv[4], pv[4], qv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xv[u] = x[i + u * gs];
+      rv[u] = r[i + u * gs];
+      pv[u] = p[i + u * gs];
+      qv[u] = q[i + u * gs];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[i + u * gs] = __dadd_rn(xv[u], __dmul_rn(a, pv[u]));
+      const double rn = __dsub_rn(rv[u], __dmul_rn(a, qv[u]));
+      r[i + u * gs] = rn;
+      v += __dmul_rn(rn, rn);
+    }
+  }
+  for (; i < n; i += gs) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(a, p[i]));
+    const double rn = __dsub_rn(r[i], __dmul_rn(a, q[i]));
+    r[i] = rn;
+    v += __dmul_rn(rn, rn);
+  }
+  v = block_sum<kBlock>(v, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = v;
+  double rr;
+  if (last_cta_sum<kBlock>(parts, ticket, rr, sh) && threadIdx.x == 0) {
+    scal[12] = rr;
+    const double rel = __ddiv_rn(__dsqrt_rn(rr), bnorm);
+    out[0] = 0.0;
+    out[1] = scal[10];
+    out[2] = rel;
+    if (rel < tol) gate[0] = 2;
+    scal[2] = rr / scal[4];  // beta
+    scal[4] = rr;            // rz
+  }
+}
+
 // p = z + b p  (solvers.py:209,255); coef == NULL -> p = z (252)
 __global__ void __launch_bounds__(kBlock) xpby_kernel(long long n, double* __restrict__ p,
                                                       const double* __restrict__ z,
@@ -617,6 +686,15 @@ int psell_axpy2(int64_t n, double* x, double* r, const double* p, const double* 
   cudaStream_t st = as_stream(stream);
   axpy2_kernel<<<kRB, kBlock, 0, st>>>(n, x, r, p, q, coef, skip_flag, partials);
   finalize(partials, kRB, 1, out1, skip_flag, st);
+  return LAUNCH_OK();
+}
+
+int psell_pcg_update_status(int64_t n, double* x, double* r, const double* p, const double* q, double* scal,
+                            int32_t* gate, double bnorm, double tol, double* out, double* partials,
+                            unsigned* ticket, void* stream) {
+  if (!ticket || !gate || !scal || !out) return PSELL_EARG;
+  pcg_update_status_kernel<<<kRB, kBlock, 0, as_stream(stream)>>>(n, x, r, p, q, scal, gate, bnorm, tol, out,
+                                                                   partials, ticket);
   return LAUNCH_OK();
 }
 

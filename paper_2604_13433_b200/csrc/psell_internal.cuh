@@ -279,6 +279,44 @@ __device__ __forceinline__ void ipcg_alpha_step(double pq, double* scal, int32_t
   scal[2] = scal[0] / pq;
 }
 
+// shared-memory mbarrier + bulk-copy (TMA 1-D) helpers of the staged kernels
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// FP64 PCG scalar steps of the fused iteration (solvers.py:196-207), identity preconditioner.
+// scal: [0]=alpha [1]=pq [2]=beta [4]=rz [10]=pq [12]=rr; gate: see psell_pcg_status
+__device__ __forceinline__ void pcg_alpha_step(double pq, double* scal, int32_t* gate) {
+  scal[1] = pq;
+  scal[10] = pq;
+  if (pq <= 0.0 || !isfinite(pq)) {
+    gate[0] = 1;
+    return;
+  }
+  scal[0] = scal[4] / pq;
+}
+
 __device__ __forceinline__ void ipcg_beta_step(double rz_new, double* scal, int32_t* iflags) {
   scal[4] = rz_new;
   scal[3] = rz_new / scal[0];

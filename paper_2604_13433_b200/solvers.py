@@ -24,6 +24,7 @@ the dot association.
 from __future__ import annotations
 
 import logging
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -689,7 +690,8 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
     h_stat = torch.zeros(6, dtype=torch.float64, pin_memory=True)
     events = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def enqueue(k):
+    def body(k):
+        st = d.st()
         if not o.apply_pq(p, q, 0):
             o.apply(p, q)
             lib.psell_pq_pr(n, p.data_ptr(), q.data_ptr(), None, d.p(d.partials), d.p(d.loc, 0), st)
@@ -701,7 +703,6 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
         slot = 16 + 3 * (k % 2)
         lib.psell_pcg_status(d.p(d.scal, 10), d.p(d.scal, 12), gp, bnorm, cfg.tol, d.p(d.scal, slot), st)
         h_stat[3 * (k % 2):3 * (k % 2) + 3].copy_(d.scal[slot:slot + 3], non_blocking=True)
-        events[k % 2].record()
         if invp is None:
             # identity: z = r, and r.z is the r.r just reduced -- the same kernel
             # grid, per-thread order and tree as psell_precond_dot, so the same bits
@@ -713,6 +714,32 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
         lib.psell_scalar_div(d.p(d.scal, rz_slot), d.p(d.scal, 4), 1, 1, d.p(d.scal, 2), None, 0, st)  # beta
         lib.psell_sum_strided(d.p(d.scal, rz_slot), 1, 1, 1, d.p(d.scal, 4), st)                   # rz = rz_new
         lib.psell_xpby(n, p.data_ptr(), z.data_ptr(), d.p(d.scal, 2), st)
+
+    # one GPU, f64 CSR operator, identity preconditioner (the FP64 comparator of config 5):
+    # three launches per iteration -- SpMV + p.q + alpha, update + r.r + status + beta,
+    # direction -- with the scalar steps in the last CTA of the first two (fixed order)
+    fused = (o.G == 1 and backend.name == "csr64" and invp is None
+             and os.environ.get("PSELL_PCG_FUSED", "1") != "0")
+    if fused:
+        D = backend.source.to_device()
+        L = d.L
+
+    def body_fused(k):
+        st = d.st()
+        slot = 16 + 3 * (k % 2)
+        err = L.PsellError()
+        rc = lib.psell_csr_spmv_dot_alpha(D.n_rows, L.ptr(D.row_ptr), L.ptr(D.col_idx), L.ptr(D.values),
+                                          p.data_ptr(), q.data_ptr(), p.data_ptr(), d.p(d.partials), d.p(d.scal),
+                                          gp, d.p(d.ticket, 0), st, err)
+        L.check(rc, err)
+        lib.psell_pcg_update_status(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal), gp,
+                                    bnorm, cfg.tol, d.p(d.scal, slot), d.p(d.partials), d.p(d.ticket, d.tstride), st)
+        h_stat[3 * (k % 2):3 * (k % 2) + 3].copy_(d.scal[slot:slot + 3], non_blocking=True)
+        lib.psell_xpby_checked(n, p.data_ptr(), r.data_ptr(), d.p(d.scal, 2), gp, st)
+
+    def enqueue(k):
+        (body_fused if fused else body)(k)
+        events[k % 2].record()
 
     converged, reason, it = False, None, 0
     if cfg.max_outer <= 0:

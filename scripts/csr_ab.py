@@ -1,4 +1,7 @@
-"""K4 CSR SpMV timing (7-point 256^3, f64 x): CUDA events over 50 launches."""
+"""K4 CSR SpMV timing (default 7-point 256^3, f64 x): CUDA events over 50 launches, and a
+digest of y so the PSELL_CSR variants (bulk default / pipe / tiled) can be checked bitwise.
+usage: csr_ab.py [nx] [kind] [dtype]"""
+import hashlib
 import sys
 
 import torch
@@ -7,9 +10,12 @@ sys.path.insert(0, ".")
 import paper_2604_13433_b200 as P  # noqa: E402
 
 nx = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-A = P.stencil_device("poisson3d", nx, scale="sym")
+kind = sys.argv[2] if len(sys.argv) > 2 else "poisson3d"
+dt = getattr(torch, sys.argv[3]) if len(sys.argv) > 3 else torch.float64
+A = P.stencil_device(kind, nx, scale="sym" if kind == "poisson3d" else None)
+n = A.n_rows
 torch.manual_seed(0)
-x = torch.rand(nx ** 3, dtype=torch.float64, device="cuda")
+x = torch.rand(n, dtype=torch.float64, device="cuda").to(dt)
 y = torch.empty_like(x)
 P.csr_spmv(A, x, out=y)
 ref = y.clone()
@@ -22,6 +28,7 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / 50 * 1e3
 nnz = int(A.nnz)
-n = nx ** 3
-by = 8 * (n + 1) + 12 * nnz + 8 * n + 8 * n
-print(f"csr f64 {us:.1f} us  {by / us / 1e3:.0f} GB/s (algorithmic {by / 1e6:.0f} MB)  checksum {float(ref.sum()):.17g}")
+es = x.element_size()
+by = 8 * (n + 1) + 12 * nnz + es * n + es * n
+h = hashlib.sha256(ref.cpu().numpy().tobytes()).hexdigest()[:16]
+print(f"csr {kind} {nx} {str(dt)[6:]} {us:.1f} us  {by / us / 1e3:.0f} GB/s (algorithmic {by / 1e6:.0f} MB)  y {h}")

@@ -231,3 +231,21 @@ def test_iocg_stopping_rules_vs_oracle():
     inner_solver = next(iter(be._inner_cache.values()))
     z = torch.empty(A.n_rows, dtype=torch.float64, device="cuda")
     assert inner_solver.solve(torch.as_tensor(b).cuda(), z) == 10
+
+
+@pytest.mark.parametrize("nx,tol,max_outer", [(24, 1e-9, 2000), (6, 1e-8, 7), (6, 10.0, 50)])
+def test_pcg_fused_iteration_matches_unfused(monkeypatch, nx, tol, max_outer):
+    """The fused FP64 PCG iteration (SpMV + p.q + alpha, update + r.r + status + beta,
+    direction: 3 launches) against the 11-launch sequence: same stopping point and
+    iterates up to the association of the two dot reductions."""
+    A, b = _problem(nx, 5)
+    cfg = S.SolveConfig(tol=tol, max_outer=max_outer)
+    monkeypatch.setenv("PSELL_PCG_FUSED", "1")
+    rf = S.pcg(A, b, cfg)
+    monkeypatch.setenv("PSELL_PCG_FUSED", "0")
+    ru = S.pcg(A, b, cfg)
+    assert (rf.converged, rf.outer_iters, rf.reason) == (ru.converged, ru.outer_iters, ru.reason)
+    assert len(rf.residual_history) == len(ru.residual_history)
+    assert np.allclose(rf.residual_history, ru.residual_history, rtol=1e-9, atol=0)
+    assert np.abs(rf.x - ru.x).max() <= 1e-10 * max(1.0, np.abs(ru.x).max())
+    assert abs(rf.final_true_relres - ru.final_true_relres) <= 1e-6 * ru.final_true_relres + 1e-300
