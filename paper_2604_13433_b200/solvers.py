@@ -645,6 +645,30 @@ class _Outer:
         return report
 
 
+class _HostMirror:
+    """The per-iteration status block read back on a side stream: the few-byte D2H copy
+    waits for its producer kernel there, so the next kernel of the iteration does not
+    queue behind a PCIe round trip on the solver's stream."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.side = torch.cuda.Stream()
+
+    def copy(self, dst, src):
+        """dst (pinned host) <- src once the work queued so far on the current stream is
+        done; returns the event that marks the copy complete."""
+        torch = self.torch
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream())
+        self.side.wait_event(ready)
+        with torch.cuda.stream(self.side):
+            dst.copy_(src, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.side)
+        return done
+
+
 def _dev_mod():
     from . import _dev
     return _dev
@@ -688,7 +712,8 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
     gate.zero_()
     gp = gate.data_ptr()
     h_stat = torch.zeros(6, dtype=torch.float64, pin_memory=True)
-    events = [torch.cuda.Event(), torch.cuda.Event()]
+    mirror = _HostMirror()
+    events = [None, None]  # per status slot: the event of its last read-back
 
     def body(k):
         st = d.st()
@@ -702,7 +727,7 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
         d.reduce(2, 1, 12)                                                 # scal12 = rr
         slot = 16 + 3 * (k % 2)
         lib.psell_pcg_status(d.p(d.scal, 10), d.p(d.scal, 12), gp, bnorm, cfg.tol, d.p(d.scal, slot), st)
-        h_stat[3 * (k % 2):3 * (k % 2) + 3].copy_(d.scal[slot:slot + 3], non_blocking=True)
+        events[k % 2] = mirror.copy(h_stat[3 * (k % 2):3 * (k % 2) + 3], d.scal[slot:slot + 3])
         if invp is None:
             # identity: z = r, and r.z is the r.r just reduced -- the same kernel
             # grid, per-thread order and tree as psell_precond_dot, so the same bits
@@ -734,12 +759,13 @@ def pcg(A, b, cfg: SolveConfig = None, x0=None, *, comm=None) -> SolveReport:
         L.check(rc, err)
         lib.psell_pcg_update_status(n, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), d.p(d.scal), gp,
                                     bnorm, cfg.tol, d.p(d.scal, slot), d.p(d.partials), d.p(d.ticket, d.tstride), st)
-        h_stat[3 * (k % 2):3 * (k % 2) + 3].copy_(d.scal[slot:slot + 3], non_blocking=True)
+        events[k % 2] = mirror.copy(h_stat[3 * (k % 2):3 * (k % 2) + 3], d.scal[slot:slot + 3])
         lib.psell_xpby_checked(n, p.data_ptr(), r.data_ptr(), d.p(d.scal, 2), gp, st)
 
     def enqueue(k):
+        if events[k % 2] is not None:  # slot k % 2 is rewritten only after its last read-back
+            torch.cuda.current_stream().wait_event(events[k % 2])
         (body_fused if fused else body)(k)
-        events[k % 2].record()
 
     converged, reason, it = False, None, 0
     if cfg.max_outer <= 0:
@@ -820,14 +846,20 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
     gp = gate.data_ptr()
     h_stat = torch.zeros(6, dtype=torch.float64, pin_memory=True)
     h_in = torch.zeros(4, dtype=torch.int32, pin_memory=True)
-    events = [torch.cuda.Event(), torch.cuda.Event()]
+    mirror = _HostMirror()
+    events = [None, None]  # per slot: the read-back of the iteration's status (after its h_in)
+    in_done = [None]       # the read-back of the inner flags (rewritten by the next inner solve)
 
     def enqueue(k):
         slot = k % 2
+        main = torch.cuda.current_stream()
+        for ev in (events[slot], in_done[0]):
+            if ev is not None:
+                main.wait_event(ev)
         if _inner is not None:
             if ahead:
                 _inner.launch(r, z)
-                h_in[2 * slot:2 * slot + 2].copy_(_inner.d.flags[:2], non_blocking=True)
+                in_done[0] = mirror.copy(h_in[2 * slot:2 * slot + 2], _inner.d.flags[:2])
             else:
                 h_in[2 * slot + 1] = _inner.solve(r, z)
         elif inner_preconditioner is not None:
@@ -855,8 +887,7 @@ def fcg(A, b, cfg: SolveConfig = None, inner_preconditioner: Callable = None, *,
         d.reduce(4, 1, 12)                                 # scal12 = r.r
         sl = 16 + 3 * slot
         lib.psell_pcg_status(d.p(d.scal, 10), d.p(d.scal, 12), gp, bnorm, cfg.tol, d.p(d.scal, sl), st)
-        h_stat[3 * slot:3 * slot + 3].copy_(d.scal[sl:sl + 3], non_blocking=True)
-        events[slot].record()
+        events[slot] = mirror.copy(h_stat[3 * slot:3 * slot + 3], d.scal[sl:sl + 3])
 
     if cfg.max_outer <= 0:
         reason = f"maximum iterations ({cfg.max_outer}) reached"
