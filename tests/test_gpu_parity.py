@@ -568,3 +568,21 @@ def test_narrow_kernel_equals_pair_kernel(monkeypatch, rng, matrix, sigma, mode)
             if dt == torch.float32:
                 assert torch.equal(res["pair"][1], res[key][1]), (matrix, pre, key)
                 assert res[key][2] == pytest.approx(res["pair"][2], rel=1e-12)
+
+
+@pytest.mark.parametrize("n", [1, 3, 255, 257, 5000])
+def test_csr_spmv_bulk_edges(n):
+    """K4's bulk-staged path on ragged small matrices: a single partial block, spans that
+    start and end off the 16-byte grid (tail entries in registers), empty rows and rows
+    longer than one stage; bitwise vs the oracle in every working precision."""
+    rng = np.random.default_rng(n)
+    lens = rng.integers(0, 12, n)
+    lens[rng.integers(0, n, max(1, n // 500))] = rng.integers(0, 2500, max(1, n // 500))
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = rng.integers(0, n, int(rp[-1])).astype(np.int32)
+    v = rng.standard_normal(int(rp[-1]))
+    A = P.CsrMatrix(n, n, rp, ci, v)
+    for dt in (np.float16, np.float32, np.float64):
+        x = rng.standard_normal(n).astype(dt)
+        y = P.csr_spmv(A, x, dt)
+        assert np.array_equal(_bits(y), _bits(O.csr_spmv(rp, ci, v, x, dt))), dt
