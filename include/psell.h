@@ -68,6 +68,10 @@ typedef enum psell_dtype { PSELL_DT_F16 = 0, PSELL_DT_F32 = 1, PSELL_DT_F64 = 2 
                                   register-pipelined dual-slice kernel (A/B experiments) */
 #define PSELL_SPMV_NARROW 4     /* mean slice width <= 12 steps (e.g. 7-point rows): 12-step chunks */
 #define PSELL_SPMV_NARROW12 8   /* with NARROW: every slice <= 12 steps, the TMA slot kernel may run */
+#define PSELL_SPMV_W32 16       /* every slice <= 32 steps: the wide TMA kernel may run.  Like NARROW12
+                                  it must be true of the matrix (PackSellMatrix.spmv_flags derives it from
+                                  the offsets); a wider slice under it is cut to its first 32 steps (the
+                                  staging never overruns its slot) and its rows come out wrong */
 
 typedef struct psell_error {
   int32_t code;  /* psell_status */

@@ -39,6 +39,7 @@ struct SpmvArgs {
   int variant;  // 0: register-pipelined kernels (default), 2: persistent TMA stream
   int narrow;   // mean slice width <= 12 steps (PSELL_SPMV_NARROW)
   int narrow12; // every slice <= 12 steps (PSELL_SPMV_NARROW12): the slot kernel applies
+  int w32;      // every slice <= 32 steps (PSELL_SPMV_W32): the wide TMA kernel applies
   int codec;
   // long-slice segmentation (0 = off): slices wider than seg_len steps run as
   // segments (see spmv_seg_kernel)
@@ -1930,6 +1931,203 @@ __global__ void __launch_bounds__(kBlock, 4) spmv_narrow_tma_kernel(const SpmvAr
   finish_dot<DOT>(a, dotv);
 }
 
+// ---- wide TMA kernel (slices of <= 32 steps: 27-point rows, config 2 / 3).  A read-only
+// stream reaches ~7.2 TB/s on this GPU against the 6.6 TB/s copy rate (scripts/probe/
+// stream_read.py), so the dual kernel's 6.2 TB/s leaves room: it has bytes in flight only
+// between a chunk's load and its decode.  Here each warp keeps the NEXT slice's words
+// (<= 4 KB) in flight while it decodes the current one: one slice per iteration, its words
+// staged by one cp.async.bulk (elected lane, mbarrier completion, evict-first) into one of
+// two per-warp shared-memory slots, the offsets of the slices ahead through a 4-entry
+// cp.async ring (as the narrow TMA kernel).  Decode in 8-step two-pass chunks (cursor
+// prefix + gathers, then FMAs).  Per row the same steps in the same order with the same
+// FMA as the dual kernel: bitwise equal to it.
+constexpr int kWtSteps = 32;
+constexpr int kWtSlotWords = kWtSteps * 32;
+struct WtMeta {
+  long long off[4][2];  // ring of {o0, o1} for the slices ahead
+};
+constexpr size_t kWtSmemBytes = kWarpsPerCta * (2 * kWtSlotWords * 4 + 2 * 8 + sizeof(WtMeta));
+#ifndef PSELL_WIDE_CTAS
+#define PSELL_WIDE_CTAS 3
+#endif
+#ifndef PSELL_WIDE_K
+#define PSELL_WIDE_K 16
+#endif
+template <int CODEC, typename XT, bool DOT, int PB, bool P2>
+__global__ void __launch_bounds__(kBlock, PSELL_WIDE_CTAS) spmv_wide_tma_kernel(const SpmvArgs a) {
+  using S = NarrowStep<CODEC, XT>;
+  constexpr int K = PSELL_WIDE_K;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  extern __shared__ __align__(128) unsigned char wt_smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint32_t* slots = reinterpret_cast<uint32_t*>(wt_smem) + warp * 2 * kWtSlotWords;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wt_smem + kWarpsPerCta * 2 * kWtSlotWords * 4) + warp * 2;
+  WtMeta* meta = reinterpret_cast<WtMeta*>(wt_smem + kWarpsPerCta * (2 * kWtSlotWords * 4 + 16)) + warp;
+  const uint32_t ns = (uint32_t)a.n_slices;
+  const uint32_t n_rows = (uint32_t)a.n_rows;
+  const uint32_t ws = gridDim.x * (unsigned)kWarpsPerCta;
+  const XT* __restrict__ x = static_cast<const XT*>(a.x);
+  const uint32_t* __restrict__ pack = static_cast<const uint32_t*>(a.pack);
+  const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+  const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+  const uint32_t kl = (uint32_t)a.k_left, row0 = (uint32_t)a.row0, se = (uint32_t)a.se;
+  const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+  auto perm_of = [&](uint32_t s) -> uint32_t {
+    const uint32_t sc = s < n_rows ? s : n_rows - 1u;
+    if constexpr (PB == 1) return (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc);
+    else return (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
+  };
+  // lanes 0..1: offsets k, k + 1 into ring entry r (async; one commit group per call)
+  auto request = [&](uint32_t k, uint32_t r) {
+    if (lane < 2u && k < ns) cp_async8(&meta->off[r][lane], a.offset + k + lane);
+    cp_async_commit();
+  };
+  // the whole warp: the bulk copy of the slice in ring entry r into slot sl (elected lane);
+  // an empty slice just arrives on the barrier
+  auto issue = [&](uint32_t sl, uint32_t r) {
+    const long long o0 = meta->off[r][0], o1 = meta->off[r][1];
+    const uint32_t b = (uint32_t)(o1 - o0) * 4u;
+    const uint32_t bytes = b < kWtSlotWords * 4u ? b : kWtSlotWords * 4u;  // never past the slot
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile(
+        "{\n .reg .pred e, z;\n elect.sync _|e, 0xffffffff;\n setp.eq.u32 z, %2, 0;\n"
+        " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n"
+        " @!z and.pred e, e, !z;\n"
+        " @e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%3], %2, [%1], %4;\n}"
+        ::"r"(smem_u32(slots + sl * kWtSlotWords)), "r"(smem_u32(bars + sl)), "r"(bytes), "l"(pack + o0),
+        "l"(policy_evict_first())
+        : "memory");
+  };
+  uint32_t k = blockIdx.x * (unsigned)kWarpsPerCta + warp;
+  if (lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  request(k, 0);
+  request(k + ws, 1);
+  request(k + 2u * ws, 2);
+  cp_async_wait_all();
+  __syncwarp();
+  if (k < ns) issue(0, 0);
+  if (k + ws < ns) issue(1, 1);
+  uint32_t n_pp = 0u;
+  if constexpr (PB != 0) n_pp = perm_of(k * 32u + lane);
+  double dotv = 0.0;
+  for (uint32_t it = 0; k < ns; k += ws, ++it) {
+    const uint32_t sl = it & 1u, r = it & 3u;
+    request(k + 3u * ws, (it + 3u) & 3u);
+    const uint32_t q0 = (uint32_t)meta->off[r][0], q1 = (uint32_t)meta->off[r][1];
+    const uint32_t wf = (q1 - q0) >> 5, w = wf < (uint32_t)kWtSteps ? wf : (uint32_t)kWtSteps;
+    const uint32_t pp = n_pp;
+    if constexpr (PB != 0) {
+      if (k + ws < ns) n_pp = perm_of((k + ws) * 32u + lane);
+    }
+    uint32_t c2;
+    {
+      const uint32_t g = row0 + k * 32u + lane;
+      const uint32_t blk = P2 ? g & ~(se - 1u) : se == 1u ? g : fast_div(g, a.se_m, a.se_l) * se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      c2 = 2u * (d < cmax ? d : cmax);
+    }
+    const uint32_t rs = k * 32u + lane;
+    uint32_t o = rs;
+    if constexpr (PB != 0) {
+      if constexpr (P2) o = ((k * 32u) & ~((uint32_t)a.sigma - 1u)) + pp;
+      else o = fast_div(k * 32u, a.sig_m, a.sig_l) * (uint32_t)a.sigma + pp;
+    }
+    float pv = 0.f;
+    if constexpr (DOT) pv = __ldg(a.p_own + (o < n_rows ? o : n_rows - 1u));
+    mbar_wait(bars + sl, (it >> 1) & 1u);
+    const uint32_t* sp = slots + sl * kWtSlotWords + lane;
+    float acc = 0.f;
+#if PSELL_WIDE_K >= 32
+    // every gather of the slice in flight at once (one L2 round trip per slice); the FMA
+    // pass reads the words from the slot again instead of holding them in registers
+    uint32_t xv[kWtSteps];
+#pragma unroll
+    for (int u = 0; u < kWtSteps; ++u)
+      if ((uint32_t)u < w) xv[u] = S::gather(sp[u * 32], c2, x, m_real);
+#pragma unroll
+    for (int u = 0; u < kWtSteps; ++u)
+      if ((uint32_t)u < w) S::fma(sp[u * 32], xv[u], acc, vmask);
+#else
+    for (uint32_t q = 0; q < w; q += K) {
+      uint32_t wv[K], xv[K];
+      if (q + K <= w) {
+#pragma unroll
+        for (int u = 0; u < K; ++u) wv[u] = sp[(q + u) * 32u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < K; ++u) wv[u] = q + u < w ? sp[(q + u) * 32u] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < K; ++u) xv[u] = S::gather(wv[u], c2, x, m_real);
+#pragma unroll
+      for (int u = 0; u < K; ++u) S::fma(wv[u], xv[u], acc, vmask);
+    }
+#endif
+    // every lane has read the slot and the offsets of slice +2 (requested an iteration
+    // ago) have landed: refill the slot with that slice
+    cp_async_wait_group1();
+    __syncwarp();
+    if (k + 2u * ws < ns) issue(sl, (it + 2u) & 3u);
+    if (rs < n_rows) {
+      XT yv;
+      if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+      else yv = acc;
+      static_cast<XT*>(a.y)[o] = yv;
+      if constexpr (DOT) dotv += (double)pv * (double)to_f<XT>(yv);
+    }
+  }
+  cp_async_wait_all();
+  finish_dot<DOT>(a, dotv);
+}
+
+// the wide TMA kernel for slices of <= 32 steps instead of the dual kernel (PSELL_WIDE=1, A/B;
+// off by default).  27-point 256^3 fp16 / f16 x (profiles/r02/wide_ab*.txt): 8-step chunks
+// 374 us, 16-step 357 us, all 32 gathers in flight with the words re-read from the slot
+// 433 us, against the dual kernel's 324-342 us; bitwise equal.  ncu (8-step): 78 % L1 hits
+// on the gathers (dual 41 %) but 24 resident warps instead of 48 -- the FMAs wait on the
+// gathers (55 % of stall samples), and the staging's shared memory is what caps the warps.
+static bool wide_tma() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_WIDE", v)) return v != 0;
+  return false;
+}
+
+static unsigned wide_grid(long long n_slices) {  // persistent: one warp per slice at most
+  const long long need = ceil_div(n_slices, kWarpsPerCta);
+  const long long cap = (long long)sm_count() * PSELL_WIDE_CTAS;
+  return (unsigned)(need < cap ? need : cap);
+}
+
+template <int CODEC, typename XT, bool DOT, int PB>
+static void launch_wide_pb(const SpmvArgs& a, cudaStream_t st) {
+  static bool attr = false;  // idempotent attributes, benign race
+  if (!attr) {
+    cudaFuncSetAttribute(spmv_wide_tma_kernel<CODEC, XT, DOT, PB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kWtSmemBytes);
+    cudaFuncSetAttribute(spmv_wide_tma_kernel<CODEC, XT, DOT, PB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kWtSmemBytes);
+    attr = true;
+  }
+  const unsigned g = wide_grid(a.n_slices);
+  const bool p2 = (a.se & (a.se - 1)) == 0 && (a.sigma & (a.sigma - 1)) == 0;  // power-of-two blocks
+  if (p2) spmv_wide_tma_kernel<CODEC, XT, DOT, PB, true><<<g, kBlock, kWtSmemBytes, st>>>(a);
+  else spmv_wide_tma_kernel<CODEC, XT, DOT, PB, false><<<g, kBlock, kWtSmemBytes, st>>>(a);
+}
+
+template <int CODEC, typename XT, bool DOT>
+static void launch_wide(const SpmvArgs& a, cudaStream_t st) {
+  if (a.mode != PSELL_MODE_IMPLICIT) launch_wide_pb<CODEC, XT, DOT, 0>(a, st);
+  else if (a.perm_bytes == 1) launch_wide_pb<CODEC, XT, DOT, 1>(a, st);
+  else launch_wide_pb<CODEC, XT, DOT, 2>(a, st);
+}
+
 // word staging of the narrow kernel (PSELL_NARROW_TMA=0: words loaded per lane from global
 // memory, A/B).  7-point 256^3 e8m14 / f32 x: 124.9 vs 137.3 us; fp16 / f16 x 116.1 vs
 // 128.9 us; fused p.q 134.5 vs 139.5 us (profiles/r02/narrow_tma_ab.txt)
@@ -2097,6 +2295,8 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
             launch_tile<CODEC, XT, DOT>(a, st);
           } else if (a.narrow12 && a.seg_len == 0 && narrow_on()) {
             launch_narrow<CODEC, XT, DOT>(a, st);
+          } else if (a.w32 && !a.narrow && a.seg_len == 0 && wide_tma()) {
+            launch_wide<CODEC, XT, DOT>(a, st);
           } else if (dual_slices(a.n_slices) && a.narrow && pair_kernel()) {
             const int pn = pair_nt(DOT);
             const unsigned gp = (unsigned)ceil_div(ceil_div(a.n_slices, 2), pn / 32);
@@ -2187,6 +2387,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.variant = 0;
   a.narrow = 0;
   a.narrow12 = 0;
+  a.w32 = 0;
   a.codec = d->codec;
   a.seg_len = 0;
   a.seg_slice = a.seg_q0 = a.long_slice = a.long_seg0 = nullptr;
@@ -2321,6 +2522,7 @@ int psell_spmv(const psell_desc* d, const void* pack, const int64_t* offset, con
   a.variant = (flags & PSELL_SPMV_TMA_STREAM) ? 2 : 0;
   a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
   a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
+  a.w32 = (flags & PSELL_SPMV_W32) != 0;
   int bad = 1;
   switch (d->codec) {
     case PSELL_FP16: bad = dispatch_x<PSELL_FP16>(a, x_dtype, ref, st); break;
@@ -2341,6 +2543,8 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
   if (flags & PSELL_SPMV_TMA_STREAM) return "spmv_stream_kernel";
   const long long ns = ceil_div(d->n_rows, d->c);
   if ((flags & PSELL_SPMV_NARROW) && tile_kernel()) return "spmv_tile_kernel (TMA ring)";
+  if (!(flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_W32) && wide_tma())
+    return "spmv_wide_tma_kernel (next slice's words staged by cp.async.bulk, two-pass decode, persistent)";
   if ((flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_NARROW12) && narrow_on())
     return narrow_tma() ? "spmv_narrow_tma_kernel (pair words staged by cp.async.bulk, two-pass decode, persistent)"
                         : "spmv_narrow_kernel (pipelined pair metadata, two-pass decode, persistent)";
@@ -2464,6 +2668,8 @@ int64_t psell_spmv_dot_partials(const psell_desc* d, int32_t flags) {
     }
     if (d->codec != PSELL_FP32EMBED && (flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_NARROW12) && narrow_on())
       return narrow_grid(ns);
+    if (d->codec != PSELL_FP32EMBED && !(flags & PSELL_SPMV_NARROW) && (flags & PSELL_SPMV_W32) && wide_tma())
+      return wide_grid(ns);
     if (d->codec != PSELL_FP32EMBED && dual_slices(ns) && pair_kernel() && (flags & PSELL_SPMV_NARROW)) {
       if (const unsigned g = pair_persist_grid(ns, true)) return g;
       return ceil_div(ceil_div(ns, 2), pair_nt(true) / 32);
@@ -2482,6 +2688,7 @@ int psell_spmv_dot(const psell_desc* d, const void* pack, const int64_t* offset,
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
   a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
   a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
+  a.w32 = (flags & PSELL_SPMV_W32) != 0;
   a.x = x;
   a.y = y;
   a.p_own = p_own;
@@ -2509,6 +2716,7 @@ int psell_spmv_dot_alpha(const psell_desc* d, const void* pack, const int64_t* o
   if (!ticket || !scal || !iflags) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null scalar state");
   a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
   a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
+  a.w32 = (flags & PSELL_SPMV_W32) != 0;
   a.x = x;
   a.y = y;
   a.p_own = p_own;

@@ -197,18 +197,21 @@ class PackSellMatrix:
 
     def spmv_flags(self) -> int:
         """Kernel-shape hint for psell_spmv / psell_spmv_dot: PSELL_SPMV_NARROW when the
-        mean slice width is <= 12 steps (7-point rows), so one 12-step chunk covers a slice."""
+        mean slice width is <= 12 steps (7-point rows), so one 12-step chunk covers a slice;
+        NARROW12 / W32 when every slice is <= 12 / 32 steps (the staged kernels' slots)."""
         if self.n_slices == 0:
             return 0
         f = self.__dict__.get("_flags_cache")
         if f is None:
+            import torch
             f = 0
+            wmax = int(torch.max(self.d_offset[1:] - self.d_offset[:-1]).item()) // self.c
             if self.n_stored <= 12 * self.c * self.n_slices:
                 f = 4  # PSELL_SPMV_NARROW
-                import torch
-                wmax = int(torch.max(self.d_offset[1:] - self.d_offset[:-1]).item()) // self.c
                 if wmax <= 12:
                     f |= 8  # PSELL_SPMV_NARROW12: every slice fits the slot kernel's 12 steps
+            if self.c == 32 and wmax <= 32:
+                f |= 16  # PSELL_SPMV_W32: every slice fits the wide TMA kernel's 32-step slot
             self.__dict__["_flags_cache"] = f
         return f
 

@@ -586,3 +586,49 @@ def test_csr_spmv_bulk_edges(n):
         x = rng.standard_normal(n).astype(dt)
         y = P.csr_spmv(A, x, dt)
         assert np.array_equal(_bits(y), _bits(O.csr_spmv(rp, ci, v, x, dt))), dt
+
+
+@pytest.mark.parametrize("matrix", ["stencil27-21", "ragged-wide"])
+@pytest.mark.parametrize("sigma,mode", [(256, "implicit"), (96, "implicit"), (65536, "implicit"), (1, "none")])
+def test_wide_kernel_equals_dual_kernel(monkeypatch, rng, matrix, sigma, mode):
+    """The wide TMA kernel (PSELL_WIDE=1, slices of <= 32 steps staged by cp.async.bulk) gives
+    the dual kernel's bits: plain SpMV over the codec / x dtypes it serves and the fused
+    SpMV + p.q, u8 / u16 / no perm, power-of-two and other sigma, a ragged last slice."""
+    import torch
+    from paper_2604_13433_b200 import _dev, _lib
+    if matrix == "stencil27-21":
+        A = P.stencil27(21)                                  # 9261 rows: ragged last slice
+    else:
+        A = _narrow_csr(rng, 100_003, 13, 27, 400)          # 13..27 entries + dummies-free widths <= 32
+    lib = _lib.lib()
+    for pre, dt in (("fp16", torch.float16), ("e8m10", torch.float32), ("fp16", torch.float32),
+                    ("e8m14", torch.float16)):
+        M = P.build_packsell(A, 32, sigma, P.parse_format(pre), mode)
+        if not M.spmv_flags() & 16:
+            continue  # a slice wider than 32 steps (dummies): the wide kernel does not apply
+        assert not M.spmv_flags() & 4
+        x = (torch.rand(M.n_cols, device="cuda") * 2 - 1).to(dt)
+        res = {}
+        for wide, kname in (("0", "spmv_dual"), ("1", "spmv_wide_tma")):
+            monkeypatch.setenv("PSELL_WIDE", wide)
+            lib.psell_reload_env()
+            name = lib.psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
+            assert name.startswith(kname), name
+            out = [P.packsell_spmv(M, x).clone()]
+            if dt == torch.float32:  # the fused SpMV + p.q is the f32 inner-PCG operator
+                npart = lib.psell_spmv_dot_partials(M.desc(), M.spmv_flags())
+                part = torch.zeros(npart, dtype=torch.float64, device="cuda")
+                q = torch.empty_like(x)
+                err = _lib.PsellError()
+                rc = lib.psell_spmv_dot(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                                        x.data_ptr(), q.data_ptr(), x.data_ptr(), part.data_ptr(), None,
+                                        M.spmv_flags(), _lib.stream_handle(), err)
+                _lib.check(rc, err)
+                out += [q.clone(), float(part.sum())]
+            res[wide] = out
+        monkeypatch.delenv("PSELL_WIDE")
+        lib.psell_reload_env()
+        assert torch.equal(res["0"][0], res["1"][0]), (matrix, pre, dt)
+        if dt == torch.float32:
+            assert torch.equal(res["0"][1], res["1"][1]), (matrix, pre, dt)
+            assert res["1"][2] == pytest.approx(res["0"][2], rel=1e-12)
