@@ -2128,6 +2128,170 @@ static void launch_wide(const SpmvArgs& a, cudaStream_t st) {
   else launch_wide_pb<CODEC, XT, DOT, 2>(a, st);
 }
 
+// ---- staged dual kernel (PSELL_DSTAGE=1, A/B): the dual kernel's pair of slices per warp
+// and its grid, with each 8-step chunk of both slices brought into a per-warp shared-memory
+// stage by two cp.async.bulk copies (1 KB each, elected lane, mbarrier) TWO chunks ahead of
+// its decode, so a chunk costs one L2 round trip (the x gathers) instead of two (the word
+// loads, then the gathers), at the dual kernel's full residency (2 x 2 KB of stages per
+// warp: 6 CTAs x 8 warps per SM).  Same FMAs in the same order: bitwise the dual kernel.
+constexpr int kDsU = 8;
+constexpr int kDsChunkWords = kDsU * 32;  // one slice's chunk, 1 KB
+constexpr size_t kDsSmemBytes = kWarpsPerCta * (2 * 2 * kDsChunkWords * 4 + 2 * 8);
+template <int CODEC, typename XT, bool DOT, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) spmv_dual_stage_kernel(const SpmvArgs a) {
+  using S = NarrowStep<CODEC, XT>;
+  if constexpr (DOT) {
+    if (a.skip && *a.skip) return;
+  }
+  extern __shared__ __align__(128) unsigned char ds_smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint32_t* stages = reinterpret_cast<uint32_t*>(ds_smem) + warp * 4 * kDsChunkWords;  // [2][A, B][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ds_smem + kWarpsPerCta * 4 * kDsChunkWords * 4) + warp * 2;
+  double dotv = 0.0;
+  const long long wg = (long long)blockIdx.x * kWarpsPerCta + warp;
+  const long long kA = 2 * wg, kB = kA + 1;
+  if (kA < a.n_slices) {
+    const bool hasB = kB < a.n_slices;
+    const long long oA = a.offset[kA], oB = a.offset[kA + 1];
+    const long long oE = hasB ? a.offset[kB + 1] : oB;
+    const int wA = (int)((oB - oA) >> 5), wB = (int)((oE - oB) >> 5);
+    const uint32_t* __restrict__ pack = static_cast<const uint32_t*>(a.pack);
+    const XT* __restrict__ x = static_cast<const XT*>(a.x);
+    const uint32_t m_real = CODEC == PSELL_FP16 ? 0xFFFEu : ((2u << a.d) - 2u);
+    const uint32_t vmask = CODEC == PSELL_FP16 ? 0u : ~((2u << a.d) - 1u);
+    const uint32_t se = (uint32_t)a.se, kl = (uint32_t)a.k_left;
+    const uint32_t cmax = a.n_cols > 0 ? (uint32_t)(a.n_cols - 1) : 0u;
+    if (lane == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // chunk c of both slices into stage st (warp-uniform operands, one elected lane)
+    auto issue = [&](uint32_t st, int c) {
+      const int rA = wA - c * kDsU, rB = wB - c * kDsU;
+      const uint32_t nA = rA <= 0 ? 0u : rA >= kDsU ? (uint32_t)kDsU : (uint32_t)rA;
+      const uint32_t nB = rB <= 0 ? 0u : rB >= kDsU ? (uint32_t)kDsU : (uint32_t)rB;
+      const uint32_t bA = nA * 128u, bB = nB * 128u;
+      uint32_t* sA = stages + st * 2 * kDsChunkWords;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile(
+          "{\n .reg .pred e, pa, pb;\n elect.sync _|e, 0xffffffff;\n"
+          " setp.ne.and.u32 pa, %2, 0, e;\n setp.ne.and.u32 pb, %3, 0, e;\n"
+          " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n"
+          " @pa cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%6], %2, [%4], %8;\n"
+          " @pb cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%1], [%7], %3, [%4], %8;\n}"
+          ::"r"(smem_u32(sA)), "r"(smem_u32(sA + kDsChunkWords)), "r"(bA), "r"(bB), "r"(smem_u32(bars + st)),
+          "r"(bA + bB), "l"(pack + oA + c * kDsChunkWords), "l"(pack + oB + c * kDsChunkWords),
+          "l"(policy_evict_first())
+          : "memory");
+    };
+    const int wmax = wA > wB ? wA : wB;
+    const int nch = (wmax + kDsU - 1) / kDsU;
+    if (nch > 0) issue(0, 0);
+    if (nch > 1) issue(1, 1);
+    auto base2 = [&](long long k) -> uint32_t {
+      const uint32_t g = (uint32_t)a.row0 + (uint32_t)(k * 32) + lane;
+      const uint32_t blk = se == 1u ? g : fast_div(g, a.se_m, a.se_l) * se;
+      const uint32_t d = blk > kl ? blk - kl : 0u;
+      return 2u * (d < cmax ? d : cmax);
+    };
+    uint32_t cA = base2(kA), cB = base2(kB);
+    float accA = 0.f, accB = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      const uint32_t st = (uint32_t)c & 1u;
+      mbar_wait(bars + st, ((uint32_t)c >> 1) & 1u);
+      const uint32_t* sa = stages + st * 2 * kDsChunkWords + lane;
+      const uint32_t* sb = sa + kDsChunkWords;
+      const int rA = wA - c * kDsU, rB = wB - c * kDsU;
+      uint32_t xa[kDsU], xb[kDsU];
+      if (rA >= kDsU && rB >= kDsU) {  // full chunk of both slices (warp-uniform): no predicates
+        uint32_t wa[kDsU], wb[kDsU];
+#pragma unroll
+        for (int u = 0; u < kDsU; ++u) {
+          wa[u] = sa[u * 32];
+          wb[u] = sb[u * 32];
+        }
+#pragma unroll
+        for (int u = 0; u < kDsU; ++u) {
+          xa[u] = S::gather(wa[u], cA, x, m_real);
+          xb[u] = S::gather(wb[u], cB, x, m_real);
+        }
+#pragma unroll
+        for (int u = 0; u < kDsU; ++u) {
+          S::fma(wa[u], xa[u], accA, vmask);
+          S::fma(wb[u], xb[u], accB, vmask);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kDsU; ++u) {
+          xa[u] = S::gather(u < rA ? sa[u * 32] : 0u, cA, x, m_real);
+          xb[u] = S::gather(u < rB ? sb[u * 32] : 0u, cB, x, m_real);
+        }
+#pragma unroll
+        for (int u = 0; u < kDsU; ++u) {
+          S::fma(u < rA ? sa[u * 32] : 0u, xa[u], accA, vmask);
+          S::fma(u < rB ? sb[u * 32] : 0u, xb[u], accB, vmask);
+        }
+      }
+      __syncwarp();  // every lane has read stage st: refill it two chunks on
+      if (c + 2 < nch) issue(st, c + 2);
+    }
+    const uint32_t sig = (uint32_t)a.sigma;
+    const uint32_t nr = (uint32_t)a.n_rows;
+    auto out_row = [&](long long k) -> uint32_t {
+      const uint32_t s = (uint32_t)(k * 32) + lane;
+      if (a.mode != PSELL_MODE_IMPLICIT) return s;
+      const uint32_t sc = s < nr ? s : nr - 1u;
+      const uint32_t pp = a.perm_bytes == 1 ? (uint32_t)__ldg(static_cast<const uint8_t*>(a.perm) + sc)
+                                            : (uint32_t)__ldg(static_cast<const uint16_t*>(a.perm) + sc);
+      return fast_div((uint32_t)(k * 32), a.sig_m, a.sig_l) * sig + pp;
+    };
+    auto flush = [&](long long k, float acc) {
+      const uint32_t s = (uint32_t)(k * 32) + lane;
+      const uint32_t o = out_row(k);
+      if ((long long)s < a.n_rows) {
+        XT yv;
+        if constexpr (sizeof(XT) == 2) yv = __float2half_rn(acc);
+        else yv = acc;
+        static_cast<XT*>(a.y)[o] = yv;
+        if constexpr (DOT) dotv += (double)a.p_own[o] * (double)to_f<XT>(yv);
+      }
+    };
+    flush(kA, accA);
+    if (hasB) flush(kB, accB);
+  }
+  finish_dot<DOT>(a, dotv);
+}
+
+static bool dual_stage() {  // PSELL_DSTAGE=1: the staged dual kernel (A/B)
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_DSTAGE", v)) return v != 0;
+  return false;
+}
+
+static int dual_stage_minb() {  // PSELL_DSTAGE=1: 6 CTAs/SM (40 registers), 2: 5 (48 registers)
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_DSTAGE", v)) return v == 2 ? 5 : 6;
+  return 6;
+}
+
+template <int CODEC, typename XT, bool DOT>
+static void launch_dual_stage(const SpmvArgs& a, cudaStream_t st, unsigned grid) {
+  static bool attr = false;  // idempotent attributes, benign race
+  if (!attr) {
+    cudaFuncSetAttribute(spmv_dual_stage_kernel<CODEC, XT, DOT, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDsSmemBytes);
+    cudaFuncSetAttribute(spmv_dual_stage_kernel<CODEC, XT, DOT, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDsSmemBytes);
+    attr = true;
+  }
+  if (dual_stage_minb() == 5) spmv_dual_stage_kernel<CODEC, XT, DOT, 5><<<grid, kBlock, kDsSmemBytes, st>>>(a);
+  else spmv_dual_stage_kernel<CODEC, XT, DOT, 6><<<grid, kBlock, kDsSmemBytes, st>>>(a);
+}
+
 // word staging of the narrow kernel (PSELL_NARROW_TMA=0: words loaded per lane from global
 // memory, A/B).  7-point 256^3 e8m14 / f32 x: 124.9 vs 137.3 us; fp16 / f16 x 116.1 vs
 // 128.9 us; fused p.q 134.5 vs 139.5 us (profiles/r02/narrow_tma_ab.txt)
@@ -2308,6 +2472,8 @@ static void launch_spmv(const SpmvArgs& a, cudaStream_t st) {
             else spmv_pair_kernel<CODEC, XT, DOT, 12, true><<<gd, kBlock, 0, st>>>(a);
           } else if (dual_slices(a.n_slices) && pair_wide()) {
             spmv_pair_kernel<CODEC, XT, DOT, 8, false><<<gd, kBlock, 0, st>>>(a);
+          } else if (dual_slices(a.n_slices) && !a.narrow && a.seg_len == 0 && dual_stage()) {
+            launch_dual_stage<CODEC, XT, DOT>(a, st, gd);
           } else if (dual_slices(a.n_slices) && du == 12)
             spmv_dual_kernel<CODEC, XT, DOT, 12><<<gd, kBlock, 0, st>>>(a);
           else if (dual_slices(a.n_slices))
@@ -2554,6 +2720,8 @@ const char* psell_spmv_kernel_name(const psell_desc* d, int32_t x_dtype, int32_t
                                                          : "spmv_pair_kernel<U=12, persistent>")
                                         : "spmv_pair_kernel<U=12>";
   if (dual_slices(ns) && pair_wide()) return "spmv_pair_kernel<U=8>";
+  if (dual_slices(ns) && !(flags & PSELL_SPMV_NARROW) && dual_stage())
+    return "spmv_dual_stage_kernel (8-step chunks of both slices staged 2 ahead by cp.async.bulk)";
   if (dual_slices(ns)) {
     const int du = dual_chunk((flags & PSELL_SPMV_NARROW) != 0);
     return du == 12 ? "spmv_dual_kernel<U=12>" : "spmv_dual_kernel<U=8>";

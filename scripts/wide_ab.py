@@ -42,7 +42,17 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
           flush=True)
     sys.exit(0)
 
-for name in sys.argv[1:] or ["c2", "c3", "c3-e8m10"]:
-    for v in ("0", "1"):
-        env = dict(os.environ, PSELL_WIDE=v)
+# usage: wide_ab.py [configs ...] [-- VAR=VAL[,VAR=VAL] ...]  (default variants PSELL_WIDE=0 / 1)
+args = sys.argv[1:]
+variants = ["PSELL_WIDE=0", "PSELL_WIDE=1"]
+if "--" in args:
+    variants = args[args.index("--") + 1:]
+    args = args[:args.index("--")]
+for name in args or ["c2", "c3", "c3-e8m10"]:
+    for v in variants:
+        env = dict(os.environ)
+        for kv in v.split(","):
+            if kv:
+                env[kv.split("=", 1)[0]] = kv.split("=", 1)[1]
+        print(f"  [{v}]", end="", flush=True)
         subprocess.run([sys.executable, __file__, "--child", name], env=env, check=False)

@@ -591,8 +591,8 @@ def test_csr_spmv_bulk_edges(n):
 @pytest.mark.parametrize("matrix", ["stencil27-21", "ragged-wide"])
 @pytest.mark.parametrize("sigma,mode", [(256, "implicit"), (96, "implicit"), (65536, "implicit"), (1, "none")])
 def test_wide_kernel_equals_dual_kernel(monkeypatch, rng, matrix, sigma, mode):
-    """The wide TMA kernel (PSELL_WIDE=1, slices of <= 32 steps staged by cp.async.bulk) gives
-    the dual kernel's bits: plain SpMV over the codec / x dtypes it serves and the fused
+    """The wide TMA kernel (PSELL_WIDE=1, slices of <= 32 steps staged by cp.async.bulk) and the
+    staged dual kernel (PSELL_DSTAGE=1, 8-step chunks staged two ahead) give the dual kernel's bits: plain SpMV over the codec / x dtypes it serves and the fused
     SpMV + p.q, u8 / u16 / no perm, power-of-two and other sigma, a ragged last slice."""
     import torch
     from paper_2604_13433_b200 import _dev, _lib
@@ -609,8 +609,9 @@ def test_wide_kernel_equals_dual_kernel(monkeypatch, rng, matrix, sigma, mode):
         assert not M.spmv_flags() & 4
         x = (torch.rand(M.n_cols, device="cuda") * 2 - 1).to(dt)
         res = {}
-        for wide, kname in (("0", "spmv_dual"), ("1", "spmv_wide_tma")):
-            monkeypatch.setenv("PSELL_WIDE", wide)
+        for wide, kname in (("0", "spmv_dual_kernel"), ("1", "spmv_wide_tma"), ("s", "spmv_dual_stage")):
+            monkeypatch.setenv("PSELL_WIDE", "1" if wide == "1" else "0")
+            monkeypatch.setenv("PSELL_DSTAGE", "1" if wide == "s" else "0")
             lib.psell_reload_env()
             name = lib.psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
             assert name.startswith(kname), name
@@ -627,8 +628,10 @@ def test_wide_kernel_equals_dual_kernel(monkeypatch, rng, matrix, sigma, mode):
                 out += [q.clone(), float(part.sum())]
             res[wide] = out
         monkeypatch.delenv("PSELL_WIDE")
+        monkeypatch.delenv("PSELL_DSTAGE")
         lib.psell_reload_env()
-        assert torch.equal(res["0"][0], res["1"][0]), (matrix, pre, dt)
-        if dt == torch.float32:
-            assert torch.equal(res["0"][1], res["1"][1]), (matrix, pre, dt)
-            assert res["1"][2] == pytest.approx(res["0"][2], rel=1e-12)
+        for v in ("1", "s"):
+            assert torch.equal(res["0"][0], res[v][0]), (matrix, pre, dt, v)
+            if dt == torch.float32:
+                assert torch.equal(res["0"][1], res[v][1]), (matrix, pre, dt, v)
+                assert res[v][2] == pytest.approx(res["0"][2], rel=1e-12)
