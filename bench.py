@@ -695,6 +695,18 @@ def gpu_slab_expect(M, cfg, rows, seed):
             "k_left": M.k_left, "y_ref": y_ref, "y_fma": y_fma}
 
 
+def seg_launches(seg, kernel_name):
+    """Launches per SpMV and the kernel label of a segmented (power-law) matrix: the long
+    slices' segments run in one grid with the short slices (spmv_dual_seg_kernel) unless
+    PSELL_SEGMERGE=0 splits them into their own launch; a combine kernel adds them up."""
+    if seg is None:
+        return 1, kernel_name
+    merged = seg["n_seg"] > 0 and os.environ.get("PSELL_SEGMERGE", "1") != "0"
+    if merged:
+        return 1 + (seg["n_long"] > 0), "spmv_dual_seg_kernel (segments + short slices in one grid) + seg_combine_kernel"
+    return 1 + (seg["n_seg"] > 0) + (seg["n_long"] > 0), kernel_name + " + spmv_seg_kernel + seg_combine_kernel"
+
+
 EXTRA_CONFIGS = ("c3", "c3-e8m10", "c4", "c4b")
 
 
@@ -728,8 +740,7 @@ def config_summary(args, name, peak):
     xsz = x.element_size()
     kernel = _lib.lib().psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
     seg = _seg_schedule(M)
-    if seg is not None:
-        kernel += " + spmv_seg_kernel + seg_combine_kernel"
+    kernel = seg_launches(seg, kernel)[1]
     for _ in range(max(3, args.warmup)):
         P.packsell_spmv(M, x, out=y)
     torch.cuda.synchronize()
@@ -854,10 +865,8 @@ def run_ours(args, cfg):
     from paper_2604_13433_b200 import _dev, _lib
     from paper_2604_13433_b200.packed import _seg_schedule
     kernel_name = _lib.lib().psell_spmv_kernel_name(M.desc(), _dev.T_DT_CODE[x.dtype], M.spmv_flags()).decode()
-    seg = _seg_schedule(M)  # long power-law slices: + segment kernel + combine kernel per step
-    launches_per_step = 1 if seg is None else 1 + (seg["n_seg"] > 0) + (seg["n_long"] > 0)
-    if seg is not None:
-        kernel_name += " + spmv_seg_kernel + seg_combine_kernel"
+    seg = _seg_schedule(M)  # long power-law slices: + segments (merged grid by default) + combine
+    launches_per_step, kernel_name = seg_launches(seg, kernel_name)
     bytes_local = M.spmv_bytes(xsz, xsz, with_perm=True, x_elems=touched)
     bytes_noperm = M.spmv_bytes(xsz, xsz, with_perm=False, x_elems=touched)
     st = torch.cuda.current_stream()

@@ -622,8 +622,10 @@ __device__ __forceinline__ void aff_exit(const SpmvArgs& a) {
   }
 }
 
+// the dual kernel's body for CTA `bid` of its grid (spmv_dual_seg_kernel runs it from a
+// merged grid whose first CTAs take the long-slice segments)
 template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
-__global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) {
+__device__ __forceinline__ void dual_body(const SpmvArgs& a, unsigned bid) {
   using S = FastStep<CODEC, XT, GR>;
   if constexpr (DOT) {
     if (a.skip && *a.skip) return;
@@ -632,7 +634,7 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
   double dotv = 0.0;
   const uint32_t npairs = (uint32_t)((a.n_slices + 1) >> 1);
   AffSched sched{AFF ? smid_u32() % (uint32_t)a.aff_chunks : 0u, 0u};
-  long long wg = AFF ? (long long)aff_next(a, sched, npairs) : ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  long long wg = AFF ? (long long)aff_next(a, sched, npairs) : ((long long)bid * kBlock + threadIdx.x) >> 5;
   for (; !AFF || wg != (long long)~0u; wg = AFF ? (long long)aff_next(a, sched, npairs) : (long long)~0u) {
   const long long kA = 2 * wg, kB = kA + 1;
   if (kA < a.n_slices) {
@@ -749,6 +751,11 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) 
   }
   if constexpr (AFF) aff_exit(a);
   finish_dot<DOT>(a, dotv);
+}
+
+template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
+__global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) {
+  dual_body<CODEC, XT, DOT, U, GR, AFF>(a, blockIdx.x);
 }
 
 // ---- pair kernel (C == 32): a warp runs slices 2w and 2w+1.  Full U-step
@@ -1186,9 +1193,9 @@ __global__ void __launch_bounds__(kBlock) seg_prefix_kernel(const SpmvArgs a, lo
 }
 
 template <int CODEC, typename XT, int U>
-__global__ void __launch_bounds__(kBlock, 6) spmv_seg_kernel(const SpmvArgs a, long long n_seg) {
+__device__ __forceinline__ void seg_body(const SpmvArgs& a, long long n_seg, unsigned bid) {
   using S = FastStep<CODEC, XT, true>;  // irregular rows: flag-predicated gathers
-  const long long sg = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long sg = ((long long)bid * kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (sg >= n_seg) return;
   const int k = a.seg_slice[sg];
@@ -1221,6 +1228,23 @@ __global__ void __launch_bounds__(kBlock, 6) spmv_seg_kernel(const SpmvArgs a, l
     for (int u = 0; u < U; ++u) cur[u] = nxt[u];
   }
   a.seg_partial[sg * 32 + lane] = acc;
+}
+
+template <int CODEC, typename XT, int U>
+__global__ void __launch_bounds__(kBlock, 6) spmv_seg_kernel(const SpmvArgs a, long long n_seg) {
+  seg_body<CODEC, XT, U>(a, n_seg, blockIdx.x);
+}
+
+// Segments and short slices in ONE grid (the default for segmented matrices): the first
+// seg_ctas CTAs run the long slices' segments, the rest the dual kernel over the short
+// slices.  CTAs dispatch in index order, so the segments start first and the dual CTAs
+// fill the GPU around them: the segment launch (551 CTAs on config 4, 62 % of one wave at
+// 6 CTAs/SM) no longer runs alone after the dual kernel.  Same code per warp: bitwise.
+template <int CODEC, typename XT, int U>
+__global__ void __launch_bounds__(kBlock, 6) spmv_dual_seg_kernel(const SpmvArgs a, long long n_seg,
+                                                                 unsigned seg_ctas) {
+  if (blockIdx.x < seg_ctas) seg_body<CODEC, XT, U>(a, n_seg, blockIdx.x);
+  else dual_body<CODEC, XT, false, 8, true, false>(a, blockIdx.x - seg_ctas);
 }
 
 template <typename XT>
@@ -2772,9 +2796,27 @@ static int aff_ctas() {
   return 6;
 }
 
+// one merged grid for segments + short slices (PSELL_SEGMERGE=0: two launches, A/B)
+static bool seg_merge() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_SEGMERGE", v)) return v != 0;
+  return true;
+}
+
 template <int CODEC, typename XT>
 static void launch_segmented(const SpmvArgs& a, long long n_seg, long long n_long, cudaStream_t st) {
-  if (a.sched && a.aff_chunks > 0 && aff_on() && a.n_slices >= 2) {
+  const bool aff = a.sched && a.aff_chunks > 0 && aff_on() && a.n_slices >= 2;
+  if (!aff && n_seg > 0 && seg_merge() && dual_slices(a.n_slices) && !a.narrow && dual_chunk(false) == 8 &&
+      !pair_wide()) {
+    const unsigned seg_ctas = (unsigned)ceil_div(n_seg * 32, kBlock);
+    const unsigned gd = (unsigned)ceil_div(ceil_div(a.n_slices, 2), kWarpsPerCta);
+    spmv_dual_seg_kernel<CODEC, XT, 8><<<seg_ctas + gd, kBlock, 0, st>>>(a, n_seg, seg_ctas);
+    if (n_long > 0)
+      seg_combine_kernel<XT><<<(unsigned)ceil_div(n_long * 32, kBlock), kBlock, 0, st>>>(a, n_long);
+    return;
+  }
+  if (aff) {
     const unsigned g = (unsigned)(sm_count() * aff_ctas());
     spmv_dual_kernel<CODEC, XT, false, 8, true, true><<<g, kBlock, 0, st>>>(a);
   } else

@@ -308,8 +308,10 @@ def test_powerlaw_build_vs_oracle():
 
 @pytest.mark.parametrize("sigma,pre,dt", [(256, "fp16", np.float16), (4096, "e8m14", np.float32),
                                           (65536, "fp16", np.float32)])
-def test_long_slice_segmentation(sigma, pre, dt):
-    """Power-law rows wider than SEG_LEN run as checkpointed segments; result within the FMA bound."""
+def test_long_slice_segmentation(monkeypatch, sigma, pre, dt):
+    """Power-law rows wider than SEG_LEN run as checkpointed segments; result within the FMA bound.
+    The merged segment + short-slice grid (default) is bitwise the two-launch form."""
+    from paper_2604_13433_b200 import _lib
     from paper_2604_13433_b200.packed import SEG_LEN, _seg_schedule
     from paper_2604_13433_b200.stencil import powerlaw_rows
     A = powerlaw_rows(1 << 17, 11)
@@ -317,7 +319,14 @@ def test_long_slice_segmentation(sigma, pre, dt):
     s = _seg_schedule(M)
     assert s is not None and s["n_long"] > 0
     x = np.random.default_rng(2).uniform(-1, 1, A.n_cols).astype(dt)
-    y = P.packsell_spmv(M, x).astype(np.float64)
+    y = P.packsell_spmv(M, x)
+    monkeypatch.setenv("PSELL_SEGMERGE", "0")
+    _lib.lib().psell_reload_env()
+    y2 = P.packsell_spmv(M, x)
+    monkeypatch.delenv("PSELL_SEGMERGE")
+    _lib.lib().psell_reload_env()
+    assert np.array_equal(_bits(y), _bits(y2))
+    y = y.astype(np.float64)
     ref = P.packsell_spmv(M, x.astype(np.float32), ref_order=True).astype(np.float64)
     lmax = int(np.max(np.diff(M.offset) // 32))
     aq = np.abs(P.quantize(P.parse_format(pre), A.values))
