@@ -756,7 +756,9 @@ def config_summary(args, name, peak):
     out = {"workload": cfg["workload"], "n": n, "nnz": nnz, "n_stored": int(M.n_stored), "counts": list(M.counts),
            "k_left": int(kl), "kernel": kernel, "steps": args.steps, "ms_per_step": ms, "bytes_per_step": int(nbytes),
            "value": gbs, "unit": "GB/s", "gflops": 2 * nnz / (ms * 1e-3) / 1e9,
-           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "frac": gbs / peak}, "build_s": build_s}
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "frac": gbs / peak,
+                        "traffic": ncu_traffic(name)[0], "traffic_source": ncu_traffic(name)[1]},
+           "build_s": build_s}
     if cfg["kind"].startswith("powerlaw"):
         try:
             from paper_2604_13433_b200.vendor import gather_ceiling
