@@ -2191,6 +2191,8 @@ __global__ void __launch_bounds__(kBlock, MINB) spmv_dual_stage_kernel(const Spm
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
+    // shared-window addresses computed once (not per chunk)
+    const uint32_t stage_u32 = smem_u32(stages), bar_u32 = smem_u32(bars);
     // chunk c of both slices into stage st (warp-uniform operands, one elected lane)
     auto issue = [&](uint32_t st, int c) {
       const int rA = wA - c * kDsU, rB = wB - c * kDsU;
@@ -2198,6 +2200,13 @@ __global__ void __launch_bounds__(kBlock, MINB) spmv_dual_stage_kernel(const Spm
       const uint32_t nB = rB <= 0 ? 0u : rB >= kDsU ? (uint32_t)kDsU : (uint32_t)rB;
       const uint32_t bA = nA * 128u, bB = nB * 128u;
       uint32_t* sA = stages + st * 2 * kDsChunkWords;
+      // steps past a slice's end read as 0 words (no-ops: no cursor move, FMA predicated off),
+      // so every chunk decodes unpredicated; each lane zeroes its own column, the only one it reads
+#pragma unroll
+      for (int u = 0; u < kDsU; ++u) {
+        if ((uint32_t)u >= nA) sA[u * 32 + lane] = 0u;
+        if ((uint32_t)u >= nB) sA[kDsChunkWords + u * 32 + lane] = 0u;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile(
           "{\n .reg .pred e, pa, pb;\n elect.sync _|e, 0xffffffff;\n"
@@ -2205,7 +2214,8 @@ __global__ void __launch_bounds__(kBlock, MINB) spmv_dual_stage_kernel(const Spm
           " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n"
           " @pa cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%6], %2, [%4], %8;\n"
           " @pb cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%1], [%7], %3, [%4], %8;\n}"
-          ::"r"(smem_u32(sA)), "r"(smem_u32(sA + kDsChunkWords)), "r"(bA), "r"(bB), "r"(smem_u32(bars + st)),
+          ::"r"(stage_u32 + st * (2 * kDsChunkWords * 4)), "r"(stage_u32 + st * (2 * kDsChunkWords * 4) + kDsChunkWords * 4),
+            "r"(bA), "r"(bB), "r"(bar_u32 + st * 8u),
           "r"(bA + bB), "l"(pack + oA + c * kDsChunkWords), "l"(pack + oB + c * kDsChunkWords),
           "l"(policy_evict_first())
           : "memory");
@@ -2224,12 +2234,15 @@ __global__ void __launch_bounds__(kBlock, MINB) spmv_dual_stage_kernel(const Spm
     float accA = 0.f, accB = 0.f;
     for (int c = 0; c < nch; ++c) {
       const uint32_t st = (uint32_t)c & 1u;
-      mbar_wait(bars + st, ((uint32_t)c >> 1) & 1u);
+      asm volatile(
+          "{\n .reg .pred p;\n WAIT_%=:\n"
+          " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          " @!p bra WAIT_%=;\n}" ::"r"(bar_u32 + st * 8u), "r"(((uint32_t)c >> 1) & 1u)
+          : "memory");
       const uint32_t* sa = stages + st * 2 * kDsChunkWords + lane;
       const uint32_t* sb = sa + kDsChunkWords;
-      const int rA = wA - c * kDsU, rB = wB - c * kDsU;
       uint32_t xa[kDsU], xb[kDsU];
-      if (rA >= kDsU && rB >= kDsU) {  // full chunk of both slices (warp-uniform): no predicates
+      {  // the stage is zero-padded past each slice's end: no predicates
         uint32_t wa[kDsU], wb[kDsU];
 #pragma unroll
         for (int u = 0; u < kDsU; ++u) {
@@ -2245,17 +2258,6 @@ __global__ void __launch_bounds__(kBlock, MINB) spmv_dual_stage_kernel(const Spm
         for (int u = 0; u < kDsU; ++u) {
           S::fma(wa[u], xa[u], accA, vmask);
           S::fma(wb[u], xb[u], accB, vmask);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kDsU; ++u) {
-          xa[u] = S::gather(u < rA ? sa[u * 32] : 0u, cA, x, m_real);
-          xb[u] = S::gather(u < rB ? sb[u * 32] : 0u, cB, x, m_real);
-        }
-#pragma unroll
-        for (int u = 0; u < kDsU; ++u) {
-          S::fma(u < rA ? sa[u * 32] : 0u, xa[u], accA, vmask);
-          S::fma(u < rB ? sb[u * 32] : 0u, xb[u], accB, vmask);
         }
       }
       __syncwarp();  // every lane has read stage st: refill it two chunks on
