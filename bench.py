@@ -578,6 +578,8 @@ def run_pcg(args, world, rank, comm, peak):
     S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="packsell-e8m14",
                                max_outer=1), backend=be, comm=comm)  # warm-up (graph capture)
     rep, t_io = timed(lambda: S.iocg(A, b, cfg, backend=be, comm=comm))
+    # warm-up of the FP64 PCG's kernels (first launches load their modules lazily)
+    S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=2), comm=comm)
     rep64, t_64 = timed(lambda: S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=5000), comm=comm))
     rep32 = t_32 = None
     if world == 1:  # FP32 IO-CG comparator: SELL-C-sigma f32 inner operator, same protocol
