@@ -341,6 +341,23 @@ PSELL_API int psell_pcg_update_status(int64_t n, double* x, double* r, const dou
                                       double* scal, int32_t* gate, double bnorm, double tol, double* out,
                                       double* partials, unsigned* ticket, void* stream);
 
+/* Fused distributed inner PCG (G ranks joined by the K8 peer arenas, reference
+ * solvers.py:293-306 on a row slab): psell_spmv_dot_alpha / psell_ipcg_update_beta whose
+ * last CTA all-reduces its local FP64 sum over the arenas (push into every peer's dot slot,
+ * system-scope release of the epoch, acquire-wait for every peer, rank-ordered sum) before
+ * the alpha / beta step -- one kernel instead of sum + exchange + scalar kernels.  peers =
+ * device array of the G arena base addresses (rank order); a wait past timeout_ns sets the
+ * arena's error word (psell_peer_error).  With G = 1 they are the single-GPU entry points. */
+PSELL_API int psell_spmv_dot_alpha_peer(const psell_desc* d, const void* pack, const int64_t* offset,
+                                        const void* perm, const float* x, float* y, const float* p_own,
+                                        double* partials, double* scal, int32_t* iflags, unsigned* ticket,
+                                        int32_t flags, int32_t G, int32_t rank, const uint64_t* peers,
+                                        int64_t timeout_ns, void* stream, psell_error* err);
+PSELL_API int psell_ipcg_update_beta_peer(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
+                                          const float* inv_diag, double* scal, int32_t* iflags, double* partials,
+                                          unsigned* ticket, int32_t G, int32_t rank, const uint64_t* peers,
+                                          int64_t timeout_ns, void* stream);
+
 /* FP64 PCG convergence gate (solvers.py:183-207): gate[2] int32 (0 running,
  * 1 breakdown -- pass gate as psell_scalar_div's flag and psell_axpy2's skip
  * flag -- 2 converged; gate[1] = breakdown reported).  out[3] = {breakdown,

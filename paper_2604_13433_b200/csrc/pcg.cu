@@ -175,7 +175,10 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
                                                              const float* __restrict__ inv,
                                                              double* scal, int32_t* iflags,
                                                              double* __restrict__ parts, unsigned* ticket,
-                                                             bool rev = false) {
+                                                             bool rev = false,
+                                                             const unsigned long long* peers = nullptr,
+                                                             int peer_G = 1, int peer_rank = 0,
+                                                             long long peer_timeout = 0) {
   if (iflags[0]) return;
   __shared__ double sh[kBlock / 32];
   const float a = __double2float_rn(scal[2]);
@@ -245,8 +248,10 @@ __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float*
   v = block_sum<kBlock>(v, sh);
   if (threadIdx.x == 0) parts[blockIdx.x] = v;
   double rz_new;  // fused beta (psell_ipcg_update_beta): the last CTA finishes the iteration's scalars
-  if (ticket && last_cta_sum<kBlock>(parts, ticket, rz_new, sh) && threadIdx.x == 0)
+  if (ticket && last_cta_sum<kBlock>(parts, ticket, rz_new, sh) && threadIdx.x == 0) {
+    if (peer_G > 1) rz_new = peer_allreduce1(peer_G, peer_rank, peers, peer_timeout, rz_new);
     ipcg_beta_step(rz_new, scal, iflags);
+  }
 }
 
 // solvers.py:304-306
@@ -639,6 +644,26 @@ int psell_ipcg_update_beta(int64_t n, float* x, float* r, float* z, const float*
                      reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
   if (vec) ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket, upd_rev());
   else ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket);
+  return LAUNCH_OK();
+}
+
+// psell_ipcg_update_beta across G ranks: the last CTA all-reduces r.z over the peer arenas
+// (K8 protocol, one value) before the beta step (reference solvers.py:300-306 on a slab)
+int psell_ipcg_update_beta_peer(int64_t n, float* x, float* r, float* z, const float* p, const float* q,
+                                const float* inv_diag, double* scal, int32_t* iflags, double* partials,
+                                unsigned* ticket, int32_t G, int32_t rank, const uint64_t* peers, int64_t timeout_ns,
+                                void* stream) {
+  if (!ticket || G < 1 || G > kPeerMax || rank < 0 || rank >= G || (G > 1 && !peers)) return PSELL_EARG;
+  cudaStream_t st = as_stream(stream);
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(z) |
+                     reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(inv_diag)) & 15) == 0;
+  const unsigned long long* pp = reinterpret_cast<const unsigned long long*>(peers);
+  if (vec)
+    ipcg_update_kernel<true><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket,
+                                                     upd_rev(), pp, G, rank, timeout_ns);
+  else
+    ipcg_update_kernel<false><<<kRB, kBlock, 0, st>>>(n, x, r, z, p, q, inv_diag, scal, iflags, partials, ticket,
+                                                      false, pp, G, rank, timeout_ns);
   return LAUNCH_OK();
 }
 

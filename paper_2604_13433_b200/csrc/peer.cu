@@ -36,32 +36,6 @@
 
 namespace psell {
 
-constexpr int kPeerMax = 64;
-constexpr int kFlagOff = 0;
-constexpr int kEpochOff = 256;
-constexpr int kTicketOff = 260;
-constexpr int kErrOff = 264;
-constexpr int kGlobOff = 4096;
-
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
-  double v;
-  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kBlock) peer_exchange_kernel(
     int G, int rank, const unsigned long long* __restrict__ peers, long long n_send,

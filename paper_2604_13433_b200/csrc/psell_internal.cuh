@@ -305,6 +305,72 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// ---- peer-memory arena protocol (K8, csrc/peer.cu; layout in include/psell.h)
+constexpr int kPeerMax = 64;
+constexpr int kFlagOff = 0;
+constexpr int kEpochOff = 256;
+constexpr int kTicketOff = 260;
+constexpr int kErrOff = 264;
+constexpr int kGlobOff = 4096;
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The dot all-reduce of the fused distributed inner PCG, run by ONE thread (thread 0 of the
+// last CTA of the kernel that produced this rank's sum): one exchange of the K8 protocol
+// with a single value -- store `local` into every peer's glob[parity][rank][0], fence at
+// system scope, release this rank's epoch into every peer's flag, acquire-wait for every
+// peer's flag, and return the rank-ordered sum (the order the scalar kernels use), so a
+// fused kernel's epilogue replaces the separate partial-sum, exchange and scalar kernels.
+// A wait past timeout_ns sets the arena's error word and returns the partial sum (the
+// host raises on it after the solve).
+__device__ __forceinline__ double peer_allreduce1(int G, int rank, const unsigned long long* peers,
+                                                  long long timeout_ns, double local) {
+  unsigned char* self = reinterpret_cast<unsigned char*>(peers[rank]);
+  uint32_t* flags = reinterpret_cast<uint32_t*>(self + kFlagOff);
+  uint32_t* epoch_p = reinterpret_cast<uint32_t*>(self + kEpochOff);
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch_p) + 1u;
+  const int par = e & 1;
+  for (int p = 0; p < G; ++p) {
+    double* g = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(peers[p]) + kGlobOff);
+    g[(par * kPeerMax + rank) * 8] = local;
+  }
+  __threadfence_system();
+  for (int p = 0; p < G; ++p)
+    st_release_sys(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(peers[p]) + kFlagOff) + rank, e);
+  const unsigned long long t0 = globaltimer();
+  for (int q = 0; q < G; ++q) {
+    unsigned spins = 0;
+    while ((int)(ld_acquire_sys(flags + q) - e) < 0) {
+      if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > timeout_ns) {
+        atomicExch(reinterpret_cast<int*>(self + kErrOff), 1);
+        break;
+      }
+    }
+  }
+  const double* g = reinterpret_cast<const double*>(self + kGlobOff);
+  double s = 0.0;
+  for (int q = 0; q < G; ++q) s += ld_relaxed_sys(g + (par * kPeerMax + q) * 8);
+  *epoch_p = e;
+  return s;
+}
+
 // FP64 PCG scalar steps of the fused iteration (solvers.py:196-207), identity preconditioner.
 // scal: [0]=alpha [1]=pq [2]=beta [4]=rz [10]=pq [12]=rr; gate: see psell_pcg_status
 __device__ __forceinline__ void pcg_alpha_step(double pq, double* scal, int32_t* gate) {

@@ -34,6 +34,11 @@ struct SpmvArgs {
   unsigned* ticket;
   double* scal;
   int32_t* iflags;
+  // ... and, across ranks (psell_spmv_dot_alpha_peer), all-reduces the sum over the
+  // peer-memory arenas before the alpha step (peer_G > 1)
+  const unsigned long long* peers;
+  int peer_G, peer_rank;
+  long long peer_timeout;
   long long n_rows, n_cols, n_slices, row0, k_left;
   int c, se, sigma, mode, d, perm_bytes;
   int variant;  // 0: register-pipelined kernels (default), 2: persistent TMA stream
@@ -192,8 +197,10 @@ __device__ __forceinline__ void finish_dot(const SpmvArgs& a, double v) {
     const double t = block_sum<NT>(v, sh);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = t;
     double pq;
-    if (a.ticket && last_cta_sum<NT>(a.partials, a.ticket, pq, sh) && threadIdx.x == 0)
+    if (a.ticket && last_cta_sum<NT>(a.partials, a.ticket, pq, sh) && threadIdx.x == 0) {
+      if (a.peer_G > 1) pq = peer_allreduce1(a.peer_G, a.peer_rank, a.peers, a.peer_timeout, pq);
       ipcg_alpha_step(pq, a.scal, a.iflags);
+    }
   }
 }
 
@@ -2563,6 +2570,10 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   a.ticket = nullptr;
   a.scal = nullptr;
   a.iflags = nullptr;
+  a.peers = nullptr;
+  a.peer_G = 1;
+  a.peer_rank = 0;
+  a.peer_timeout = 0;
   a.sched = nullptr;
   a.aff_chunks = 0;
   a.n_rows = d->n_rows;
@@ -2945,6 +2956,43 @@ int psell_spmv_dot_alpha(const psell_desc* d, const void* pack, const int64_t* o
     case PSELL_FP32EMBED: launch_spmv<PSELL_FP32EMBED, float, false, true>(a, st); break;
   }
   PSELL_CHECK_LAUNCH(err, "psell_spmv_dot_alpha");
+  return ok(err);
+}
+
+// psell_spmv_dot_alpha across G ranks: the last CTA all-reduces p.q over the peer arenas
+// (K8 protocol, one value) before the alpha step (reference solvers.py:293-299 on a slab)
+int psell_spmv_dot_alpha_peer(const psell_desc* d, const void* pack, const int64_t* offset, const void* perm,
+                              const float* x, float* y, const float* p_own, double* partials, double* scal,
+                              int32_t* iflags, unsigned* ticket, int32_t flags, int32_t G, int32_t rank,
+                              const uint64_t* peers, int64_t timeout_ns, void* stream, psell_error* err) {
+  SpmvArgs a;
+  if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
+  if (!ticket || !scal || !iflags) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "null scalar state");
+  a.narrow = (flags & PSELL_SPMV_NARROW) != 0;
+  a.narrow12 = a.narrow && (flags & PSELL_SPMV_NARROW12) != 0;
+  a.w32 = (flags & PSELL_SPMV_W32) != 0;
+  a.x = x;
+  a.y = y;
+  a.p_own = p_own;
+  a.partials = partials;
+  a.skip = iflags;
+  a.ticket = ticket;
+  a.scal = scal;
+  a.iflags = iflags;
+  if (G < 1 || G > kPeerMax || rank < 0 || rank >= G || (G > 1 && !peers))
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "invalid peer group");
+  a.peers = reinterpret_cast<const unsigned long long*>(peers);
+  a.peer_G = G;
+  a.peer_rank = rank;
+  a.peer_timeout = timeout_ns;
+  cudaStream_t st = as_stream(stream);
+  if (a.n_rows == 0) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "empty operator");
+  switch (d->codec) {
+    case PSELL_FP16: launch_spmv<PSELL_FP16, float, false, true>(a, st); break;
+    case PSELL_E8MY: launch_spmv<PSELL_E8MY, float, false, true>(a, st); break;
+    case PSELL_FP32EMBED: launch_spmv<PSELL_FP32EMBED, float, false, true>(a, st); break;
+  }
+  PSELL_CHECK_LAUNCH(err, "psell_spmv_dot_alpha_peer");
   return ok(err);
 }
 

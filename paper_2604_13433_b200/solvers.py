@@ -367,6 +367,29 @@ class _InnerPCG:
                                            d.p(d.scal), d.p(d.flags), st)
             lib.psell_ipcg_end(self.n, self.x.data_ptr(), z64.data_ptr(), st)
             return
+        if self.peer is not None and os.environ.get("PSELL_PEER_FUSED", "1") != "0":
+            # G ranks over the peer arenas: the halo push (K8) and the single-GPU iteration's
+            # three kernels, the SpMV's and the update's last CTAs all-reducing their dot
+            # sums over the arenas before the alpha / beta steps -- 4 launches per iteration
+            pe = self.peer
+            peers = pe.d_peers.data_ptr()
+            for _ in range(self.m_in):
+                _gather_full(self.comm, self.p, self.p_full, self.halo, self.peer, self.row0)
+                rc = lib.psell_spmv_dot_alpha_peer(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
+                                                   self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
+                                                   d.p(d.partials), d.p(d.scal), d.p(d.flags), d.p(d.ticket, 0),
+                                                   M.spmv_flags(), pe.G, pe.rank, peers, pe.timeout_ns, st, err)
+                L.check(rc, err, M.fmt)
+                rc = lib.psell_ipcg_update_beta_peer(self.n, None, self.r.data_ptr(), self.z.data_ptr(),
+                                                     self.p.data_ptr(), self.q.data_ptr(), inv, d.p(d.scal),
+                                                     d.p(d.flags), d.p(d.partials), d.p(d.ticket, d.tstride), pe.G,
+                                                     pe.rank, peers, pe.timeout_ns, st)
+                if rc:
+                    raise L.LibpsellError(f"psell_ipcg_update_beta_peer failed ({rc})")
+                lib.psell_ipcg_direction_x(self.n, self.p.data_ptr(), self.z.data_ptr(), self.x.data_ptr(),
+                                           d.p(d.scal), d.p(d.flags), st)
+            lib.psell_ipcg_end(self.n, self.x.data_ptr(), z64.data_ptr(), st)
+            return
         for _ in range(self.m_in):
             _gather_full(self.comm, self.p, self.p_full, self.halo, self.peer, self.row0)
             rc = lib.psell_spmv_dot(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),

@@ -114,8 +114,11 @@ def _rank_peer(rank, world, port, nx, slabs, q):
         b, _ = S.make_rhs_and_x0(n, 42)
         cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200)
         out = {}
-        for xport in ("nccl", "peer"):   # "nccl" = the torch.distributed collectives (gloo here)
-            os.environ["PSELL_XPORT"] = xport
+        # "nccl" = the torch.distributed collectives (gloo here); "peer0" = the peer transport
+        # with separate exchange kernels; "peer" = the fused dot all-reduces (default)
+        for xport in ("nccl", "peer0", "peer"):
+            os.environ["PSELL_XPORT"] = "nccl" if xport == "nccl" else "peer"
+            os.environ["PSELL_PEER_FUSED"] = "0" if xport == "peer0" else "1"
             A = P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1)
             kl = comm.allreduce_max(lower_bandwidth(A))
             be = S.make_backend(A, "packsell-e8m14", k_left=kl)
@@ -138,8 +141,11 @@ def _rank_peer(rank, world, port, nx, slabs, q):
 
 @pytest.mark.parametrize("split", ["equal", "unequal"])
 def test_peer_transport_matches_collectives_and_single_gpu(split):
-    """2 ranks on one GPU: the peer-memory path (graph-captured distributed inner loop)
-    gives the same x bit for bit as the collective path, on equal and unequal slabs."""
+    """2 ranks on one GPU: the peer-memory path with separate exchange kernels gives the
+    same x bit for bit as the collective path, on equal and unequal slabs; the fused path
+    (dot sums all-reduced over the arenas by the SpMV's and the update's last CTAs, 4
+    launches per inner iteration) the same solve up to the association of the local dot
+    sums (its last-CTA tree), deterministic across graph replays."""
     import torch.multiprocessing as mp
     import paper_2604_13433_b200 as P
     from paper_2604_13433_b200 import solvers as S
@@ -163,14 +169,17 @@ def test_peer_transport_matches_collectives_and_single_gpu(split):
     x, xp = np.zeros(n), np.zeros(n)
     for rank, r0, r1, out in res:
         cg = out["nccl"]
-        pe = out["peer"]
-        assert pe[9] and pe[10], "peer transport + CUDA graph not used"
+        pe = out["peer0"]
+        fu = out["peer"]
+        assert pe[9] and pe[10] and fu[9] and fu[10], "peer transport + CUDA graph not used"
         assert not cg[10]
         assert pe[0] and pe[1] == cg[1] and pe[2] == cg[2] and pe[3] < 1e-9
         assert np.array_equal(pe[4], cg[4]) and np.array_equal(pe[5], pe[4])
         assert pe[6] and pe[7] == cg[7] and np.array_equal(pe[8], cg[8])
         assert abs(pe[1] - ref.outer_iters) <= 1
-        x[r0:r1] = pe[4]
+        assert fu[0] and abs(fu[1] - pe[1]) <= 1 and fu[3] < 1e-9 and np.array_equal(fu[5], fu[4])
+        assert np.abs(fu[4] - pe[4]).max() <= 1e-6 * np.abs(pe[4]).max()
+        x[r0:r1] = fu[4]
         xp[r0:r1] = pe[8]
     assert np.abs(x - ref.x).max() / np.abs(ref.x).max() < 1e-6
     assert np.abs(xp - refp.x).max() / np.abs(refp.x).max() < 1e-9
