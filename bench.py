@@ -620,9 +620,12 @@ def run_pcg(args, world, rank, comm, peak):
         "speedup_iocg_vs_fp32_sell_iocg": None if t_32 is None else t_32 / t_io,
         "build_s": t_build,
         "collectives": "none" if world == 1 else (
-            "peer-memory transport (K8, csrc/peer.cu): one kernel per exchange pushes the halo of p (f32 inner, "
-            "f64 outer) into the peers' vectors over NVLink and all-gathers the FP64 per-rank dot sums "
-            "(rank-ordered sums); the distributed inner iteration is one CUDA graph per outer step"
+            "peer-memory transport (K8, csrc/peer.cu): one kernel per halo exchange pushes p's halo (f32 inner, "
+            "f64 outer) into the peers' vectors over NVLink; the inner iteration's two FP64 dot all-reduces run in "
+            "the last CTA of the SpMV and of the r update (push to every peer's arena, flag, rank-ordered sum; "
+            + ("fused, 4 launches per inner iteration" if os.environ.get("PSELL_PEER_FUSED", "1") != "0"
+               else "PSELL_PEER_FUSED=0: separate exchange kernels, 9 launches per inner iteration")
+            + "); the distributed inner iteration is one CUDA graph per outer step"
             if comm.peer(n) is not None else
             "torch.distributed: point-to-point halo exchange of p (K7 pack/unpack, dist.Halo) + all-gather of the "
             "FP64 per-rank dot sums (rank-ordered), eager"),
