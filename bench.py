@@ -623,7 +623,8 @@ def run_pcg(args, world, rank, comm, peak):
             "peer-memory transport (K8, csrc/peer.cu): one kernel per halo exchange pushes p's halo (f32 inner, "
             "f64 outer) into the peers' vectors over NVLink; the inner iteration's two FP64 dot all-reduces run in "
             "the last CTA of the SpMV and of the r update (push to every peer's arena, flag, rank-ordered sum; "
-            + ("fused, 4 launches per inner iteration" if os.environ.get("PSELL_PEER_FUSED", "1") != "0"
+            + ("fused; the halo pushed by the direction kernel: 3 launches per inner iteration"
+               if os.environ.get("PSELL_PEER_FUSED", "1") != "0"
                else "PSELL_PEER_FUSED=0: separate exchange kernels, 9 launches per inner iteration")
             + "); the distributed inner iteration is one CUDA graph per outer step"
             if comm.peer(n) is not None else

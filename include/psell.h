@@ -358,6 +358,15 @@ PSELL_API int psell_ipcg_update_beta_peer(int64_t n, float* x, float* r, float* 
                                           unsigned* ticket, int32_t G, int32_t rank, const uint64_t* peers,
                                           int64_t timeout_ns, void* stream);
 
+/* psell_ipcg_direction_x across G ranks with the halo push fused in: the rows listed as up
+ * to 2 contiguous local ranges [lo[k], hi[k]) owed to rank dst[k] are stored into that
+ * peer's arena vector (vec_off, global position row0 + row) as they are computed, and the
+ * last CTA runs the K8 signal / wait -- the next SpMV's halo has arrived when it returns. */
+PSELL_API int psell_ipcg_direction_x_push(int64_t n, float* p, const float* z, float* x, const double* scal,
+                                          const int32_t* iflags, int32_t G, int32_t rank, const uint64_t* peers,
+                                          int64_t row0, int64_t vec_off, int32_t n_ranges, const int64_t* lo,
+                                          const int64_t* hi, const int32_t* dst, int64_t timeout_ns, void* stream);
+
 /* FP64 PCG convergence gate (solvers.py:183-207): gate[2] int32 (0 running,
  * 1 breakdown -- pass gate as psell_scalar_div's flag and psell_axpy2's skip
  * flag -- 2 converged; gate[1] = breakdown reported).  out[3] = {breakdown,

@@ -98,6 +98,8 @@ _SIGS = {
     "psell_ipcg_update_beta": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psell_spmv_dot_alpha_peer": (c_int32, [_D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, c_int32, c_int32,
                                             _P, c_int64, _P, _E]),
+    "psell_ipcg_direction_x_push": (c_int32, [c_int64, _P, _P, _P, _P, _P, c_int32, c_int32, _P, c_int64, c_int64,
+                                              c_int32, _P, _P, _P, c_int64, _P]),
     "psell_ipcg_update_beta_peer": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int32, c_int32, _P,
                                               c_int64, _P]),
     "psell_ipcg_direction_x": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P]),

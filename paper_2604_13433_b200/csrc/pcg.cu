@@ -168,6 +168,111 @@ __global__ void __launch_bounds__(kBlock) ipcg_direction_x_kernel(long long n, f
   }
 }
 
+// The distributed direction pass with the halo push fused in (peer transport): the same
+// x += alpha p_old; p = z + beta p_old as ipcg_direction_x_kernel, and every row a peer's
+// slab reads (up to kHaloRanges contiguous local ranges, each owed to one peer) is stored
+// straight into that peer's full vector in its arena as soon as it is computed; the last
+// CTA then runs the K8 signal / wait (system-scope fence, epoch released into every peer's
+// flag, acquire-wait for every peer), so when this kernel ends every peer's halo of the
+// next SpMV has arrived -- the halo exchange costs no kernel of its own.
+constexpr int kHaloRanges = 2;
+struct HaloRanges {
+  long long lo[kHaloRanges], hi[kHaloRanges];
+  int dst[kHaloRanges];
+  int n;
+};
+
+__global__ void __launch_bounds__(kBlock) ipcg_direction_x_push_kernel(long long n, float* __restrict__ p,
+                                                                       const float* __restrict__ z,
+                                                                       float* __restrict__ x,
+                                                                       const double* __restrict__ scal,
+                                                                       const int32_t* __restrict__ iflags, bool rev,
+                                                                       const unsigned long long* __restrict__ peers,
+                                                                       int G, int rank, long long row0,
+                                                                       long long vec_off, HaloRanges hr,
+                                                                       long long timeout_ns) {
+  if (iflags[0]) return;  // breakdown / closed gate: every rank skips alike (global scalars)
+  const float al = __double2float_rn(scal[2]);
+  const float b = __double2float_rn(scal[3]);
+  const long long gt = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gs = (long long)gridDim.x * kBlock;
+  auto owed = [&](long long i0, long long i1) {  // does [i0, i1) meet a halo range?
+    bool m = false;
+#pragma unroll
+    for (int k = 0; k < kHaloRanges; ++k) m |= k < hr.n && i0 < hr.hi[k] && i1 > hr.lo[k];
+    return m;
+  };
+  auto push = [&](long long i, float v) {
+#pragma unroll
+    for (int k = 0; k < kHaloRanges; ++k)
+      if (k < hr.n && i >= hr.lo[k] && i < hr.hi[k])
+        reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(peers[hr.dst[k]]) + vec_off)[row0 + i] = v;
+  };
+  long long done = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(z) |
+                     reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  if (vec) {
+    const long long n4 = n >> 2;
+    for (long long k4 = gt; k4 < n4; k4 += gs) {
+      const long long i4 = rev ? n4 - 1 - k4 : k4;
+      float4 pv = reinterpret_cast<float4*>(p)[i4];
+      float4 xv = reinterpret_cast<float4*>(x)[i4];
+      const float4 zv = reinterpret_cast<const float4*>(z)[i4];
+      xv.x = __fadd_rn(xv.x, __fmul_rn(al, pv.x));
+      xv.y = __fadd_rn(xv.y, __fmul_rn(al, pv.y));
+      xv.z = __fadd_rn(xv.z, __fmul_rn(al, pv.z));
+      xv.w = __fadd_rn(xv.w, __fmul_rn(al, pv.w));
+      pv.x = __fadd_rn(zv.x, __fmul_rn(b, pv.x));
+      pv.y = __fadd_rn(zv.y, __fmul_rn(b, pv.y));
+      pv.z = __fadd_rn(zv.z, __fmul_rn(b, pv.z));
+      pv.w = __fadd_rn(zv.w, __fmul_rn(b, pv.w));
+      reinterpret_cast<float4*>(x)[i4] = xv;
+      reinterpret_cast<float4*>(p)[i4] = pv;
+      if (owed(4 * i4, 4 * i4 + 4)) {
+        push(4 * i4, pv.x);
+        push(4 * i4 + 1, pv.y);
+        push(4 * i4 + 2, pv.z);
+        push(4 * i4 + 3, pv.w);
+      }
+    }
+    done = n4 * 4;
+  }
+  for (long long i = done + gt; i < n; i += gs) {
+    const float pv = p[i];
+    x[i] = __fadd_rn(x[i], __fmul_rn(al, pv));
+    const float pn = __fadd_rn(z[i], __fmul_rn(b, pv));
+    p[i] = pn;
+    push(i, pn);
+  }
+  // signal / wait: this rank's halo pushes are complete toward every peer
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  unsigned char* self = reinterpret_cast<unsigned char*>(peers[rank]);
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(self + kTicketOff);
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence_system();
+  *ticket = 0u;
+  uint32_t* flags = reinterpret_cast<uint32_t*>(self + kFlagOff);
+  uint32_t* epoch_p = reinterpret_cast<uint32_t*>(self + kEpochOff);
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(epoch_p) + 1u;
+  for (int q = 0; q < G; ++q)
+    st_release_sys(reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(peers[q]) + kFlagOff) + rank, e);
+  const unsigned long long t0 = globaltimer();
+  for (int q = 0; q < G; ++q) {
+    unsigned spins = 0;
+    while ((int)(ld_acquire_sys(flags + q) - e) < 0) {
+      if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > timeout_ns) {
+        atomicExch(reinterpret_cast<int*>(self + kErrOff), 1);
+        break;
+      }
+    }
+  }
+  *epoch_p = e;
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(kBlock) ipcg_update_kernel(long long n, float* __restrict__ x, float* r,
                                                              float* z, const float* __restrict__ p,
@@ -681,6 +786,27 @@ int psell_ipcg_direction(int64_t n, float* p, const float* z, const double* scal
 int psell_ipcg_direction_x(int64_t n, float* p, const float* z, float* x, const double* scal,
                            const int32_t* iflags, void* stream) {
   ipcg_direction_x_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(n, p, z, x, scal, iflags, dir_rev());
+  return LAUNCH_OK();
+}
+
+int psell_ipcg_direction_x_push(int64_t n, float* p, const float* z, float* x, const double* scal,
+                                const int32_t* iflags, int32_t G, int32_t rank, const uint64_t* peers, int64_t row0,
+                                int64_t vec_off, int32_t n_ranges, const int64_t* lo, const int64_t* hi,
+                                const int32_t* dst, int64_t timeout_ns, void* stream) {
+  if (G < 2 || G > kPeerMax || rank < 0 || rank >= G || !peers || n_ranges < 0 || n_ranges > kHaloRanges ||
+      (n_ranges > 0 && (!lo || !hi || !dst)))
+    return PSELL_EARG;
+  HaloRanges hr;
+  hr.n = n_ranges;
+  for (int k = 0; k < kHaloRanges; ++k) {
+    hr.lo[k] = k < n_ranges ? lo[k] : 0;
+    hr.hi[k] = k < n_ranges ? hi[k] : 0;
+    hr.dst[k] = k < n_ranges ? dst[k] : 0;
+    if (k < n_ranges && (dst[k] < 0 || dst[k] >= G || dst[k] == rank)) return PSELL_EARG;
+  }
+  ipcg_direction_x_push_kernel<<<vgrid(n) * 2, kBlock, 0, as_stream(stream)>>>(
+      n, p, z, x, scal, iflags, dir_rev(), reinterpret_cast<const unsigned long long*>(peers), G, rank, row0, vec_off,
+      hr, timeout_ns);
   return LAUNCH_OK();
 }
 

@@ -173,6 +173,26 @@ class PeerTransport:
             self._plans[key] = (torch.as_tensor(dst).cuda(), torch.as_tensor(loc).cuda(), int(row0), len(dst))
         return self._plans[key]
 
+    def ranges(self, halo: "Halo", n_local: int):
+        """The push list as at most 2 contiguous local row ranges, each owed to one peer
+        ((lo, hi, dst) host tuples; stencil slabs: the first / last boundary planes), or
+        None when it does not decompose so (irregular halos, all-gather fallback): the
+        direction kernel can then push it itself (psell_ipcg_direction_x_push)."""
+        key = ("ranges", None if halo is None else id(halo))
+        if key not in self._plans:
+            dst, loc = push_lists(halo, self.rank, self.G, n_local)
+            out = []
+            for q in np.unique(dst):
+                li = np.sort(loc[dst == q].astype(np.int64))
+                if len(li) == 0:
+                    continue
+                if li[-1] - li[0] + 1 != len(li) or len(np.unique(li)) != len(li):
+                    out = None
+                    break
+                out.append((int(li[0]), int(li[-1]) + 1, int(q)))
+            self._plans[key] = out if out is not None and len(out) <= 2 else None
+        return self._plans[key]
+
     def exchange(self, local=None, plan=None, loc=None, n_loc: int = 0, out=None):
         """Push `local`'s planned entries and loc[:n_loc], wait for all ranks, out <- dot sums."""
         from . import _lib

@@ -373,8 +373,19 @@ class _InnerPCG:
             # sums over the arenas before the alpha / beta steps -- 4 launches per iteration
             pe = self.peer
             peers = pe.d_peers.data_ptr()
-            for _ in range(self.m_in):
+            # the halo of p: pushed by K8 before the first SpMV, then by each iteration's direction
+            # kernel itself when the push list is <= 2 contiguous ranges (stencil slabs)
+            rg = pe.ranges(self.halo, self.n) if os.environ.get("PSELL_PEER_HALO_FUSED", "1") != "0" else None
+            if rg is not None:
+                import ctypes
+                k = len(rg)
+                lo = (ctypes.c_int64 * 2)(*[r[0] for r in rg], *([0] * (2 - k)))
+                hi = (ctypes.c_int64 * 2)(*[r[1] for r in rg], *([0] * (2 - k)))
+                dst = (ctypes.c_int32 * 2)(*[r[2] for r in rg], *([0] * (2 - k)))
                 _gather_full(self.comm, self.p, self.p_full, self.halo, self.peer, self.row0)
+            for it in range(self.m_in):
+                if rg is None:
+                    _gather_full(self.comm, self.p, self.p_full, self.halo, self.peer, self.row0)
                 rc = lib.psell_spmv_dot_alpha_peer(self.desc, L.ptr(M.d_pack), L.ptr(M.d_offset), L.ptr(M.d_perm),
                                                    self.p_full.data_ptr(), self.q.data_ptr(), self.p.data_ptr(),
                                                    d.p(d.partials), d.p(d.scal), d.p(d.flags), d.p(d.ticket, 0),
@@ -386,8 +397,16 @@ class _InnerPCG:
                                                      pe.rank, peers, pe.timeout_ns, st)
                 if rc:
                     raise L.LibpsellError(f"psell_ipcg_update_beta_peer failed ({rc})")
-                lib.psell_ipcg_direction_x(self.n, self.p.data_ptr(), self.z.data_ptr(), self.x.data_ptr(),
-                                           d.p(d.scal), d.p(d.flags), st)
+                if rg is not None and it + 1 < self.m_in:
+                    rc = lib.psell_ipcg_direction_x_push(self.n, self.p.data_ptr(), self.z.data_ptr(),
+                                                         self.x.data_ptr(), d.p(d.scal), d.p(d.flags), pe.G, pe.rank,
+                                                         peers, self.row0, pe.vec_off[4], k, lo, hi, dst,
+                                                         pe.timeout_ns, st)
+                    if rc:
+                        raise L.LibpsellError(f"psell_ipcg_direction_x_push failed ({rc})")
+                else:
+                    lib.psell_ipcg_direction_x(self.n, self.p.data_ptr(), self.z.data_ptr(), self.x.data_ptr(),
+                                               d.p(d.scal), d.p(d.flags), st)
             lib.psell_ipcg_end(self.n, self.x.data_ptr(), z64.data_ptr(), st)
             return
         for _ in range(self.m_in):

@@ -116,9 +116,11 @@ def _rank_peer(rank, world, port, nx, slabs, q):
         out = {}
         # "nccl" = the torch.distributed collectives (gloo here); "peer0" = the peer transport
         # with separate exchange kernels; "peer" = the fused dot all-reduces (default)
-        for xport in ("nccl", "peer0", "peer"):
+        # "peer1" = fused dot all-reduces with the halo still pushed by its own K8 kernel
+        for xport in ("nccl", "peer0", "peer1", "peer"):
             os.environ["PSELL_XPORT"] = "nccl" if xport == "nccl" else "peer"
             os.environ["PSELL_PEER_FUSED"] = "0" if xport == "peer0" else "1"
+            os.environ["PSELL_PEER_HALO_FUSED"] = "0" if xport == "peer1" else "1"
             A = P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1)
             kl = comm.allreduce_max(lower_bandwidth(A))
             be = S.make_backend(A, "packsell-e8m14", k_left=kl)
@@ -128,7 +130,8 @@ def _rank_peer(rank, world, port, nx, slabs, q):
             pc = S.pcg(P.stencil_device("poisson3d", nx, scale="sym", row_begin=r0, row_end=r1), b[r0:r1],
                        S.SolveConfig(tol=1e-9, max_outer=2000), comm=comm)
             out[xport] = (rep.converged, rep.outer_iters, rep.total_inner_iters, rep.final_true_relres, rep.x,
-                          rep2.x, pc.converged, pc.outer_iters, pc.x, inner.use_graph, inner.peer is not None)
+                          rep2.x, pc.converged, pc.outer_iters, pc.x, inner.use_graph, inner.peer is not None,
+                          inner.peer is not None and inner.peer.ranges(inner.halo, inner.n) is not None)
         comm.close()
         q.put((rank, r0, r1, out))
     except Exception as e:  # noqa: BLE001
@@ -143,9 +146,10 @@ def _rank_peer(rank, world, port, nx, slabs, q):
 def test_peer_transport_matches_collectives_and_single_gpu(split):
     """2 ranks on one GPU: the peer-memory path with separate exchange kernels gives the
     same x bit for bit as the collective path, on equal and unequal slabs; the fused path
-    (dot sums all-reduced over the arenas by the SpMV's and the update's last CTAs, 4
-    launches per inner iteration) the same solve up to the association of the local dot
-    sums (its last-CTA tree), deterministic across graph replays."""
+    (dot sums all-reduced over the arenas by the SpMV's and the update's last CTAs, the
+    halo pushed by the direction kernel: 3 launches per inner iteration) the same solve up
+    to the association of the local dot sums (its last-CTA tree), deterministic across
+    graph replays, and bitwise the same with the halo pushed by a separate K8 kernel."""
     import torch.multiprocessing as mp
     import paper_2604_13433_b200 as P
     from paper_2604_13433_b200 import solvers as S
@@ -178,6 +182,10 @@ def test_peer_transport_matches_collectives_and_single_gpu(split):
         assert pe[6] and pe[7] == cg[7] and np.array_equal(pe[8], cg[8])
         assert abs(pe[1] - ref.outer_iters) <= 1
         assert fu[0] and abs(fu[1] - pe[1]) <= 1 and fu[3] < 1e-9 and np.array_equal(fu[5], fu[4])
+        # the halo pushed by the direction kernel itself: the same values as its K8 push
+        f1 = out["peer1"]
+        assert fu[11], "the halo push list did not reduce to contiguous ranges"
+        assert (f1[1], f1[2]) == (fu[1], fu[2]) and np.array_equal(f1[4], fu[4])
         assert np.abs(fu[4] - pe[4]).max() <= 1e-6 * np.abs(pe[4]).max()
         x[r0:r1] = fu[4]
         xp[r0:r1] = pe[8]
