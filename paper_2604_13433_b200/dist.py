@@ -180,17 +180,7 @@ class PeerTransport:
         direction kernel can then push it itself (psell_ipcg_direction_x_push)."""
         key = ("ranges", None if halo is None else id(halo))
         if key not in self._plans:
-            dst, loc = push_lists(halo, self.rank, self.G, n_local)
-            out = []
-            for q in np.unique(dst):
-                li = np.sort(loc[dst == q].astype(np.int64))
-                if len(li) == 0:
-                    continue
-                if li[-1] - li[0] + 1 != len(li) or len(np.unique(li)) != len(li):
-                    out = None
-                    break
-                out.append((int(li[0]), int(li[-1]) + 1, int(q)))
-            self._plans[key] = out if out is not None and len(out) <= 2 else None
+            self._plans[key] = push_ranges(*push_lists(halo, self.rank, self.G, n_local))
         return self._plans[key]
 
     def exchange(self, local=None, plan=None, loc=None, n_loc: int = 0, out=None):
@@ -348,6 +338,24 @@ def push_lists(halo, rank: int, world: int, n_local: int):
     peers = [s for s in range(world) if s != rank]
     return (np.repeat(np.asarray(peers, np.int32), n_local),
             np.tile(np.arange(n_local, dtype=np.int32), len(peers)))
+
+
+def push_ranges(dst, loc, max_ranges: int = 2):
+    """A push list (destination rank, local row) as contiguous local row ranges, one per
+    destination: [(lo, hi, dst), ...] sorted by destination, or None when some destination's
+    rows are not one contiguous duplicate-free range or there are more than `max_ranges`
+    destinations (the fused halo push of psell_ipcg_direction_x_push then does not apply)."""
+    dst = np.asarray(dst)
+    loc = np.asarray(loc, dtype=np.int64)
+    out = []
+    for q in np.unique(dst):
+        li = np.sort(loc[dst == q])
+        if len(li) == 0:
+            continue
+        if li[-1] - li[0] + 1 != len(li) or np.any(np.diff(li) == 0):
+            return None
+        out.append((int(li[0]), int(li[-1]) + 1, int(q)))
+    return out if len(out) <= max_ranges else None
 
 
 def equal_row_slabs(n: int, world: int, sigma: int) -> List[Tuple[int, int]]:

@@ -176,7 +176,23 @@ def _push_worker(rank, world, port, slabs, use_halo, q):
             full[g_[sel]] = v_[sel]
         need = np.unique(cols)
         ok = bool(np.array_equal(full[need], need * 0.25 + 3.0))
-        q.put((rank, ok, int(len(dst)), None if h is None else h.volume))
+        # the same pushes as contiguous ranges (the direction kernel's fused halo push)
+        rg = D.push_ranges(dst, loc)
+        ok_rg = None
+        if rg is not None:
+            pushed = [None] * world
+            dist.all_gather_object(pushed, rg)
+            full_r = np.zeros(n)
+            full_r[r0:r1] = np.arange(r0, r1) * 0.25 + 3.0
+            for src, rgs in enumerate(pushed):
+                for lo, hi, d_ in rgs:
+                    if d_ == rank:
+                        g = slabs[src][0] + np.arange(lo, hi)
+                        full_r[g] = g * 0.25 + 3.0
+            ok_rg = bool(np.array_equal(full_r[need], need * 0.25 + 3.0))
+        else:
+            dist.all_gather_object([None] * world, None)
+        q.put((rank, ok and ok_rg is not False, int(len(dst)), None if h is None else h.volume, rg))
     finally:
         dist.destroy_process_group()
 
@@ -196,9 +212,21 @@ def test_peer_push_lists_cover_every_read_column(world, slabs, use_halo):
     res = sorted(q.get(timeout=120) for _ in ps)
     for p in ps:
         p.join(timeout=60)
-    assert all(ok for _, ok, _, _ in res), res
+    assert all(ok for _, ok, _, _, _ in res), res
     if not use_halo:
-        assert [k for _, _, k, _ in res] == [(b - a) * (world - 1) for a, b in slabs]
+        assert [k for _, _, k, _, _ in res] == [(b - a) * (world - 1) for a, b in slabs]
+    # stencil slabs: every rank's pushes are <= 2 contiguous ranges (boundary planes, or the
+    # whole slab to each of the other two ranks), so the direction kernel can push them
+    assert all(rg is not None and len(rg) <= 2 for _, _, _, _, rg in res), res
+
+
+def test_push_ranges():
+    assert D.push_ranges(np.array([1, 1, 1], np.int32), np.array([4, 5, 6], np.int32)) == [(4, 7, 1)]
+    assert D.push_ranges(np.array([2, 0, 2, 0], np.int32), np.array([9, 0, 8, 1], np.int32)) == [(0, 2, 0), (8, 10, 2)]
+    assert D.push_ranges(np.array([1, 1], np.int32), np.array([4, 6], np.int32)) is None        # gap
+    assert D.push_ranges(np.array([1, 1], np.int32), np.array([4, 4], np.int32)) is None        # duplicate
+    assert D.push_ranges(np.array([0, 1, 2], np.int32), np.array([0, 0, 0], np.int32)) is None  # 3 destinations
+    assert D.push_ranges(np.zeros(0, np.int32), np.zeros(0, np.int32)) == []
 
 
 def _slab_check_worker(rank, world, port, q):
