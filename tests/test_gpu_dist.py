@@ -142,7 +142,7 @@ def _rank_peer(rank, world, port, nx, slabs, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("split", ["equal", "unequal"])
+@pytest.mark.parametrize("split", ["equal", "unequal", "three"])
 def test_peer_transport_matches_collectives_and_single_gpu(split):
     """2 ranks on one GPU: the peer-memory path with separate exchange kernels gives the
     same x bit for bit as the collective path, on equal and unequal slabs; the fused path
@@ -153,9 +153,11 @@ def test_peer_transport_matches_collectives_and_single_gpu(split):
     import torch.multiprocessing as mp
     import paper_2604_13433_b200 as P
     from paper_2604_13433_b200 import solvers as S
-    nx, world = 16, 2
+    nx = 16
     n = nx ** 3
-    slabs = [(0, n // 2), (n // 2, n)] if split == "equal" else [(0, 1280), (1280, n)]
+    world = 3 if split == "three" else 2   # three ranks: the middle one pushes two halo ranges
+    slabs = {"equal": [(0, n // 2), (n // 2, n)], "unequal": [(0, 1280), (1280, n)],
+             "three": [(0, 1280), (1280, 2560), (2560, n)]}[split]
     A = P.sym_diag_scale(P.poisson3d(nx))
     b, _ = S.make_rhs_and_x0(n, 42)
     ref = S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=20, a_backend="packsell-e8m14", max_outer=200))
