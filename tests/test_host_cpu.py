@@ -235,3 +235,40 @@ def test_powerlaw_far_rows_properties():
     assert kl == powerlaw_far_k_left(n, 9) and kl > n - 4096
     B = powerlaw_far_rows(n, 9, 1000, 3000)
     assert np.array_equal(B.col_idx, ci[rp[1000]:rp[3000]]) and np.array_equal(B.values, A.values[rp[1000]:rp[3000]])
+
+
+def test_fused_peer_entry_points_validate_before_launch():
+    """The fused distributed entry points refuse a bad peer group on the host (no launch,
+    no CUDA call): ranks out of range, G outside [1, 64] (or < 2 for the halo push), missing
+    arena table or halo ranges."""
+    import ctypes
+    l = _lib.load(require_gpu=False)
+    EARG = 4
+    lo = (ctypes.c_int64 * 2)(0, 0)
+    hi = (ctypes.c_int64 * 2)(4, 0)
+    dst = (ctypes.c_int32 * 2)(1, 0)
+    fake = ctypes.c_void_p(16)  # never dereferenced: validation fails first
+    # halo push: G must be >= 2, rank in range, peers non-null, <= 2 ranges, dst a peer
+    assert l.psell_ipcg_direction_x_push(8, fake, fake, fake, fake, fake, 1, 0, fake, 0, 0, 1, lo, hi, dst, 1, None) == EARG
+    assert l.psell_ipcg_direction_x_push(8, fake, fake, fake, fake, fake, 2, 2, fake, 0, 0, 1, lo, hi, dst, 1, None) == EARG
+    assert l.psell_ipcg_direction_x_push(8, fake, fake, fake, fake, fake, 2, 0, None, 0, 0, 1, lo, hi, dst, 1, None) == EARG
+    assert l.psell_ipcg_direction_x_push(8, fake, fake, fake, fake, fake, 2, 0, fake, 0, 0, 3, lo, hi, dst, 1, None) == EARG
+    assert l.psell_ipcg_direction_x_push(8, fake, fake, fake, fake, fake, 2, 1, fake, 0, 0, 1, lo, hi, dst, 1, None) == EARG
+    # the fused dot all-reduce of the update: same group checks
+    assert l.psell_ipcg_update_beta_peer(8, None, fake, fake, fake, fake, None, fake, fake, fake, fake,
+                                         65, 0, fake, 1, None) == EARG
+    assert l.psell_ipcg_update_beta_peer(8, None, fake, fake, fake, fake, None, fake, fake, fake, fake,
+                                         2, 0, None, 1, None) == EARG
+    assert l.psell_ipcg_update_beta_peer(8, None, fake, fake, fake, fake, None, fake, fake, fake, None,
+                                         2, 0, fake, 1, None) == EARG
+    # the FP64 PCG fused entry points: missing scalars / gate / ticket
+    assert l.psell_pcg_update_status(8, fake, fake, fake, fake, None, fake, 1.0, 1e-9, fake, fake, fake, None) == EARG
+    err = _lib.PsellError()
+    assert l.psell_csr_spmv_dot_alpha(8, fake, fake, fake, fake, fake, fake, fake, None, fake, fake, None,
+                                      ctypes.byref(err)) == EARG
+    d = _lib.PsellDesc()
+    d.w, d.d, d.codec, d.c, d.sigma, d.mode = 32, 8, 1, 32, 256, 2
+    d.n_rows, d.n_cols, d.row0, d.k_left, d.nnz = 4096, 4096, 0, 256, 28672
+    for G, rank, peers in ((0, 0, fake), (2, 2, fake), (2, 0, None), (65, 0, fake)):
+        assert l.psell_spmv_dot_alpha_peer(d, fake, fake, fake, fake, fake, fake, fake, fake, fake, fake, 4, G, rank,
+                                           peers, 1, None, ctypes.byref(err)) == EARG, (G, rank)
