@@ -707,6 +707,9 @@ def seg_launches(seg, kernel_name):
     PSELL_SEGMERGE=0 splits them into their own launch; a combine kernel adds them up."""
     if seg is None:
         return 1, kernel_name
+    if os.environ.get("PSELL_DSTATIC", "1") != "0" and os.environ.get("PSELL_AFF", "0") == "0":
+        return 1 + (seg["n_long"] > 0), ("spmv_dual_static_kernel (one CTA per SM: its segments, then a "
+                                         "contiguous word-balanced range of short-slice pairs) + seg_combine_kernel")
     merged = seg["n_seg"] > 0 and os.environ.get("PSELL_SEGMERGE", "1") != "0"
     if merged:
         return 1 + (seg["n_long"] > 0), "spmv_dual_seg_kernel (segments + short slices in one grid) + seg_combine_kernel"

@@ -54,6 +54,7 @@ struct SpmvArgs {
   // (A/B).  Prefetching the next pair in the persistent pair kernel was measured
   // slower (7-point 166 -> 180-187 us) and is not implemented.
   int l2pf;
+  int sched_static;  // sched holds the static pair ranges behind the counters (PSELL_DSTATIC)
   const int32_t* seg_slice;   // [n_seg] slice of each segment
   const int32_t* seg_q0;      // [n_seg] first step of each segment
   uint32_t* seg_c2;           // [n_seg][32] cursor checkpoints (2 * column)
@@ -631,7 +632,8 @@ __device__ __forceinline__ void aff_exit(const SpmvArgs& a) {
 
 // the dual kernel's body for CTA `bid` of its grid (spmv_dual_seg_kernel runs it from a
 // merged grid whose first CTAs take the long-slice segments)
-template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
+template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false, bool STATIC = false,
+          int NT = kBlock>
 __device__ __forceinline__ void dual_body(const SpmvArgs& a, unsigned bid) {
   using S = FastStep<CODEC, XT, GR>;
   if constexpr (DOT) {
@@ -641,8 +643,19 @@ __device__ __forceinline__ void dual_body(const SpmvArgs& a, unsigned bid) {
   double dotv = 0.0;
   const uint32_t npairs = (uint32_t)((a.n_slices + 1) >> 1);
   AffSched sched{AFF ? smid_u32() % (uint32_t)a.aff_chunks : 0u, 0u};
-  long long wg = AFF ? (long long)aff_next(a, sched, npairs) : ((long long)bid * kBlock + threadIdx.x) >> 5;
-  for (; !AFF || wg != (long long)~0u; wg = AFF ? (long long)aff_next(a, sched, npairs) : (long long)~0u) {
+  // STATIC: this CTA walks the contiguous, word-balanced pair range [pb, pe) of the ranges
+  // table behind the SM-affine counters (sched[aff_chunks + 1 ...]), its warps interleaved
+  long long st_pe = 0;
+  long long wg;
+  if constexpr (STATIC) {
+    const uint32_t* rg = a.sched + a.aff_chunks + 1;
+    st_pe = rg[bid + 1];
+    wg = (long long)rg[bid] + (threadIdx.x >> 5);
+  } else {
+    wg = AFF ? (long long)aff_next(a, sched, npairs) : ((long long)bid * NT + threadIdx.x) >> 5;
+  }
+  for (; STATIC ? wg < st_pe : (!AFF || wg != (long long)~0u);
+       wg = STATIC ? wg + NT / 32 : AFF ? (long long)aff_next(a, sched, npairs) : (long long)~0u) {
   const long long kA = 2 * wg, kB = kA + 1;
   if (kA < a.n_slices) {
     const bool hasB = kB < a.n_slices;
@@ -754,10 +767,27 @@ __device__ __forceinline__ void dual_body(const SpmvArgs& a, unsigned bid) {
     if (!skipA) flush(kA, accA);
     if (hasB && !skipB) flush(kB, accB);
   }
-  if (!AFF) break;
+  if (!AFF && !STATIC) break;
   }
   if constexpr (AFF) aff_exit(a);
-  finish_dot<DOT>(a, dotv);
+  finish_dot<DOT, NT>(a, dotv);
+}
+
+// Static SM-affine kernel (segmented matrices, the default): one 1024-thread CTA per SM, each
+// running its share of the long slices' segments and then one contiguous, word-balanced range
+// of short-slice pairs -- about a sigma window of rows per SM, whose x gathers then hit the
+// SM's L1 (the SM-affine claim scheduler, PSELL_AFF=1, got the locality but paid per-pair
+// atomics) -- so one launch covers segments and short slices, then the combine
+template <int CODEC, typename XT, int U>
+__device__ __forceinline__ void seg_one(const SpmvArgs& a, long long sg);
+
+template <int CODEC, typename XT, int U>
+__global__ void __launch_bounds__(1024, 1) spmv_dual_static_kernel(const SpmvArgs a, long long n_seg) {
+  // this CTA's share of the long slices' segments first (the same per-warp code as
+  // spmv_seg_kernel), then its contiguous range of short-slice pairs
+  const long long s0 = n_seg * blockIdx.x / gridDim.x, s1 = n_seg * (blockIdx.x + 1) / gridDim.x;
+  for (long long sg = s0 + (threadIdx.x >> 5); sg < s1; sg += 32) seg_one<CODEC, XT, U>(a, sg);
+  dual_body<CODEC, XT, false, U, true, false, true, 1024>(a, blockIdx.x);
 }
 
 template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
@@ -1199,12 +1229,11 @@ __global__ void __launch_bounds__(kBlock) seg_prefix_kernel(const SpmvArgs a, lo
   }
 }
 
+// one 256-step segment of a long slice, by one warp (sg warp-uniform)
 template <int CODEC, typename XT, int U>
-__device__ __forceinline__ void seg_body(const SpmvArgs& a, long long n_seg, unsigned bid) {
+__device__ __forceinline__ void seg_one(const SpmvArgs& a, long long sg) {
   using S = FastStep<CODEC, XT, true>;  // irregular rows: flag-predicated gathers
-  const long long sg = ((long long)bid * kBlock + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (sg >= n_seg) return;
   const int k = a.seg_slice[sg];
   const int q0 = a.seg_q0[sg];
   const long long o0 = a.offset[k];
@@ -1235,6 +1264,12 @@ __device__ __forceinline__ void seg_body(const SpmvArgs& a, long long n_seg, uns
     for (int u = 0; u < U; ++u) cur[u] = nxt[u];
   }
   a.seg_partial[sg * 32 + lane] = acc;
+}
+
+template <int CODEC, typename XT, int U>
+__device__ __forceinline__ void seg_body(const SpmvArgs& a, long long n_seg, unsigned bid) {
+  const long long sg = ((long long)bid * kBlock + threadIdx.x) >> 5;
+  if (sg < n_seg) seg_one<CODEC, XT, U>(a, sg);
 }
 
 template <int CODEC, typename XT, int U>
@@ -2599,6 +2634,7 @@ static int make_args(const psell_desc* d, const void* pack, const int64_t* offse
   magic_div((uint32_t)(a.se > 0 ? a.se : 1), a.se_m, a.se_l);
   magic_div((uint32_t)(a.sigma > 0 ? a.sigma : 1), a.sig_m, a.sig_l);
   a.l2pf = 1;
+  a.sched_static = 0;
   static EnvCache c;
   int v;
   if (env_int(c, "PSELL_L2PF", v)) a.l2pf = v;
@@ -2817,8 +2853,24 @@ static bool seg_merge() {
   return true;
 }
 
+// the static SM-affine grid for segmented matrices (default; PSELL_DSTATIC=0: the merged
+// segment + dual grid).  Config 4 327.8 -> 275.8 us, 4b 309.2 -> 257.1 us, bitwise
+// (profiles/r02/static_ab*.txt): a sigma window's rows per SM keep the x gathers in its L1.
+static bool dual_static() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_DSTATIC", v)) return v != 0;
+  return true;
+}
+
 template <int CODEC, typename XT>
 static void launch_segmented(const SpmvArgs& a, long long n_seg, long long n_long, cudaStream_t st) {
+  if (a.sched && a.aff_chunks > 0 && dual_static() && !aff_on() && a.n_slices >= 2 && a.sched_static) {
+    spmv_dual_static_kernel<CODEC, XT, 8><<<(unsigned)a.aff_chunks, 1024, 0, st>>>(a, n_seg);
+    if (n_long > 0)
+      seg_combine_kernel<XT><<<(unsigned)ceil_div(n_long * 32, kBlock), kBlock, 0, st>>>(a, n_long);
+    return;
+  }
   const bool aff = a.sched && a.aff_chunks > 0 && aff_on() && a.n_slices >= 2;
   if (!aff && n_seg > 0 && seg_merge() && dual_slices(a.n_slices) && !a.narrow && dual_chunk(false) == 8 &&
       !pair_wide()) {
@@ -2853,6 +2905,7 @@ int psell_spmv_segmented(const psell_desc* d, const void* pack, const int64_t* o
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
   a.sched = sched;
   a.aff_chunks = sched ? sched_chunks : 0;
+  a.sched_static = sched ? 1 : 0;  // PackSellMatrix's schedule carries the static ranges too
   if (d->c != 32 || d->codec == PSELL_FP32EMBED || (x_dtype != PSELL_DT_F16 && x_dtype != PSELL_DT_F32))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0,
                    "segmented SpMV: C = 32, fp16/e8my codec, f16/f32 x only");

@@ -329,11 +329,22 @@ def _seg_schedule(M: PackSellMatrix):
     n_seg = int(seg0[-1])
     seg_slice = np.repeat(long_, per).astype(np.int32)
     seg_q0 = ((np.arange(n_seg) - np.repeat(seg0[:-1], per)) * SEG_LEN).astype(np.int32)
+    G = _lib.sm_count()
+    # static SM-affine ranges (PSELL_DSTATIC A/B): G contiguous slice-pair ranges balanced by the
+    # words of the short slices (the long ones run as segments)
+    ws = np.where(w > SEG_LEN, 0, w).astype(np.int64)
+    ws = np.concatenate([ws, np.zeros(len(ws) % 2, np.int64)])
+    pw = np.cumsum(ws[0::2] + ws[1::2])
+    npairs = len(pw)
+    cut = np.searchsorted(pw, (pw[-1] * np.arange(1, G)) // G, side="right") if npairs else np.zeros(G - 1, np.int64)
+    ranges = np.concatenate([[0], np.minimum(cut, npairs), [npairs]]).astype(np.uint32)
+    sched = np.concatenate([np.zeros(G + 1, np.uint32), ranges])
     s = dict(n_seg=n_seg, n_long=int(long_.size), seg_slice=_dev.upload(seg_slice), seg_q0=_dev.upload(seg_q0),
              long_slice=_dev.upload(long_.astype(np.int32)), long_seg0=_dev.upload(seg0),
              seg_c2=_dev.empty(n_seg * 32, np.uint32),
-             # SM-affine scheduler counters of the short-slice kernel (left zeroed by every launch)
-             sched=_dev.zeros(_lib.sm_count() + 1, np.uint32), sched_chunks=_lib.sm_count())
+             # SM-affine scheduler counters of the short-slice kernel (left zeroed by every launch),
+             # then the static ranges
+             sched=_dev.upload(sched), sched_chunks=G)
     lib = _lib.lib()
     err = _lib.PsellError()
     rc = lib.psell_spmv_seg_checkpoints(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), SEG_LEN, n_seg,

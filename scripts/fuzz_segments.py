@@ -1,7 +1,7 @@
 """Randomised parity of the segmented (long-slice) SpMV: random power-law matrices with rows up
-to a few thousand entries, random sigma / codec / x dtype and row slabs (row0 > 0): the merged
-segment grid (default) bitwise equal to the two-launch form, both within the FMA bound of the
-oracle's REF-order SpMV.  usage: fuzz_segments.py [n_cases] [seed]"""
+to a few thousand entries, random sigma / codec / x dtype: the static SM-affine grid (default) bitwise equal to the
+merged segment grid and to the two-launch form, within the FMA bound of the oracle's
+REF-order SpMV.  usage: fuzz_segments.py [n_cases] [seed]"""
 import os
 import sys
 
@@ -40,12 +40,14 @@ for it in range(n_cases):
         segs += s is not None and s["n_seg"] > 0
         x = rng.uniform(-1, 1, n).astype(dt)
         y1 = P.packsell_spmv(M, x)
-        os.environ["PSELL_SEGMERGE"] = "0"
-        lib.psell_reload_env()
-        y0 = P.packsell_spmv(M, x)
-        os.environ.pop("PSELL_SEGMERGE")
-        lib.psell_reload_env()
-        assert np.array_equal(y1.view(np.uint8), y0.view(np.uint8)), "merged != two-launch"
+        for env in ({"PSELL_DSTATIC": "0"}, {"PSELL_DSTATIC": "0", "PSELL_SEGMERGE": "0"}):
+            os.environ.update(env)
+            lib.psell_reload_env()
+            y0 = P.packsell_spmv(M, x)
+            for k in env:
+                os.environ.pop(k)
+            lib.psell_reload_env()
+            assert np.array_equal(y1.view(np.uint8), y0.view(np.uint8)), f"static != {env}"
         OM = O.build(A.row_ptr, A.col_idx, A.values, A.n_cols, 32, sigma, O.preset(pre), "implicit")
         ref = O.spmv(OM, x.astype(np.float32)).astype(np.float64)
         lmax = int(np.max(np.diff(OM.offset) // 32))

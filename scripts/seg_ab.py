@@ -38,7 +38,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     sys.exit(0)
 
 args = sys.argv[1:]
-variants = ["PSELL_SEGMERGE=0", "PSELL_SEGMERGE=1"]
+variants = ["PSELL_DSTATIC=0,PSELL_SEGMERGE=0", "PSELL_DSTATIC=0", "PSELL_DSTATIC=1"]
 if "--" in args:
     variants = args[args.index("--") + 1:]
     args = args[:args.index("--")]

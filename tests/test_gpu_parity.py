@@ -310,7 +310,8 @@ def test_powerlaw_build_vs_oracle():
                                           (65536, "fp16", np.float32)])
 def test_long_slice_segmentation(monkeypatch, sigma, pre, dt):
     """Power-law rows wider than SEG_LEN run as checkpointed segments; result within the FMA bound.
-    The merged segment + short-slice grid (default) is bitwise the two-launch form."""
+    The static SM-affine grid (default), the merged segment + short-slice grid and the
+    two-launch form are bitwise equal."""
     from paper_2604_13433_b200 import _lib
     from paper_2604_13433_b200.packed import SEG_LEN, _seg_schedule
     from paper_2604_13433_b200.stencil import powerlaw_rows
@@ -320,12 +321,15 @@ def test_long_slice_segmentation(monkeypatch, sigma, pre, dt):
     assert s is not None and s["n_long"] > 0
     x = np.random.default_rng(2).uniform(-1, 1, A.n_cols).astype(dt)
     y = P.packsell_spmv(M, x)
-    monkeypatch.setenv("PSELL_SEGMERGE", "0")
-    _lib.lib().psell_reload_env()
-    y2 = P.packsell_spmv(M, x)
-    monkeypatch.delenv("PSELL_SEGMERGE")
-    _lib.lib().psell_reload_env()
-    assert np.array_equal(_bits(y), _bits(y2))
+    for env in ({"PSELL_DSTATIC": "0"}, {"PSELL_DSTATIC": "0", "PSELL_SEGMERGE": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        _lib.lib().psell_reload_env()
+        y2 = P.packsell_spmv(M, x)
+        for k in env:
+            monkeypatch.delenv(k)
+        _lib.lib().psell_reload_env()
+        assert np.array_equal(_bits(y), _bits(y2)), env
     y = y.astype(np.float64)
     ref = P.packsell_spmv(M, x.astype(np.float32), ref_order=True).astype(np.float64)
     lmax = int(np.max(np.diff(M.offset) // 32))
