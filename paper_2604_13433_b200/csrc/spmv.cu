@@ -648,9 +648,15 @@ __device__ __forceinline__ void dual_body(const SpmvArgs& a, unsigned bid) {
   long long st_pe = 0;
   long long wg;
   if constexpr (STATIC) {
+    // the table holds 2 x aff_chunks word-balanced chunks: a 1024-thread CTA (one per SM) takes
+    // chunks 2b, 2b+1; with 768-thread CTAs (two per SM, CTA b and b + G sharing an SM when
+    // the grid is dispatched round robin) CTA b < G takes chunk 2b and CTA b + G chunk 2b + 1
     const uint32_t* rg = a.sched + a.aff_chunks + 1;
-    st_pe = rg[bid + 1];
-    wg = (long long)rg[bid] + (threadIdx.x >> 5);
+    const unsigned G = (unsigned)a.aff_chunks;
+    const unsigned c0 = NT == 1024 ? 2u * bid : (bid < G ? 2u * bid : 2u * (bid - G) + 1u);
+    const unsigned c1 = NT == 1024 ? c0 + 2u : c0 + 1u;
+    st_pe = rg[c1];
+    wg = (long long)rg[c0] + (threadIdx.x >> 5);
   } else {
     wg = AFF ? (long long)aff_next(a, sched, npairs) : ((long long)bid * NT + threadIdx.x) >> 5;
   }
@@ -781,13 +787,22 @@ __device__ __forceinline__ void dual_body(const SpmvArgs& a, unsigned bid) {
 template <int CODEC, typename XT, int U>
 __device__ __forceinline__ void seg_one(const SpmvArgs& a, long long sg);
 
-template <int CODEC, typename XT, int U>
-__global__ void __launch_bounds__(1024, 1) spmv_dual_static_kernel(const SpmvArgs a, long long n_seg) {
+template <int CODEC, typename XT, int U, int NT = 1024>
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 2) spmv_dual_static_kernel(const SpmvArgs a, long long n_seg) {
   // this CTA's share of the long slices' segments first (the same per-warp code as
   // spmv_seg_kernel), then its contiguous range of short-slice pairs
   const long long s0 = n_seg * blockIdx.x / gridDim.x, s1 = n_seg * (blockIdx.x + 1) / gridDim.x;
-  for (long long sg = s0 + (threadIdx.x >> 5); sg < s1; sg += 32) seg_one<CODEC, XT, U>(a, sg);
-  dual_body<CODEC, XT, false, U, true, false, true, 1024>(a, blockIdx.x);
+  for (long long sg = s0 + (threadIdx.x >> 5); sg < s1; sg += NT / 32) seg_one<CODEC, XT, U>(a, sg);
+  dual_body<CODEC, XT, false, U, true, false, true, NT>(a, blockIdx.x);
+}
+
+// PSELL_DSTATIC_NT=768: two 768-thread CTAs per SM (A/B; config 4b 323 vs 257 us -- the two
+// CTAs an SM receives do not get adjacent chunks, so each SM holds two x windows)
+static int dual_static_nt() {
+  static EnvCache c;
+  int v;
+  if (env_int(c, "PSELL_DSTATIC_NT", v) && v == 768) return 768;
+  return 1024;
 }
 
 template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
@@ -2866,7 +2881,10 @@ static bool dual_static() {
 template <int CODEC, typename XT>
 static void launch_segmented(const SpmvArgs& a, long long n_seg, long long n_long, cudaStream_t st) {
   if (a.sched && a.aff_chunks > 0 && dual_static() && !aff_on() && a.n_slices >= 2 && a.sched_static) {
-    spmv_dual_static_kernel<CODEC, XT, 8><<<(unsigned)a.aff_chunks, 1024, 0, st>>>(a, n_seg);
+    if (dual_static_nt() == 768)
+      spmv_dual_static_kernel<CODEC, XT, 8, 768><<<2u * (unsigned)a.aff_chunks, 768, 0, st>>>(a, n_seg);
+    else
+      spmv_dual_static_kernel<CODEC, XT, 8, 1024><<<(unsigned)a.aff_chunks, 1024, 0, st>>>(a, n_seg);
     if (n_long > 0)
       seg_combine_kernel<XT><<<(unsigned)ceil_div(n_long * 32, kBlock), kBlock, 0, st>>>(a, n_long);
     return;

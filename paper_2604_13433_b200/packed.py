@@ -336,7 +336,8 @@ def _seg_schedule(M: PackSellMatrix):
     ws = np.concatenate([ws, np.zeros(len(ws) % 2, np.int64)])
     pw = np.cumsum(ws[0::2] + ws[1::2])
     npairs = len(pw)
-    cut = np.searchsorted(pw, (pw[-1] * np.arange(1, G)) // G, side="right") if npairs else np.zeros(G - 1, np.int64)
+    NC = 2 * G  # word-balanced chunks: two per SM (psell: one 1024- or two 768-thread CTAs per SM)
+    cut = np.searchsorted(pw, (pw[-1] * np.arange(1, NC)) // NC, side="right") if npairs else np.zeros(NC - 1, np.int64)
     ranges = np.concatenate([[0], np.minimum(cut, npairs), [npairs]]).astype(np.uint32)
     sched = np.concatenate([np.zeros(G + 1, np.uint32), ranges])
     s = dict(n_seg=n_seg, n_long=int(long_.size), seg_slice=_dev.upload(seg_slice), seg_q0=_dev.upload(seg_q0),
