@@ -471,8 +471,16 @@ struct FillArgs {
 // packed.py:216-231: word q of storage row s lives at offset[s//C] + s%C + q*C.
 // A dummy (flag 0, full gap) precedes a real word whose gap >= 2^D; that real
 // word then stores delta 0.  Everything past the stored count is padding 0.
+#ifndef PSELL_FILL_U
+#define PSELL_FILL_U 4
+#endif
+#ifndef PSELL_FILL_MINB
+#define PSELL_FILL_MINB 1
+#endif
+constexpr int kFillU = PSELL_FILL_U;
+
 template <typename W>
-__global__ void __launch_bounds__(kBlock) fill_kernel(FillArgs a) {
+__global__ void __launch_bounds__(kBlock, PSELL_FILL_MINB) fill_kernel(FillArgs a) {
   __shared__ long long sh[32];
   const long long s = (long long)blockIdx.x * kBlock + threadIdx.x;
   long long bad_nf = kI64Max, bad_of = kI64Max;
@@ -497,21 +505,37 @@ __global__ void __launch_bounds__(kBlock) fill_kernel(FillArgs a) {
         return blk > a.k_left ? blk - a.k_left : 0ll;
       }();
       lng = end - beg > kLongRow;
-      for (long long j = beg; j < (lng ? beg : end); ++j) {
-        const long long col = a.col_idx[j];
-        long long gap = col - prev;
-        prev = col;
-        int stc = ENC_OK;
-        const W pat = (W)encode_value(a.f, a.values[j], stc);
-        if (stc == ENC_NONFINITE) bad_nf = j < bad_nf ? j : bad_nf;
-        else if (stc == ENC_OVERFLOW) bad_of = j < bad_of ? j : bad_of;
-        if (gap >= thr) {
-          out[q * stride] = ((W)gap) << 1;
-          ++q;
-          gap = 0;
+      const long long jend = lng ? beg : end;
+      // entries in groups of kFillU: the group's column / value loads issue together (the
+      // walk itself is sequential: the gap and the word index carry from entry to entry)
+      for (long long j0 = beg; j0 < jend; j0 += kFillU) {
+        int32_t cv[kFillU];
+        double vv[kFillU];
+#pragma unroll
+        for (int u = 0; u < kFillU; ++u) {
+          const bool in = j0 + u < jend;
+          cv[u] = in ? a.col_idx[j0 + u] : 0;
+          vv[u] = in ? a.values[j0 + u] : 0.0;
         }
-        out[q * stride] = (pat << sh_v) | (((W)gap) << 1) | W(1);
-        ++q;
+#pragma unroll
+        for (int u = 0; u < kFillU; ++u) {
+          const long long j = j0 + u;
+          if (j >= jend) break;
+          const long long col = cv[u];
+          long long gap = col - prev;
+          prev = col;
+          int stc = ENC_OK;
+          const W pat = (W)encode_value(a.f, vv[u], stc);
+          if (stc == ENC_NONFINITE) bad_nf = j < bad_nf ? j : bad_nf;
+          else if (stc == ENC_OVERFLOW) bad_of = j < bad_of ? j : bad_of;
+          if (gap >= thr) {
+            out[q * stride] = ((W)gap) << 1;
+            ++q;
+            gap = 0;
+          }
+          out[q * stride] = (pat << sh_v) | (((W)gap) << 1) | W(1);
+          ++q;
+        }
       }
     }
     if (!lng)
