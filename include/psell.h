@@ -175,9 +175,13 @@ PSELL_API int psell_spmv_segmented(const psell_desc* desc, const void* pack, con
                                    const int32_t* seg_q0, const uint32_t* seg_c2, float* seg_partial,
                                    int64_t n_long, const int32_t* long_slice, const int32_t* long_seg0,
                                    uint32_t* sched, int32_t sched_chunks, void* stream, psell_error* err);
-/* sched (nullable): sched_chunks + 1 zeroed uint32 of device scratch kept with the
- * matrix; the short slices then run on an SM-affine persistent grid (one chunk of
- * consecutive slice pairs per SM, work stealing) and the kernel leaves it zeroed. */
+/* sched (nullable): G + 1 zeroed uint32 of device scratch kept with the matrix, G =
+ * |sched_chunks| = the SM count; with PSELL_AFF=1 the short slices then run on an
+ * SM-affine claim grid (one chunk of consecutive slice pairs per SM, work stealing) and
+ * the kernel leaves the counters zeroed.  sched_chunks < 0: the G + 1 counters are
+ * followed by 2 G + 1 slice-pair bounds (2 G chunks balanced by the short slices' words),
+ * and the default static SM-affine grid runs: one 1024-thread CTA per SM takes chunks
+ * 2b, 2b + 1 after its share of the segments, no atomics (PackSellMatrix builds both). */
 
 /* Number of double partials psell_spmv_dot writes (one per CTA) for these flags. */
 PSELL_API int64_t psell_spmv_dot_partials(const psell_desc* desc, int32_t flags);

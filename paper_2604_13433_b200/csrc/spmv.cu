@@ -2922,8 +2922,9 @@ int psell_spmv_segmented(const psell_desc* d, const void* pack, const int64_t* o
   SpmvArgs a;
   if (int rc = make_args(d, pack, offset, perm, a, err)) return rc;
   a.sched = sched;
-  a.aff_chunks = sched ? sched_chunks : 0;
-  a.sched_static = sched ? 1 : 0;  // PackSellMatrix's schedule carries the static ranges too
+  // sched_chunks < 0: sched also carries the static grid's 2 |sched_chunks| + 1 chunk bounds
+  a.aff_chunks = sched ? (sched_chunks < 0 ? -sched_chunks : sched_chunks) : 0;
+  a.sched_static = sched && sched_chunks < 0 ? 1 : 0;
   if (d->c != 32 || d->codec == PSELL_FP32EMBED || (x_dtype != PSELL_DT_F16 && x_dtype != PSELL_DT_F32))
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0,
                    "segmented SpMV: C = 32, fp16/e8my codec, f16/f32 x only");

@@ -345,7 +345,7 @@ def _seg_schedule(M: PackSellMatrix):
              seg_c2=_dev.empty(n_seg * 32, np.uint32),
              # SM-affine scheduler counters of the short-slice kernel (left zeroed by every launch),
              # then the static ranges
-             sched=_dev.upload(sched), sched_chunks=G)
+             sched=_dev.upload(sched), sched_chunks=-G)  # < 0: the static chunk table follows
     lib = _lib.lib()
     err = _lib.PsellError()
     rc = lib.psell_spmv_seg_checkpoints(M.desc(), _lib.ptr(M.d_pack), _lib.ptr(M.d_offset), SEG_LEN, n_seg,
