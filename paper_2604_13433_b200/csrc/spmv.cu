@@ -806,7 +806,10 @@ static int dual_static_nt() {
 }
 
 template <int CODEC, typename XT, bool DOT, int U, bool GR = false, bool AFF = false>
-__global__ void __launch_bounds__(kBlock, 6) spmv_dual_kernel(const SpmvArgs a) {
+#ifndef PSELL_DUAL_MINB
+#define PSELL_DUAL_MINB 6
+#endif
+__global__ void __launch_bounds__(kBlock, PSELL_DUAL_MINB) spmv_dual_kernel(const SpmvArgs a) {
   dual_body<CODEC, XT, DOT, U, GR, AFF>(a, blockIdx.x);
 }
 
