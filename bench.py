@@ -582,13 +582,17 @@ def run_pcg(args, world, rank, comm, peak):
     S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=2), comm=comm)
     rep64, t_64 = timed(lambda: S.pcg(A, b, S.SolveConfig(tol=1e-9, max_outer=5000), comm=comm))
     rep32 = t_32 = None
+    sell_spmv_bytes = 0
     if world == 1:  # FP32 IO-CG comparator: SELL-C-sigma f32 inner operator, same protocol
         be32 = S.make_backend(A, "sell32")
         cfg32 = S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="sell32", max_outer=400)
         S.iocg(A, b, S.SolveConfig(solver="iocg", tol=1e-9, m_in=args.pcg_m_in, a_backend="sell32", max_outer=1),
                backend=be32)
         rep32, t_32 = timed(lambda: S.iocg(A, b, cfg32, backend=be32))
-        del be32
+        Ms = be32.matrix  # SELL bytes per inner SpMV: f32 value + int32 column per stored entry
+        sell_spmv_bytes = (8 * Ms.n_stored + 8 * (Ms.n_slices + 1) + (Ms.n_rows if Ms.mode == "implicit" else 0)
+                           + 4 * n + 4 * (r1 - r0))
+        del be32, Ms
     touched = n if world == 1 else (r1 - r0) + 2 * nx * nx
     ib, ob = pcg_bytes(be.matrix, r1 - r0, A.nnz, touched)
     io_bytes = rep.total_inner_iters * ib + (rep.outer_iters + 1) * ob
@@ -611,13 +615,22 @@ def run_pcg(args, world, rank, comm, peak):
         "fp32_sell_iocg": None if rep32 is None else {
             "inner": "SELL-C-sigma (C=32, sigma=256) f32 values + int32 columns, f32 vectors, m_in=%d" % args.pcg_m_in,
             "solve_s": t_32, "outer_iters": rep32.outer_iters, "inner_iters": rep32.total_inner_iters,
-            "converged": rep32.converged, "true_relres": rep32.final_true_relres},
+            "converged": rep32.converged, "true_relres": rep32.final_true_relres,
+            # the same roofline accounting as the PackSELL IO-CG (inner SpMV bytes + 36 B/row of
+            # vectors per inner iteration, the outer iterations as there)
+            "roofline_s": (rep32.total_inner_iters * (sell_spmv_bytes + 36 * (r1 - r0))
+                           + (rep32.outer_iters + 1) * ob) / (peak * 1e9),
+            "frac_of_roofline": (rep32.total_inner_iters * (sell_spmv_bytes + 36 * (r1 - r0))
+                                 + (rep32.outer_iters + 1) * ob) / (peak * 1e9) / t_32},
         "speedup_iocg_vs_fp64_pcg": t_64 / t_io,
         # the comparator runs at a lower fraction of its own roofline than the IO-CG, so the
         # measured speed-up overstates the format's advantage: the roofline-to-roofline ratio
         # is the one a perfectly tuned FP64 PCG would see
         "speedup_iocg_vs_fp64_pcg_roofline_to_roofline": (agg(p64_bytes) / agg(io_bytes)),
         "speedup_iocg_vs_fp32_sell_iocg": None if t_32 is None else t_32 / t_io,
+        "speedup_iocg_vs_fp32_sell_iocg_roofline_to_roofline": None if t_32 is None else (
+            (rep32.total_inner_iters * (sell_spmv_bytes + 36 * (r1 - r0)) + (rep32.outer_iters + 1) * ob)
+            / agg(io_bytes)),
         "build_s": t_build,
         "collectives": "none" if world == 1 else (
             "peer-memory transport (K8, csrc/peer.cu): one kernel per halo exchange pushes p's halo (f32 inner, "
