@@ -403,6 +403,14 @@ PSELL_API int psell_gen_stencil_fill(int64_t d0, int64_t d1, int64_t d2, int32_t
 PSELL_API int psell_sell_fill(const psell_desc* desc, const int64_t* row_ptr, const int32_t* col_idx,
                               const double* values, const void* plan_workspace, const int64_t* offset,
                               int32_t val_dtype, void* val, int32_t* col, void* stream, psell_error* err);
+/* The FP32 IO-CG comparator's inner operator (SELL-C-sigma f32, C = 32, f32 x): the SpMV
+ * (bitwise psell_sell_spmv) fused with p_own . y and, in the last CTA, the alpha step
+ * (psell_spmv_dot_alpha's contract; partials >= psell_sell_spmv_dot_partials + groups). */
+PSELL_API int64_t psell_sell_spmv_dot_partials(const psell_desc* desc);
+PSELL_API int psell_sell_spmv_dot_alpha(const psell_desc* desc, const void* val, int32_t val_dtype,
+                                        const int32_t* col, const int64_t* offset, const void* perm, const float* x,
+                                        float* y, const float* p_own, double* partials, double* scal,
+                                        int32_t* iflags, unsigned* ticket, void* stream, psell_error* err);
 PSELL_API int psell_sell_spmv(const psell_desc* desc, const void* val, int32_t val_dtype, const int32_t* col,
                               const int64_t* offset, const void* perm, const void* x, int32_t x_dtype,
                               void* y, void* stream, psell_error* err);

@@ -118,6 +118,8 @@ _SIGS = {
     "psell_pcg_update_status": (c_int32, [c_int64, _P, _P, _P, _P, _P, _P, c_double, c_double, _P, _P, _P, _P]),
     "psell_sell_fill": (c_int32, [_D, _P, _P, _P, _P, _P, c_int32, _P, _P, _P, _E]),
     "psell_sell_spmv": (c_int32, [_D, _P, c_int32, _P, _P, _P, _P, c_int32, _P, _P, _E]),
+    "psell_sell_spmv_dot_partials": (c_int64, [_D]),
+    "psell_sell_spmv_dot_alpha": (c_int32, [_D, _P, c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _E]),
     "psell_gen_workspace_bytes": (c_size_t, [c_int64]),
     "psell_gen_powerlaw_plan": (c_int32, [c_int64, c_uint64, _P, c_int64, c_int64, _P, c_size_t, _P,
                                           POINTER(c_int64), _P, _E]),

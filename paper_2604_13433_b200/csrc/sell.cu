@@ -163,6 +163,83 @@ __global__ void __launch_bounds__(kBlock, 6) sell_spmv_c32_kernel(const VT* __re
   y[out] = acc;
 }
 
+// The FP32 IO-CG comparator's inner operator fused like the PackSELL one (psell_spmv_dot_alpha):
+// sell_spmv_c32_kernel's SpMV (same per-row order: bitwise y) plus this thread's rows of
+// p_own . y in FP64, the CTA sums as partials and, in the last CTA, the fixed-order total and
+// the alpha step -- one launch instead of SpMV, dot and alpha.
+template <typename VT>
+__global__ void __launch_bounds__(kBlock, 6) sell_spmv_dot_alpha_kernel(const VT* __restrict__ val,
+                                                                        const int32_t* __restrict__ col,
+                                                                        const int64_t* __restrict__ offset,
+                                                                        const void* perm, int perm_bytes, int implicit,
+                                                                        unsigned sigma, long long n_rows,
+                                                                        long long n_slices, const float* __restrict__ x,
+                                                                        float* __restrict__ y,
+                                                                        const float* __restrict__ p_own,
+                                                                        double* __restrict__ parts, double* scal,
+                                                                        int32_t* iflags, unsigned* ticket) {
+  constexpr int U = 8;
+  if (*iflags) return;  // breakdown / closed gate: the whole inner solve is a no-op
+  __shared__ double sh[kBlock / 32];
+  // persistent: short CTAs would each pay the fence + ticket of the epilogue, so every warp walks
+  // slices with a grid stride and the CTA reduces once
+  const int lane = threadIdx.x & 31;
+  const long long n_warps = (long long)gridDim.x * (kBlock / 32);
+  double dotv = 0.0;
+  for (long long k = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; k < n_slices; k += n_warps) {
+    const long long o = offset[k];
+    const int width = (int)((offset[k + 1] - o) >> 5);
+    const VT* pv = val + o + lane;
+    const int32_t* pc = col + o + lane;
+    float acc = RefOps<float>::zero();
+    for (int q = 0; q < width; q += U) {
+      VT v[U];
+      int32_t c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool in = q + u < width;
+        v[u] = in ? __ldcs(pv + (q + u) * 32) : VT(0);
+        c[u] = in ? __ldcs(pc + (q + u) * 32) : 0;
+      }
+      float xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = x[c[u]];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q + u < width) acc = RefOps<float>::step(acc, vcast<VT, float>(v[u]), xv[u]);
+    }
+    const unsigned s = (unsigned)(k * 32) + lane;
+    if ((long long)s < n_rows) {
+      unsigned out = s;
+      if (implicit) {
+        const unsigned pp = perm_bytes == 1 ? (unsigned)static_cast<const uint8_t*>(perm)[s]
+                                            : (unsigned)static_cast<const uint16_t*>(perm)[s];
+        out = (s / sigma) * sigma + pp;
+      }
+      y[out] = acc;
+      dotv += (double)p_own[out] * (double)acc;
+    }
+  }
+  const double t = block_sum<kBlock>(dotv, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = t;
+  double pq;
+  if (last_cta_sum<kBlock>(parts, ticket, pq, sh) && threadIdx.x == 0) ipcg_alpha_step(pq, scal, iflags);
+}
+
+// persistent grid of the fused kernel: 6 resident CTAs per SM (its launch bounds), never more
+// CTAs than slices need
+static long long sell_dot_grid(long long n_slices) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long need = ceil_div(n_slices * 32, (long long)kBlock), cap = 6LL * sms;
+  return need < 1 ? 1 : (need < cap ? need : cap);
+}
+
 template <typename VT, typename XT>
 static void launch_sell(const psell_desc* d, const void* val, const int32_t* col, const int64_t* offset,
                         const void* perm, const void* x, void* y, cudaStream_t st) {
@@ -242,6 +319,27 @@ PSELL_API int psell_sell_spmv(const psell_desc* d, const void* val, int32_t val_
   }
   if (bad) return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0, "bad dtype");
   PSELL_CHECK_LAUNCH(err, "psell_sell_spmv");
+  return ok(err);
+}
+
+PSELL_API int64_t psell_sell_spmv_dot_partials(const psell_desc* d) {
+  if (!d || d->n_rows <= 0) return 1;
+  return sell_dot_grid(ceil_div(d->n_rows, 32));
+}
+
+PSELL_API int psell_sell_spmv_dot_alpha(const psell_desc* d, const void* val, int32_t val_dtype, const int32_t* col,
+                                        const int64_t* offset, const void* perm, const float* x, float* y,
+                                        const float* p_own, double* partials, double* scal, int32_t* iflags,
+                                        unsigned* ticket, void* stream, psell_error* err) {
+  if (!d || d->c != 32 || d->n_rows <= 0 || d->n_rows >= (1LL << 31) || val_dtype != PSELL_DT_F32 || !ticket ||
+      !scal || !iflags || !partials)
+    return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0,
+                   "psell_sell_spmv_dot_alpha: C = 32 f32 SELL, f32 x, scalar state");
+  const long long ns = ceil_div(d->n_rows, 32);
+  sell_spmv_dot_alpha_kernel<float><<<(unsigned)sell_dot_grid(ns), kBlock, 0, as_stream(stream)>>>(
+      static_cast<const float*>(val), col, offset, perm, d->sigma <= 256 ? 1 : 2, d->mode == PSELL_MODE_IMPLICIT,
+      (unsigned)d->sigma, d->n_rows, ns, x, y, p_own, partials, scal, iflags, ticket);
+  PSELL_CHECK_LAUNCH(err, "psell_sell_spmv_dot_alpha");
   return ok(err);
 }
 

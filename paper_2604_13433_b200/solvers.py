@@ -485,7 +485,15 @@ class _GenericInner:
         self.f32 = self.tdt == torch.float32
         self.dt_code = _dev.T_DT_CODE[self.tdt]
         self.inv = inv
-        self.d = _Dev(_lib.RED_BLOCKS)
+        # f32 SELL-C-sigma (C = 32) comparator: SpMV + p.q + alpha as one launch, like the PackSELL
+        # inner loop (psell_sell_spmv_dot_alpha; PSELL_SELL_FUSED=0 restores the three launches)
+        M = backend.matrix
+        self.sell_fused = (self.f32 and backend.name == "sell32" and getattr(M, "c", 0) == 32
+                           and os.environ.get("PSELL_SELL_FUSED", "1") != "0")
+        n_part = _lib.RED_BLOCKS
+        if self.sell_fused:
+            n_part = max(n_part, int(_lib.lib().psell_sell_spmv_dot_partials(M.desc())))
+        self.d = _Dev(n_part)
         self.n = None
 
     def _alloc(self, n):
@@ -515,10 +523,21 @@ class _GenericInner:
         lib.psell_ipcg_begin(n, r64.data_ptr(), x.data_ptr(), r.data_ptr(), z.data_ptr(), p.data_ptr(), inv,
                              d.p(d.partials), d.p(d.loc, 0), st)
         lib.psell_ipcg_set_rz_gated(d.p(d.loc, 0), 1, 8, d.p(d.scal), d.p(d.flags), self.gate.data_ptr(), st)
+        M, L = self.backend.matrix, d.L
+        if self.sell_fused:
+            from . import _dev
+            sdesc, err = M.desc(), L.PsellError()
         for _ in range(self.m_in):
-            self.backend.apply_into(p, q)
-            lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
-            lib.psell_ipcg_alpha(d.p(d.loc, 1), 1, 8, d.p(d.scal), d.p(d.flags), st)
+            if self.sell_fused:
+                rc = lib.psell_sell_spmv_dot_alpha(sdesc, L.ptr(M.d_val), _dev.DT_CODE[M.value_dtype], L.ptr(M.d_col),
+                                                   L.ptr(M.d_offset), L.ptr(M.d_perm), p.data_ptr(), q.data_ptr(),
+                                                   p.data_ptr(), d.p(d.partials), d.p(d.scal), d.p(d.flags),
+                                                   d.p(d.ticket, 0), st, err)
+                L.check(rc, err)
+            else:
+                self.backend.apply_into(p, q)
+                lib.psell_dot(p.data_ptr(), q.data_ptr(), self.dt_code, n, d.p(d.partials), d.p(d.loc, 1), st)
+                lib.psell_ipcg_alpha(d.p(d.loc, 1), 1, 8, d.p(d.scal), d.p(d.flags), st)
             lib.psell_ipcg_update_beta(n, None, r.data_ptr(), z.data_ptr(), p.data_ptr(), q.data_ptr(), inv,
                                        d.p(d.scal), d.p(d.flags), d.p(d.partials), d.p(d.ticket, d.tstride), st)
             lib.psell_ipcg_direction_x(n, p.data_ptr(), z.data_ptr(), x.data_ptr(), d.p(d.scal), d.p(d.flags), st)

@@ -84,3 +84,58 @@ def test_sell32_c32_kernel_large_vs_row_sequential():
         nz = w != 0
         assert np.array_equal(_bits(y[nz]), _bits(w[nz])), mode
         assert np.all(y[~nz] == 0), mode
+
+
+@pytest.mark.parametrize("mode,sigma", [("implicit", 256), ("implicit", 4096), ("explicit", 1024), ("none", 1)])
+def test_sell_spmv_dot_alpha_fused(mode, sigma):
+    """psell_sell_spmv_dot_alpha (the FP32 IO-CG comparator's inner operator): y bitwise equal
+    to psell_sell_spmv, p.y equal to the FP64 sum of the f32 products (exact in f64) up to
+    summation order, alpha = rz / pq in scal[2], the tickets re-armed for the next launch."""
+    import torch
+    from paper_2604_13433_b200 import _lib, _dev
+    rng = np.random.default_rng(21)
+    n = 200_003
+    lens = rng.integers(0, 14, n)
+    lens[rng.integers(0, n, 50)] = 150
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.sort(rng.integers(0, n, int(rp[-1])).astype(np.int32))
+    A = P.CsrMatrix(n, n, rp, ci, rng.standard_normal(int(rp[-1])))
+    M = P.build_sell(A, 32, sigma, mode, np.dtype(np.float32))
+    lib = _lib.lib()
+    p = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).cuda()
+    want = P.sell_spmv(M, p)
+    n_part = int(lib.psell_sell_spmv_dot_partials(M.desc()))
+    parts = torch.zeros(n_part + n_part // 32 + 8, dtype=torch.float64, device="cuda")
+    ticket = torch.zeros(2 + n_part // 32, dtype=torch.int32, device="cuda")
+    y = torch.empty_like(p)
+    for rep in range(3):
+        scal = torch.zeros(32, dtype=torch.float64, device="cuda")
+        scal[0] = 3.0 + rep
+        flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+        err = _lib.PsellError()
+        rc = lib.psell_sell_spmv_dot_alpha(M.desc(), _lib.ptr(M.d_val), _dev.DT_CODE[M.value_dtype],
+                                           _lib.ptr(M.d_col), _lib.ptr(M.d_offset), _lib.ptr(M.d_perm),
+                                           p.data_ptr(), y.data_ptr(), p.data_ptr(), parts.data_ptr(),
+                                           scal.data_ptr(), flags.data_ptr(), ticket.data_ptr(),
+                                           _lib.stream_handle(), err)
+        _lib.check(rc, err)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int32), want.view(torch.int32)), (mode, rep)
+        pq = float((p.double() * y.double()).sum())
+        assert abs(float(scal[1]) - pq) <= 1e-12 * float((p.double() * y.double()).abs().sum())
+        assert int(flags[0]) == (1 if pq <= 0 else 0)
+        if pq > 0:
+            assert float(scal[2]) == (3.0 + rep) / float(scal[1])
+        assert int(ticket.abs().sum()) == 0
+
+
+def test_iocg_sell32_fused_matches_unfused(monkeypatch):
+    """The fused comparator inner loop and the three-launch one agree to summation order."""
+    A = P.sym_diag_scale(P.poisson3d(24))
+    b, _ = S.make_rhs_and_x0(A.n_rows, 9)
+    cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=30, a_backend="sell32", max_outer=200)
+    r1 = S.iocg(A, b, cfg)
+    monkeypatch.setenv("PSELL_SELL_FUSED", "0")
+    r0 = S.iocg(A, b, cfg)
+    assert r1.converged and r0.converged and abs(r1.outer_iters - r0.outer_iters) <= 1
+    assert np.abs(r1.x - r0.x).max() <= 1e-7 * np.abs(r0.x).max()
