@@ -87,15 +87,45 @@ class Comm:
         mode = os.environ.get("PSELL_XPORT", "auto")
         if mode == "nccl" or (mode == "auto" and not self.nccl):
             return None
+        if mode == "auto" and not self._peer_capable():
+            return None  # another node, or no P2P path between two ranks' GPUs: NCCL
         cache = self.__dict__.setdefault("_peers", {})
         if n_cols not in cache:
             cache[n_cols] = PeerTransport(self, n_cols)
         return cache[n_cols]
 
+    def _peer_capable(self) -> bool:
+        """Every rank can map every other rank's arena (collective, cached): all GPUs are
+        visible on this node and each pair has a P2P path (NVLink / NVSwitch), so no rank
+        fails in cudaIpcOpenMemHandle while the others wait in the exchange kernel."""
+        if "_p2p" not in self.__dict__:
+            import torch
+            mine = str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)
+            uuids = [None] * self.world
+            self.dist.all_gather_object(uuids, mine, group=self.group)
+            local = [str(torch.cuda.get_device_properties(i).uuid) for i in range(torch.cuda.device_count())]
+            ok = peer_capable(torch.cuda.current_device(), uuids, local, torch.cuda.can_device_access_peer)
+            votes = [None] * self.world
+            self.dist.all_gather_object(votes, bool(ok), group=self.group)
+            self._p2p = all(votes)
+        return self._p2p
+
     def close(self):
         """Release the peer arenas (collective)."""
         for t in self.__dict__.pop("_peers", {}).values():
             t.close()
+
+
+def peer_capable(my_dev: int, rank_uuids: Sequence[str], local_uuids: Sequence[str], can_access) -> bool:
+    """This rank can map every rank's device memory: each rank's GPU (by UUID) is one of this
+    node's devices, and the same GPU or one `can_access(my_dev, dev)` reaches."""
+    for u in rank_uuids:
+        if u not in local_uuids:
+            return False
+        d = list(local_uuids).index(u)
+        if d != my_dev and not can_access(my_dev, d):
+            return False
+    return True
 
 
 class _CudaView:

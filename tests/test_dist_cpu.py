@@ -267,3 +267,14 @@ def test_allgather_transport_refuses_unequal_slabs():
         p.join(timeout=60)
     for _, out in res:
         assert out == ["equal ok", "unequal refused", "peer ok"], out
+
+
+def test_peer_capable():
+    """The peer transport is used only when every rank's GPU is on this node and reachable."""
+    from paper_2604_13433_b200.dist import peer_capable
+    local = ["GPU-a", "GPU-b", "GPU-c"]
+    allp = lambda i, j: True  # noqa: E731
+    assert peer_capable(0, ["GPU-a", "GPU-b", "GPU-c"], local, allp)
+    assert peer_capable(1, ["GPU-b", "GPU-b"], local, lambda i, j: False)  # ranks sharing one GPU
+    assert not peer_capable(0, ["GPU-a", "GPU-z"], local, allp)  # a rank on another node
+    assert not peer_capable(0, ["GPU-a", "GPU-c"], local, lambda i, j: (i, j) != (0, 2))  # no P2P path
