@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(kBlock, 6) sell_spmv_c32_kernel(const VT* __re
 // sell_spmv_c32_kernel's SpMV (same per-row order: bitwise y) plus this thread's rows of
 // p_own . y in FP64, the CTA sums as partials and, in the last CTA, the fixed-order total and
 // the alpha step -- one launch instead of SpMV, dot and alpha.
-template <typename VT>
-__global__ void __launch_bounds__(kBlock, 6) sell_spmv_dot_alpha_kernel(const VT* __restrict__ val,
+template <typename VT, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) sell_spmv_dot_alpha_kernel(const VT* __restrict__ val,
                                                                         const int32_t* __restrict__ col,
                                                                         const int64_t* __restrict__ offset,
                                                                         const void* perm, int perm_bytes, int implicit,
@@ -226,8 +226,20 @@ __global__ void __launch_bounds__(kBlock, 6) sell_spmv_dot_alpha_kernel(const VT
   if (last_cta_sum<kBlock>(parts, ticket, pq, sh) && threadIdx.x == 0) ipcg_alpha_step(pq, scal, iflags);
 }
 
-// persistent grid of the fused kernel: 6 resident CTAs per SM (its launch bounds), never more
+// persistent grid of the fused kernel: its resident CTAs per SM (launch bounds), never more
 // CTAs than slices need
+// resident CTAs per SM of the fused kernel: 6 (40 registers, 24 B of spills) beats 4 (no spills,
+// 0.539 vs 0.455 s per comparator solve, profiles/r02/sell_dot_minb_ab.txt); PSELL_SELL_DOT_MINB=4|8 A/B
+static int sell_dot_minb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PSELL_SELL_DOT_MINB");
+    const int m = e ? atoi(e) : 6;
+    v = (m == 4 || m == 8) ? m : 6;
+  }
+  return v;
+}
+
 static long long sell_dot_grid(long long n_slices) {
   static int sms = 0;
   if (!sms) {
@@ -236,7 +248,7 @@ static long long sell_dot_grid(long long n_slices) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const long long need = ceil_div(n_slices * 32, (long long)kBlock), cap = 6LL * sms;
+  const long long need = ceil_div(n_slices * 32, (long long)kBlock), cap = (long long)sell_dot_minb() * sms;
   return need < 1 ? 1 : (need < cap ? need : cap);
 }
 
@@ -336,7 +348,10 @@ PSELL_API int psell_sell_spmv_dot_alpha(const psell_desc* d, const void* val, in
     return set_err(err, PSELL_EARG, PSELL_KIND_PARAM, -1, 0, 0,
                    "psell_sell_spmv_dot_alpha: C = 32 f32 SELL, f32 x, scalar state");
   const long long ns = ceil_div(d->n_rows, 32);
-  sell_spmv_dot_alpha_kernel<float><<<(unsigned)sell_dot_grid(ns), kBlock, 0, as_stream(stream)>>>(
+  const int mb = sell_dot_minb();
+  auto kern = mb == 6 ? sell_spmv_dot_alpha_kernel<float, 6>
+                      : mb == 8 ? sell_spmv_dot_alpha_kernel<float, 8> : sell_spmv_dot_alpha_kernel<float, 4>;
+  kern<<<(unsigned)sell_dot_grid(ns), kBlock, 0, as_stream(stream)>>>(
       static_cast<const float*>(val), col, offset, perm, d->sigma <= 256 ? 1 : 2, d->mode == PSELL_MODE_IMPLICIT,
       (unsigned)d->sigma, d->n_rows, ns, x, y, p_own, partials, scal, iflags, ticket);
   PSELL_CHECK_LAUNCH(err, "psell_sell_spmv_dot_alpha");
