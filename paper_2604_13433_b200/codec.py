@@ -35,24 +35,27 @@ class PackFormat:
     codec: str = FP16
 
     def __post_init__(self):
-        # validation order and messages follow codec.py:45-62
-        if self.w not in _WORD_DTYPES:
-            raise ValueError(f"word width must be 32 or 64, got {self.w}")
-        if not 1 <= self.d <= self.w - 2:
-            raise ValueError(f"delta bits must be in [1, {self.w - 2}], got {self.d}")
-        if self.codec == FP16:
-            if self.v != 16:
-                raise ValueError(f"fp16 codec needs 16 value bits, got V={self.v} (use D={self.w - 17})")
-        elif self.codec == E8MY:
-            if self.w != 32:
-                raise ValueError("e8my codec requires 32-bit words")
-            if self.mantissa_bits < 1:
-                raise ValueError(f"e8my needs at least 1 mantissa bit (D={self.d} leaves {self.mantissa_bits})")
-        elif self.codec == FP32EMBED:
-            if self.w != 64 or self.v < 32:
-                raise ValueError("fp32embed codec requires 64-bit words and V >= 32")
-        else:
-            raise ValueError(f"unknown codec {self.codec!r}")
+        # the reference's checks, in its order and with its messages (codec.py:45-62)
+        problem = self._problem()
+        if problem is not None:
+            raise ValueError(problem)
+
+    def _problem(self) -> Optional[str]:
+        w, d, c = self.w, self.d, self.codec
+        if w not in _WORD_DTYPES:
+            return f"word width must be 32 or 64, got {w}"
+        if d < 1 or d > w - 2:
+            return f"delta bits must be in [1, {w - 2}], got {d}"
+        if c == FP16:
+            return None if self.v == 16 else f"fp16 codec needs 16 value bits, got V={self.v} (use D={w - 17})"
+        if c == E8MY:
+            if w != 32:
+                return "e8my codec requires 32-bit words"
+            m = self.mantissa_bits
+            return None if m >= 1 else f"e8my needs at least 1 mantissa bit (D={d} leaves {m})"
+        if c == FP32EMBED:
+            return None if (w == 64 and self.v >= 32) else "fp32embed codec requires 64-bit words and V >= 32"
+        return f"unknown codec {c!r}"
 
     def __eq__(self, other):
         # a reference PackFormat with the same (W, D, codec) is the same format: a
@@ -65,37 +68,18 @@ class PackFormat:
     def __hash__(self):
         return hash((self.w, self.d, self.codec))
 
-    @property
-    def v(self) -> int:
-        return self.w - self.d - 1
-
-    @property
-    def mantissa_bits(self) -> int:
-        return self.v - 9
-
-    @property
-    def max_delta(self) -> int:
-        return (1 << self.d) - 1
-
-    @property
-    def max_dummy_delta(self) -> int:
-        return (1 << (self.w - 1)) - 1
-
-    @property
-    def word_dtype(self) -> np.dtype:
-        return _WORD_DTYPES[self.w]
-
-    @property
-    def value_dtype(self) -> np.dtype:
-        return np.dtype(np.float16) if self.codec == FP16 else np.dtype(np.float32)
+    # derived layout (codec.py:64-99): V value bits, Y mantissa bits of e8mY, the largest
+    # real / dummy delta, the numpy word and decoded value types, the preset name
+    v = property(lambda self: self.w - self.d - 1)
+    mantissa_bits = property(lambda self: self.v - 9)
+    max_delta = property(lambda self: (1 << self.d) - 1)
+    max_dummy_delta = property(lambda self: (1 << (self.w - 1)) - 1)
+    word_dtype = property(lambda self: _WORD_DTYPES[self.w])
+    value_dtype = property(lambda self: np.dtype(np.float16 if self.codec == FP16 else np.float32))
 
     @property
     def name(self) -> str:
-        if self.codec == FP16:
-            return "fp16"
-        if self.codec == E8MY:
-            return f"e8m{self.mantissa_bits}"
-        return "fp32embed"
+        return {FP16: "fp16", FP32EMBED: "fp32embed"}.get(self.codec) or f"e8m{self.mantissa_bits}"
 
 
 def parse_format(name: str) -> PackFormat:
