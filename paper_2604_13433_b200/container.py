@@ -17,22 +17,52 @@ error is raised before the upload.
 
 from __future__ import annotations
 
+import contextlib
 import struct
 from pathlib import Path
-from typing import BinaryIO, Union
+from typing import BinaryIO, NamedTuple, Union
 
 import numpy as np
 
-from .codec import E8MY, FP16, FP32EMBED, PackFormat
+from . import codec as _codec
+from .codec import PackFormat
 from .packed import PackSellMatrix, StorageCounts
-from .sell import perm_dtype
+from .sell import perm_dtype as _perm_dtype
 
 MAGIC = b"PSELL\x00v1"
-_HEADER = struct.Struct("<BBBBIIQQQQQQQ")
-_CODEC_IDS = {FP16: 1, E8MY: 2, FP32EMBED: 3}
-_CODEC_NAMES = {v: k for k, v in _CODEC_IDS.items()}
-_MODE_IDS = {"none": 0, "explicit": 1, "implicit": 2}
-_MODE_NAMES = {v: k for k, v in _MODE_IDS.items()}
+
+
+class _Header(NamedTuple):
+    """The fixed little-endian header after the magic (container.py:27-36): u8 W, D, codec id,
+    mode id; u32 C, sigma; u64 n_rows, n_cols, k_left, nnz, n_dummy, n_padding, n_slices."""
+    w: int
+    d: int
+    codec_id: int
+    mode_id: int
+    c: int
+    sigma: int
+    n_rows: int
+    n_cols: int
+    k_left: int
+    nnz: int
+    n_dummy: int
+    n_pad: int
+    n_slices: int
+
+
+_LAYOUT = struct.Struct("<4B2I7Q")
+_CODECS = (None, _codec.FP16, _codec.E8MY, _codec.FP32EMBED)  # id -> codec (id 0 unused)
+_MODES = ("none", "explicit", "implicit")                       # id -> mode
+
+
+@contextlib.contextmanager
+def _stream(target, mode: str):
+    """A path is opened (and closed) here; a file object is used as is."""
+    if isinstance(target, (str, Path)):
+        with open(target, mode) as f:
+            yield f
+    else:
+        yield target
 
 
 class ContainerError(ValueError):
@@ -63,36 +93,27 @@ def _device_bytes(t, nbytes: int) -> np.ndarray:
 
 def header_bytes(M: PackSellMatrix) -> bytes:
     """Magic + header of M exactly as the reference writes them (container.py:43-48)."""
-    return MAGIC + _HEADER.pack(
-        M.fmt.w, M.fmt.d, _CODEC_IDS[M.fmt.codec], _MODE_IDS[M.mode],
-        M.c, M.sigma, M.n_rows, M.n_cols, M.k_left,
-        M.counts.nnz_real, M.counts.n_dummy, M.counts.n_padding, M.n_slices)
+    h = _Header(M.fmt.w, M.fmt.d, _CODECS.index(M.fmt.codec), _MODES.index(M.mode), M.c, M.sigma, M.n_rows,
+                M.n_cols, M.k_left, M.counts.nnz_real, M.counts.n_dummy, M.counts.n_padding, M.n_slices)
+    return MAGIC + _LAYOUT.pack(*h)
 
 
 def write_psell(M: PackSellMatrix, dest: Union[str, Path, BinaryIO]) -> None:
     """Serialise M (container.py:39-53); identical bytes for identical matrices."""
     if not isinstance(M, PackSellMatrix):
         raise TypeError(f"write_psell expects a PackSellMatrix, got {type(M).__name__}")
-    own = isinstance(dest, (str, Path))
-    f = open(dest, "wb") if own else dest
-    try:
-        f.write(header_bytes(M))
-        # offsets are non-negative int64: their bytes are the reference's '<u8' bytes
-        f.write(np.ascontiguousarray(M.offset, dtype="<i8").tobytes())
-        if M.mode == "implicit":
-            pdt = perm_dtype(M.sigma).newbyteorder("<")
-            if "perm" in M._h and M._h["perm"] is not None:
-                f.write(np.ascontiguousarray(M._h["perm"]).astype(pdt).tobytes())
-            else:
-                f.write(memoryview(_device_bytes(M.d_perm, M.n_rows * pdt.itemsize)))
-        wbytes = M.n_stored * M.fmt.word_dtype.itemsize
-        if "pack" in M._h:
-            f.write(np.ascontiguousarray(M._h["pack"]).astype(M.fmt.word_dtype.newbyteorder("<")).tobytes())
-        else:
-            f.write(memoryview(_device_bytes(M.d_pack, wbytes)))
-    finally:
-        if own:
-            f.close()
+    le_word = M.fmt.word_dtype.newbyteorder("<")
+    sections = [header_bytes(M), np.ascontiguousarray(M.offset, dtype="<i8").tobytes()]  # offsets >= 0: '<u8' bytes
+    if M.mode == "implicit":
+        le_perm = _perm_dtype(M.sigma).newbyteorder("<")
+        host_perm = M._h.get("perm")
+        sections.append(np.ascontiguousarray(host_perm).astype(le_perm).tobytes() if host_perm is not None
+                        else memoryview(_device_bytes(M.d_perm, M.n_rows * le_perm.itemsize)))
+    sections.append(np.ascontiguousarray(M._h["pack"]).astype(le_word).tobytes() if "pack" in M._h
+                    else memoryview(_device_bytes(M.d_pack, M.n_stored * le_word.itemsize)))
+    with _stream(dest, "wb") as f:
+        for part in sections:
+            f.write(part)
 
 
 def _read_exact(f: BinaryIO, n: int, what: str, into: np.ndarray = None):
@@ -121,43 +142,40 @@ def _read_exact(f: BinaryIO, n: int, what: str, into: np.ndarray = None):
 
 
 def read_psell(source: Union[str, Path, BinaryIO]) -> PackSellMatrix:
-    """Parse and validate a .psell container into an HBM-resident PackSellMatrix (container.py:63-103)."""
-    own = isinstance(source, (str, Path))
-    f = open(source, "rb") if own else source
-    try:
+    """Parse and validate a .psell container into an HBM-resident PackSellMatrix (container.py:63-103).
+
+    The reference's checks in its order and words; the arrays land in page-locked
+    buffers and go to HBM in one copy each."""
+    with _stream(source, "rb") as f:
         if _read_exact(f, len(MAGIC), "magic") != MAGIC:
             raise ContainerError("not a .psell container (bad magic)")
-        fields = _HEADER.unpack(_read_exact(f, _HEADER.size, "header"))
-        w, d, codec_id, mode_id, c, sigma, n_rows, n_cols, k_left, nnz, n_dummy, n_pad, n_slices = fields
-        if codec_id not in _CODEC_NAMES:
-            raise ContainerError(f"unknown codec id {codec_id}")
-        if mode_id not in _MODE_NAMES:
-            raise ContainerError(f"unknown mode id {mode_id}")
+        h = _Header(*_LAYOUT.unpack(_read_exact(f, _LAYOUT.size, "header")))
+        if not 1 <= h.codec_id < len(_CODECS):
+            raise ContainerError(f"unknown codec id {h.codec_id}")
+        if h.mode_id >= len(_MODES):
+            raise ContainerError(f"unknown mode id {h.mode_id}")
         try:
-            fmt = PackFormat(w, d, _CODEC_NAMES[codec_id])
+            fmt = PackFormat(h.w, h.d, _CODECS[h.codec_id])
         except ValueError as e:
             raise ContainerError(f"invalid format in header: {e}") from None
-        mode = _MODE_NAMES[mode_id]
-
-        offset = np.frombuffer(_read_exact(f, 8 * (n_slices + 1), "offset array"), dtype="<u8").astype(np.int64)
-        if len(offset) and (offset[0] != 0 or np.any(np.diff(offset) < 0)):
+        mode = _MODES[h.mode_id]
+        raw_off = _read_exact(f, 8 * (h.n_slices + 1), "offset array")
+        offset = np.frombuffer(raw_off, dtype="<u8").astype(np.int64)
+        if offset.size and (offset[0] != 0 or (offset[1:] < offset[:-1]).any()):
             raise ContainerError("offset array is not a non-decreasing prefix starting at 0")
         perm_raw = None
         if mode == "implicit":
-            pdt = perm_dtype(sigma)
-            perm_raw = _read_exact(f, pdt.itemsize * n_rows, "perm array", into=_pinned(pdt.itemsize * n_rows))
-        n_words = int(offset[-1]) if len(offset) else 0
-        _check_device_safe(fmt, c, sigma, mode, n_rows, n_cols, k_left, n_slices, offset, perm_raw)
-        wdt = fmt.word_dtype
-        pack_raw = _read_exact(f, wdt.itemsize * n_words, "pack array", into=_pinned(wdt.itemsize * n_words))
-        if nnz + n_dummy + n_pad != n_words:
-            raise ContainerError(
-                f"header counts ({nnz} + {n_dummy} + {n_pad}) do not sum to the stored word count {n_words}")
-    finally:
-        if own:
-            f.close()
-    M = _upload(n_rows, n_cols, c, sigma, mode, fmt, pack_raw, offset, perm_raw, k_left,
-                StorageCounts(nnz, n_dummy, n_pad))
+            nb = _perm_dtype(h.sigma).itemsize * h.n_rows
+            perm_raw = _read_exact(f, nb, "perm array", into=_pinned(nb))
+        n_words = int(offset[-1]) if offset.size else 0
+        _check_device_safe(fmt, h.c, h.sigma, mode, h.n_rows, h.n_cols, h.k_left, h.n_slices, offset, perm_raw)
+        nb = fmt.word_dtype.itemsize * n_words
+        pack_raw = _read_exact(f, nb, "pack array", into=_pinned(nb))
+        if h.nnz + h.n_dummy + h.n_pad != n_words:
+            raise ContainerError(f"header counts ({h.nnz} + {h.n_dummy} + {h.n_pad}) do not sum to the "
+                                 f"stored word count {n_words}")
+    M = _upload(h.n_rows, h.n_cols, h.c, h.sigma, mode, fmt, pack_raw, offset, perm_raw, h.k_left,
+                StorageCounts(h.nnz, h.n_dummy, h.n_pad))
     _check_stream_columns(M)
     return M
 
@@ -179,7 +197,7 @@ def _check_device_safe(fmt, c, sigma, mode, n_rows, n_cols, k_left, n_slices, of
     if len(offset) and np.any(offset % c):
         raise ContainerError(f"offset array holds a slice start that is not a multiple of C = {c}")
     if perm_raw is not None and n_rows:
-        perm = np.frombuffer(perm_raw, dtype=perm_dtype(sigma)).astype(np.int64)
+        perm = np.frombuffer(perm_raw, dtype=_perm_dtype(sigma)).astype(np.int64)
         lim = np.minimum(sigma, n_rows - (np.arange(n_rows) // sigma) * sigma)
         bad = np.nonzero(perm >= lim)[0]
         if bad.size:
@@ -216,7 +234,7 @@ def _upload(n_rows, n_cols, c, sigma, mode, fmt, pack_raw, offset, perm_raw, k_l
 
     d_pack = up(pack_raw, fmt.word_dtype)
     d_offset = _dev.upload(offset)
-    d_perm = up(perm_raw, perm_dtype(sigma)) if perm_raw is not None else None
+    d_perm = up(perm_raw, _perm_dtype(sigma)) if perm_raw is not None else None
     torch.cuda.current_stream().synchronize()  # staging buffers may be reused by the caller
     return PackSellMatrix(n_rows, n_cols, c, sigma, mode, fmt, d_pack, d_offset, d_perm, k_left, counts)
 
