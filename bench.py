@@ -819,9 +819,14 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # PSELL_SHARE_GPU=1 + PSELL_DIST_BACKEND=gloo: every rank on cuda:0 over gloo, to
     # exercise the multi-rank bench path on a single GPU (the real run uses NCCL)
-    if os.environ.get("PSELL_SHARE_GPU"):
+    # More ranks than visible GPUs (e.g. --gpus 2 on a one-GPU box): the same shared mode,
+    # chosen automatically and labelled in the line, instead of an invalid-device error.
+    shared = bool(os.environ.get("PSELL_SHARE_GPU")) or (world > 1 and world > torch.cuda.device_count())
+    if shared:
         local = 0
-    backend = os.environ.get("PSELL_DIST_BACKEND", "nccl")
+        os.environ.setdefault("PSELL_XPORT", "peer")  # CUDA IPC works between ranks on one GPU
+    backend = os.environ.get("PSELL_DIST_BACKEND", "gloo" if shared and not os.environ.get("PSELL_SHARE_GPU")
+                             else "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -1077,6 +1082,9 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype_label(cfg, "ours"), "data": "synthetic",
             "config": {"workload": cfg["workload"], "n": n, "nnz": int(nnz_all),
+                       **({"shared_gpu": f"{world} ranks on one GPU ({torch.cuda.device_count()} visible): "
+                                         "a functional run of the multi-rank path, not a scaling number"}
+                          if shared and world > 1 else {}),
                        "n_stored_rank0": m_info[0], "counts_rank0": m_info[1], "k_left": kl,
                        "partition": "sigma-aligned row slabs, x replicated (no collective in the step)",
                        "l2": f"inputs larger than L2: {m_info[0] * 4 / 1e9:.2f} GB of packed words stream per "
