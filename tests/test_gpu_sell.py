@@ -139,3 +139,24 @@ def test_iocg_sell32_fused_matches_unfused(monkeypatch):
     r0 = S.iocg(A, b, cfg)
     assert r1.converged and r0.converged and abs(r1.outer_iters - r0.outer_iters) <= 1
     assert np.abs(r1.x - r0.x).max() <= 1e-7 * np.abs(r0.x).max()
+
+
+def test_iocg_sell32_fused_stopping_rules_vs_oracle():
+    """The fused FP32 SELL comparator inside IO-CG (outer look-ahead, gated inner graph)
+    stops where the oracle's IO-CG with an f32 row-sequential SELL inner operator does."""
+    import oracle as O
+    A = P.sym_diag_scale(P.poisson3d(8))
+    b, _ = S.make_rhs_and_x0(A.n_rows, 4)
+    a64 = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, A.values, v, np.float64)  # noqa: E731
+    v32 = A.values.astype(np.float32).astype(np.float64)
+    inner = lambda v: O.csr_spmv(A.row_ptr, A.col_idx, v32, v, np.float32)  # noqa: E731
+    full = O.iocg(a64, inner, b, 1e-9, 200, 10)
+    be = S.make_backend(A, "sell32")
+    for max_outer in (1, 2, full["outer_iters"] - 1, full["outer_iters"], 200):
+        cfg = S.SolveConfig(solver="iocg", tol=1e-9, m_in=10, a_backend="sell32", max_outer=max_outer)
+        r = S.iocg(A, b, cfg, backend=be)
+        ro = O.iocg(a64, inner, b, 1e-9, max_outer, 10)
+        assert (r.converged, r.outer_iters, r.total_inner_iters) == \
+            (ro["converged"], ro["outer_iters"], ro["total_inner_iters"]), max_outer
+        assert np.abs(r.x - ro["x"]).max() <= 1e-6 * np.abs(ro["x"]).max()
+    assert next(iter(be._inner_cache.values())).sell_fused
