@@ -85,6 +85,16 @@ const int32_t* build_ws_order(const psell_desc* d, const void* ws) {
 constexpr long long kLongRow = 64;  // rows longer than this are walked by a whole warp
 
 // grid of the warp-per-long-row kernels: a resident wave (8 CTAs of 8 warps per SM)
+// PSELL_FOLD_KLEFT=0: the separate lower_bandwidth pass before row_stats (A/B)
+static bool fold_k_left() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PSELL_FOLD_KLEFT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static unsigned long_grid() {
   static int sms = 0;
   if (!sms) {
@@ -155,27 +165,42 @@ __global__ void lower_bandwidth_kernel(const int64_t* __restrict__ row_ptr,
 }
 
 // packed.py:145-173 — stored word count per row and the layout error inputs.
+// FOLD (k_left not given): the lower bandwidth is reduced in this same pass (matrix.py:334-339:
+// max over non-empty rows of i - first column, floor 0) instead of a pass of its own over the
+// rows' scattered first columns; only each row's FIRST gap depends on k_left, so this pass
+// counts the inner gaps, records the first column in fcol[], and first_gap_fold_kernel adds
+// the first gaps once k_left is known.  Same counts, sums, minima and maxima.
+template <bool FOLD>
 __global__ void row_stats_kernel(const int64_t* __restrict__ row_ptr,
                                  const int32_t* __restrict__ col_idx, long long n, long long row0,
                                  long long se, int d_bits, BuildStats* st,
-                                 uint32_t* __restrict__ counts, int32_t* __restrict__ long_rows) {
+                                 uint32_t* __restrict__ counts, int32_t* __restrict__ long_rows,
+                                 int32_t* __restrict__ fcol) {
   __shared__ long long sh[32];
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long dum = 0, fg = kI64Max, gmax = kI64Min;
-  const long long k_left = st->k_left;
+  long long dum = 0, fg = kI64Max, gmax = kI64Min, kl = 0;
+  const long long k_left = FOLD ? 0 : st->k_left;
   const long long thr = 1ll << d_bits;
-  long long beg = 0, end = 0;
+  long long beg = 0, end = 0, first = 0;
   if (i < n) {
     beg = row_ptr[i];
     end = row_ptr[i + 1];
-    if (end > beg) fg = (long long)col_idx[beg] - base_of(row0 + i, se, k_left);
+    if (end > beg) {
+      first = col_idx[beg];
+      if (FOLD) {
+        kl = (row0 + i) - first;
+        fcol[i] = (int32_t)first;
+      } else {
+        fg = first - base_of(row0 + i, se, k_left);
+      }
+    }
   }
   // rows longer than kLongRow entries go to row_stats_long_kernel, one warp each
   // (power-law rows: one thread per row left the kernel waiting on its longest row)
   const bool lng = i < n && end - beg > kLongRow;
   if (i < n && !lng) {
-    long long prev = base_of(row0 + i, se, k_left);
-    for (long long j = beg; j < end; ++j) {
+    long long prev = FOLD ? first : base_of(row0 + i, se, k_left);
+    for (long long j = FOLD ? beg + 1 : beg; j < end; ++j) {
       const long long col = col_idx[j];
       const long long gap = col - prev;
       prev = col;
@@ -186,6 +211,55 @@ __global__ void row_stats_kernel(const int64_t* __restrict__ row_ptr,
   }
   if (lng) long_rows[atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_long), 1ull)] = (int32_t)i;
   const long long sd = cta_reduce(dum, AddOp{}, 0ll, sh);
+  const long long sf = FOLD ? kI64Max : cta_reduce(fg, MinOp{}, kI64Max, sh);
+  const long long sg = cta_reduce(gmax, MaxOp{}, kI64Min, sh);
+  const long long sk = FOLD ? cta_reduce(kl, MaxOp{}, 0ll, sh) : 0;
+  if (threadIdx.x == 0) {
+    if (sd) atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_dummy), (unsigned long long)sd);
+    if (sf != kI64Max) atomicMin(&st->min_first_gap, sf);
+    if (sg != kI64Min) atomicMax(&st->max_gap, sg);
+    if (sk > 0) atomicMax(&st->k_left, sk);
+  }
+}
+
+// FOLD: every non-empty row's first gap (first column - Eq. 4 base with the reduced k_left):
+// its dummy added to the row's count and the sum, the minimum first gap, the maximum gap
+__global__ void __launch_bounds__(kBlock) first_gap_fold_kernel(const int64_t* __restrict__ row_ptr,
+                                                                const int32_t* __restrict__ fcol, long long n,
+                                                                long long row0, long long se, int d_bits,
+                                                                BuildStats* st, uint32_t* __restrict__ counts) {
+  // a resident grid-stride grid, 4 rows per trip with their loads issued together: one set of
+  // CTA reductions per CTA (one per 256 rows cost more than the row work)
+  constexpr int R = 4;
+  __shared__ long long sh[32];
+  const long long k_left = st->k_left, thr = 1ll << d_bits;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  long long dum = 0, fg = kI64Max, gmax = kI64Min;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += R * gs) {
+    long long b[R], e[R];
+    int32_t f[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const long long i = i0 + u * gs;
+      b[u] = i < n ? row_ptr[i] : 0;
+      e[u] = i < n ? row_ptr[i + 1] : 0;
+      f[u] = i < n ? fcol[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const long long i = i0 + u * gs;
+      if (e[u] > b[u]) {
+        const long long g = (long long)f[u] - base_of(row0 + i, se, k_left);
+        fg = g < fg ? g : fg;
+        gmax = g > gmax ? g : gmax;
+        if (g >= thr) {
+          ++dum;
+          counts[i] += 1u;
+        }
+      }
+    }
+  }
+  const long long sd = cta_reduce(dum, AddOp{}, 0ll, sh);
   const long long sf = cta_reduce(fg, MinOp{}, kI64Max, sh);
   const long long sg = cta_reduce(gmax, MaxOp{}, kI64Min, sh);
   if (threadIdx.x == 0) {
@@ -195,7 +269,7 @@ __global__ void row_stats_kernel(const int64_t* __restrict__ row_ptr,
   }
 }
 
-// row_stats for the listed long rows: one warp per row, 32 entries per trip
+template <bool FOLD>
 __global__ void __launch_bounds__(kBlock) row_stats_long_kernel(const int64_t* __restrict__ row_ptr,
                                                                 const int32_t* __restrict__ col_idx,
                                                                 long long row0, long long se, int d_bits,
@@ -203,7 +277,7 @@ __global__ void __launch_bounds__(kBlock) row_stats_long_kernel(const int64_t* _
                                                                 const int32_t* __restrict__ long_rows) {
   __shared__ long long sh[32];
   const long long nl = st->n_long;
-  const long long k_left = st->k_left;
+  const long long k_left = FOLD ? 0 : st->k_left;
   const long long thr = 1ll << d_bits;
   const int lane = threadIdx.x & 31;
   long long dum = 0, gmax = kI64Min;
@@ -211,9 +285,9 @@ __global__ void __launch_bounds__(kBlock) row_stats_long_kernel(const int64_t* _
        w += (long long)gridDim.x * (kBlock / 32)) {
     const long long ri = long_rows[w];
     const long long rb = row_ptr[ri], re = row_ptr[ri + 1];
-    const long long d0 = base_of(row0 + ri, se, k_left);
+    const long long d0 = FOLD ? 0 : base_of(row0 + ri, se, k_left);
     long long cnt = 0;
-    for (long long j = rb + lane; j < re; j += 32) {
+    for (long long j = rb + lane + (FOLD ? 1 : 0); j < re; j += 32) {  // FOLD: first gap in first_gap_fold
       const long long col = col_idx[j];
       const long long gap = col - (j == rb ? d0 : (long long)col_idx[j - 1]);
       cnt += gap >= thr;
@@ -688,12 +762,23 @@ int psell_build_plan(const psell_desc* d, const int64_t* row_ptr, const int32_t*
 
   init_stats_kernel<<<1, 1, 0, st>>>(w.stats, d->k_left);
   if (n > 0) {
-    if (d->k_left < 0)
-      lower_bandwidth_kernel<<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, w.stats);
-    row_stats_kernel<<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, se, d->d,
-                                                   w.stats, w.counts, w.long_rows);
-    row_stats_long_kernel<<<long_grid(), kBlock, 0, st>>>(row_ptr, col_idx, d->row0, se, d->d, w.stats,
-                                                          w.counts, w.long_rows);
+    if (d->k_left < 0 && fold_k_left()) {
+      // w.scount is free until the sort (which writes every entry): the rows' first columns
+      int32_t* fcol = reinterpret_cast<int32_t*>(w.scount);
+      row_stats_kernel<true><<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, se, d->d, w.stats,
+                                                           w.counts, w.long_rows, fcol);
+      row_stats_long_kernel<true><<<long_grid(), kBlock, 0, st>>>(row_ptr, col_idx, d->row0, se, d->d, w.stats,
+                                                                  w.counts, w.long_rows);
+      first_gap_fold_kernel<<<grid_rows < long_grid() ? grid_rows : long_grid(), kBlock, 0, st>>>(
+          row_ptr, fcol, n, d->row0, se, d->d, w.stats, w.counts);
+    } else {
+      if (d->k_left < 0)
+        lower_bandwidth_kernel<<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, w.stats);
+      row_stats_kernel<false><<<grid_rows, kBlock, 0, st>>>(row_ptr, col_idx, n, d->row0, se, d->d, w.stats,
+                                                            w.counts, w.long_rows, nullptr);
+      row_stats_long_kernel<false><<<long_grid(), kBlock, 0, st>>>(row_ptr, col_idx, d->row0, se, d->d,
+                                                                   w.stats, w.counts, w.long_rows);
+    }
   }
   PSELL_CHECK_LAUNCH(err, "row_stats");
   BuildStats hs;
