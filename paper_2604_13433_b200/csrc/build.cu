@@ -319,17 +319,22 @@ __global__ void first_gap_row_kernel(const int64_t* __restrict__ row_ptr,
 
 // sell.py:22-30 — stable descending sort of stored counts inside each sigma
 // block (the last partial block alone).  LSD radix on key = max - count.
-template <int NT>
+// RB-bit digits: 8 for the 256-thread kernel (sigma <= 256: the stencils' counts need <= 8 bits,
+// one pass), 4 for the 1024-thread one (a 256-bucket warp table would be 32 KB there)
+template <int NT, int RB = (NT == 256 ? 8 : 4)>
 __global__ void __launch_bounds__(NT) sort_blocks_kernel(const uint32_t* __restrict__ counts,
                                                          long long n, int sigma,
                                                          int32_t* __restrict__ order,
                                                          uint32_t* __restrict__ scount,
                                                          void* perm, int perm_bytes,
                                                          uint32_t* gscratch) {
+  constexpr int NB = 1 << RB;
+  static_assert(NB <= 16 || NB == NT, "wide digits scan one bucket per thread");
   extern __shared__ uint32_t dyn[];
-  __shared__ int hist[16];
-  __shared__ int wcnt[NT / 32][16];
+  __shared__ int hist[NB];
+  __shared__ int wcnt[NT / 32][NB];
   __shared__ uint32_t s_red[NT / 32];
+  __shared__ int s_wtot[NT / 32];
   const long long b0 = (long long)blockIdx.x * sigma;
   const int len = (int)min((long long)sigma, n - b0);
   uint32_t *ka, *ia, *kb, *ib;
@@ -365,32 +370,47 @@ __global__ void __launch_bounds__(NT) sort_blocks_kernel(const uint32_t* __restr
   const int bits = smax ? 32 - __clz(smax) : 0;
   const unsigned lt = (1u << lane) - 1u;
   __syncthreads();
-  for (int sh = 0; sh < bits; sh += 4) {
-    if (tid < 16) hist[tid] = 0;
+  for (int sh = 0; sh < bits; sh += RB) {
+    if (tid < NB) hist[tid] = 0;
     __syncthreads();
-    for (int i = tid; i < len; i += NT) atomicAdd(&hist[(ka[i] >> sh) & 15], 1);
+    for (int i = tid; i < len; i += NT) atomicAdd(&hist[(ka[i] >> sh) & (NB - 1)], 1);
     __syncthreads();
-    if (tid == 0) {
-      int run = 0;
-      for (int dg = 0; dg < 16; ++dg) {
-        const int t = hist[dg];
-        hist[dg] = run;
-        run += t;
+    if constexpr (NB <= 16) {
+      if (tid == 0) {
+        int run = 0;
+        for (int dg = 0; dg < NB; ++dg) {
+          const int t = hist[dg];
+          hist[dg] = run;
+          run += t;
+        }
       }
+    } else {  // exclusive scan of NB == NT buckets, one per thread
+      const int h = hist[tid];
+      int inc = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (lane == 31) s_wtot[warp] = inc;
+      __syncthreads();
+      int before = 0;
+      for (int w2 = 0; w2 < warp; ++w2) before += s_wtot[w2];
+      hist[tid] = before + inc - h;
     }
     __syncthreads();
     for (int t0 = 0; t0 < len; t0 += NT) {
       const int i = t0 + tid;
       const bool valid = i < len;
       const uint32_t key = valid ? ka[i] : 0u;
-      const int dg = valid ? (int)((key >> sh) & 15) : 16;
+      const int dg = valid ? (int)((key >> sh) & (NB - 1)) : NB;
       const unsigned m = __match_any_sync(0xffffffffu, dg);
       const int rank = __popc(m & lt);
-      for (int e = tid; e < (NT / 32) * 16; e += NT) (&wcnt[0][0])[e] = 0;
+      for (int e = tid; e < (NT / 32) * NB; e += NT) (&wcnt[0][0])[e] = 0;
       __syncthreads();
       if (valid && rank == 0) wcnt[warp][dg] = __popc(m);
       __syncthreads();
-      if (tid < 16) {
+      if (tid < NB) {
         int run = hist[tid];
         for (int w = 0; w < NT / 32; ++w) {
           const int t = wcnt[w][tid];
