@@ -584,7 +584,9 @@ __global__ void __launch_bounds__(kBlock, PSELL_FILL_MINB) fill_kernel(FillArgs 
   // rows longer than kLongRow entries are listed for fill_long_kernel (one warp each)
   bool lng = false;
   if (s < a.n_slices * a.c) {
-    const long long k = s / a.c;
+    // 32-bit divisions when the sizes allow (the 64-bit ones cost ~2x a row's encode work)
+    const bool n32 = a.n_slices * a.c < (1ll << 31);
+    const long long k = n32 ? (long long)((uint32_t)s / (uint32_t)a.c) : s / a.c;
     const int lane = (int)(s - k * a.c);
     const long long o = a.offset[k];
     const long long width = (a.offset[k + 1] - o) / a.c;
@@ -595,7 +597,8 @@ __global__ void __launch_bounds__(kBlock, PSELL_FILL_MINB) fill_kernel(FillArgs 
       const long long beg = a.row_ptr[r], end = a.row_ptr[r + 1];
       long long prev = [&] {
         const long long g = a.row0 + r;
-        const long long blk = (g / a.se) * a.se;
+        const long long blk = (g < (1ll << 32) && a.se < (1ll << 32))
+                                  ? (long long)((uint32_t)g / (uint32_t)a.se) * a.se : (g / a.se) * a.se;
         return blk > a.k_left ? blk - a.k_left : 0ll;
       }();
       lng = end - beg > kLongRow;
@@ -636,6 +639,8 @@ __global__ void __launch_bounds__(kBlock, PSELL_FILL_MINB) fill_kernel(FillArgs 
       for (; q < width; ++q) out[q * stride] = W(0);
   }
   if (lng) a.long_rows[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->n_long), 1ull)] = (int32_t)s;
+  // the error reductions only in a CTA that saw a non-finite or overflowing value
+  if (!__syncthreads_or(bad_nf != kI64Max || bad_of != kI64Max)) return;
   const long long m1 = cta_reduce(bad_nf, MinOp{}, kI64Max, sh);
   const long long m2 = cta_reduce(bad_of, MinOp{}, kI64Max, sh);
   if (threadIdx.x == 0) {
