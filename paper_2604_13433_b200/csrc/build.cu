@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(NT) sort_blocks_kernel(const uint32_t* __restr
                                                          void* perm, int perm_bytes,
                                                          uint32_t* gscratch) {
   constexpr int NB = 1 << RB;
-  static_assert(NB <= 16 || NB == NT, "wide digits scan one bucket per thread");
+  static_assert(NB <= 16 || (NB % 32 == 0 && NB <= NT), "wide digits scan one bucket per thread");
   extern __shared__ uint32_t dyn[];
   __shared__ int hist[NB];
   __shared__ int wcnt[NT / 32][NB];
@@ -384,19 +384,24 @@ __global__ void __launch_bounds__(NT) sort_blocks_kernel(const uint32_t* __restr
           run += t;
         }
       }
-    } else {  // exclusive scan of NB == NT buckets, one per thread
-      const int h = hist[tid];
-      int inc = h;
+    } else {  // exclusive scan of the NB buckets, one per thread of the first NB / 32 warps
+      int h = 0, inc = 0;
+      if (tid < NB) {  // whole warps (NB is a multiple of 32)
+        h = hist[tid];
+        inc = h;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (lane == 31) s_wtot[warp] = inc;
       }
-      if (lane == 31) s_wtot[warp] = inc;
       __syncthreads();
-      int before = 0;
-      for (int w2 = 0; w2 < warp; ++w2) before += s_wtot[w2];
-      hist[tid] = before + inc - h;
+      if (tid < NB) {
+        int before = 0;
+        for (int w2 = 0; w2 < warp; ++w2) before += s_wtot[w2];
+        hist[tid] = before + inc - h;
+      }
     }
     __syncthreads();
     for (int t0 = 0; t0 < len; t0 += NT) {
@@ -839,8 +844,9 @@ int psell_build_plan(const psell_desc* d, const int64_t* row_ptr, const int32_t*
         sort_blocks_kernel<1024><<<nblk, 1024, smem, st>>>(w.counts, n, d->sigma, w.order, w.scount,
                                                            perm, perm_bytes, nullptr);
     } else {
-      sort_blocks_kernel<1024><<<nblk, 1024, 0, st>>>(w.counts, n, d->sigma, w.order, w.scount,
-                                                      perm, perm_bytes, w.sort_tmp);
+      // keys in global scratch: the 8-bit digit table fits beside them (fewer passes)
+      sort_blocks_kernel<1024, 8><<<nblk, 1024, 0, st>>>(w.counts, n, d->sigma, w.order, w.scount,
+                                                         perm, perm_bytes, w.sort_tmp);
     }
     PSELL_CHECK_LAUNCH(err, "sort_blocks");
     scount = w.scount;
@@ -933,7 +939,7 @@ int psell_sort_order(const uint32_t* counts, int64_t n, int32_t sigma, int32_t* 
   else if (sigma <= kSortSmemMaxSigma)
     sort_blocks_kernel<1024><<<nblk, 1024, 16 * (size_t)sigma, st>>>(counts, n, sigma, order, scount, nullptr, 0, nullptr);
   else
-    sort_blocks_kernel<1024><<<nblk, 1024, 0, st>>>(counts, n, sigma, order, scount, nullptr, 0, tmp);
+    sort_blocks_kernel<1024, 8><<<nblk, 1024, 0, st>>>(counts, n, sigma, order, scount, nullptr, 0, tmp);
   PSELL_CHECK_LAUNCH(err, "psell_sort_order");
   return ok(err);
 }
